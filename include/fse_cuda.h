@@ -1,0 +1,169 @@
+/*
+ * fse_cuda.h -- C-ABI of the B200-native free-space Spectral Ewald library
+ * (libfse_b200.so).  Plain pointers, sizes and PODs; no C++ or torch types.
+ *
+ * This is the drop-in boundary for the reference's hot path,
+ * fse::total_sum (/root/reference/proj/src/ewald.cpp:394-415) and the
+ * functions under it.  Each entry point names the reference interface it
+ * replaces.  The C++ wrapper (paper_1607_04808_b200/cpp/include/fse/*.hpp,
+ * namespace fse) re-exposes the reference's C++ signatures over this ABI.
+ *
+ * Conventions
+ *   - positions / targets: N x 3 doubles, AoS (x,y,z), like std::vector<fse::Vec3>
+ *     (vec3.hpp:8-17);
+ *   - strengths: N x a doubles, a = fse_arity(kind) (3, or 9 for the stresslet with
+ *     f_lm at 3l+m), i.e. the first `arity` slots of fse::Strength::c (kernels.hpp:25-56);
+ *   - velocities: NT x 3 doubles;
+ *   - kinds: FSE_STOKESLET / FSE_STRESSLET / FSE_ROTLET (kernels.hpp:16 order);
+ *   - every call returns an fse_status; FSE_EINVAL maps to std::invalid_argument,
+ *     FSE_EDOMAIN to std::domain_error, the rest to std::runtime_error.
+ *     fse_cuda_last_error(ctx) holds the message (per context, per thread).
+ *   - calls are blocking (results are complete on return) and thread-safe per
+ *     context (one mutex per context); use one context per host thread for
+ *     concurrency, as the reference allows concurrent calls.
+ *   - "_dev" variants take device pointers on the context's device and do no
+ *     host<->device copies.
+ */
+#ifndef FSE_CUDA_H
+#define FSE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSE_CUDA_ABI_VERSION 1
+
+typedef enum {
+    FSE_OK = 0,
+    FSE_EINVAL = 1,   /* std::invalid_argument */
+    FSE_EDOMAIN = 2,  /* std::domain_error */
+    FSE_ERUNTIME = 3, /* std::runtime_error (I/O) */
+    FSE_ECUDA = 4,
+    FSE_ECUFFT = 5,
+    FSE_ENOMEM = 6,
+    FSE_ENCCL = 7
+} fse_status;
+
+typedef enum { FSE_STOKESLET = 0, FSE_STRESSLET = 1, FSE_ROTLET = 2 } fse_kernel_kind;
+typedef enum { FSE_HARMONIC = 0, FSE_BIHARMONIC = 1 } fse_green_kind;
+
+/* Bitwise mirror of fse::EwaldConfig (ewald.hpp:16-35), 120 bytes. */
+typedef struct {
+    double L, xi, rc;
+    int32_t M, P;
+    double h, d, m, eta, deltaL, Ltilde;
+    int32_t Mtilde;
+    int32_t _pad0;
+    double kinf, R, sf;
+    uint8_t deterministic;
+    uint8_t _pad1[7];
+} fse_config;
+
+/* Mirror of fse::StageTimings (ewald.hpp:56-64), seconds; calls ACCUMULATE (+=). */
+typedef struct {
+    double precompute, spread, fft, scale, quadrature, realspace, total;
+} fse_timings;
+
+typedef struct fse_cuda_ctx fse_cuda_ctx;
+typedef struct fse_green fse_green; /* device-resident MollifiedGreen */
+
+/* ---- context ------------------------------------------------------------ */
+fse_status fse_cuda_create(int device, fse_cuda_ctx** out);
+void fse_cuda_destroy(fse_cuda_ctx* ctx);
+const char* fse_cuda_last_error(const fse_cuda_ctx* ctx);
+int fse_cuda_abi_version(void);
+int fse_arity(int kind);
+/* release cached device buffers and FFT plans (the context stays usable) */
+fse_status fse_cuda_trim(fse_cuda_ctx* ctx);
+/* pinned host memory for fast copies (optional) */
+fse_status fse_cuda_host_alloc(fse_cuda_ctx* ctx, size_t bytes, void** out);
+void fse_cuda_host_free(void* p);
+/* device memory on the context's device (for the _dev entry points) */
+fse_status fse_cuda_dev_alloc(fse_cuda_ctx* ctx, size_t bytes, void** out);
+void fse_cuda_dev_free(fse_cuda_ctx* ctx, void* p);
+fse_status fse_cuda_memcpy(fse_cuda_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* device time (ms) between the last two fse_cuda_mark() calls on the context stream */
+fse_status fse_cuda_mark(fse_cuda_ctx* ctx);
+fse_status fse_cuda_elapsed_ms(fse_cuda_ctx* ctx, double* ms);
+/* number of kernels this library launched on the context since creation */
+uint64_t fse_cuda_launch_count(const fse_cuda_ctx* ctx);
+
+/* ---- config: replaces fse::make_config (ewald.cpp:103-134) -------------- */
+fse_status fse_make_config(double L, double xi, double rc, int M, int P, double sf,
+                           fse_config* out, char* err, size_t errlen);
+
+/* ---- Green's function: replaces fse::precompute_mollified_green
+ *      (greens.cpp:48-113), computed on the GPU ---------------------------- */
+fse_status fse_cuda_green_precompute(fse_cuda_ctx* ctx, int green_kind, double Ltilde,
+                                     int Mtilde, double sf, fse_green** out);
+/* upload a host table in the reference layout: (2 Mtilde)^3 doubles, standard FFT order */
+fse_status fse_cuda_green_upload(fse_cuda_ctx* ctx, int green_kind, double Ltilde,
+                                 int Mtilde, double h, double R, const double* fourier_full,
+                                 fse_green** out);
+/* download the full (2 Mtilde)^3 table (reference layout) */
+fse_status fse_cuda_green_download(fse_cuda_ctx* ctx, const fse_green* g, double* fourier_full);
+/* kind, Ltilde, h, R, Mtilde */
+fse_status fse_cuda_green_info(const fse_green* g, int* green_kind, double* Ltilde, double* h,
+                               double* R, int* Mtilde);
+void fse_cuda_green_free(fse_green* g);
+/* FSEG binary cache (greens.cpp:141-203): same on-disk format */
+fse_status fse_cuda_green_save(fse_cuda_ctx* ctx, const fse_green* g, const char* path);
+fse_status fse_cuda_green_load(fse_cuda_ctx* ctx, const char* path, fse_green** out);
+
+/* ---- hot path ----------------------------------------------------------- */
+/* replaces fse::total_sum (ewald.cpp:394-415).  targets_are_sources: -1 detect
+ * by value (std::equal, ewald.cpp:405-407), 0 no, 1 yes. */
+fse_status fse_cuda_total_sum(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                              const double* pos, const double* str, int64_t n,
+                              double box_side, const double* targets, int64_t nt,
+                              int targets_are_sources, const fse_green* green, double* u,
+                              fse_timings* timings);
+fse_status fse_cuda_total_sum_dev(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                  const double* d_pos, const double* d_str, int64_t n,
+                                  double box_side, const double* d_targets, int64_t nt,
+                                  int targets_are_sources, const fse_green* green, double* d_u,
+                                  fse_timings* timings);
+/* replaces fse::fourier_sum (ewald.cpp:295-392) */
+fse_status fse_cuda_fourier_sum(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                const double* pos, const double* str, int64_t n,
+                                double box_side, const double* targets, int64_t nt,
+                                const fse_green* green, double* u, fse_timings* timings);
+/* replaces fse::real_space_sum (realspace.cpp:86-149) */
+fse_status fse_cuda_real_space_sum(fse_cuda_ctx* ctx, int kind, const double* pos,
+                                   const double* str, int64_t n, double box_side, double xi,
+                                   double rc, const double* targets, int64_t nt, double* u);
+/* replaces fse::spread (ewald.cpp:136-214): grid = a planes of Mtilde^3 */
+fse_status fse_cuda_spread(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                           const double* pos, const double* str, int64_t n, double box_side,
+                           double* grid);
+/* replaces fse::kspace_scale (ewald.cpp:216-293) on full D^3 interleaved complex
+ * planes: ghat a planes in, 3 planes out (D = 2 Mtilde) */
+fse_status fse_cuda_kspace_scale(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                 const fse_green* green, const double* ghat, double* out);
+/* replaces fse::build_cell_list (realspace.cpp:65-84) plus the bucket-contiguous
+ * order of realspace.cpp:95-109.  Call with bstart == NULL to get dims first;
+ * bstart has dims^3 + 1 entries, perm n entries (source indices, ascending per bucket). */
+fse_status fse_cuda_build_cell_list(fse_cuda_ctx* ctx, const double* pos, int64_t n,
+                                    double box_side, double rc, double domain_pad, int* dims,
+                                    double* cell_side, double* origin, int64_t* bstart,
+                                    int64_t* perm);
+/* per-point support start indices i0 (ewald.cpp:33-51), n x 3 ints; FSE_EINVAL
+ * if a support leaves the grid (ewald.cpp:87-91) */
+fse_status fse_cuda_support_index(fse_cuda_ctx* ctx, const fse_config* cfg, const double* pos,
+                                  int64_t n, int32_t* i0);
+/* replaces fse::direct_sum (kernels.cpp:59-82), O(N NT) on the GPU */
+fse_status fse_cuda_direct_sum(fse_cuda_ctx* ctx, int kind, const double* pos,
+                               const double* str, int64_t n, const double* targets, int64_t nt,
+                               int exclude_self, double* u);
+/* the FFT seam (fft.hpp:11,14): in-place 3D C2C on interleaved complex host data;
+ * inverse scales by 1/(n0 n1 n2) */
+fse_status fse_cuda_fft3d(fse_cuda_ctx* ctx, double* data, int n0, int n1, int n2, int inverse);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSE_CUDA_H */

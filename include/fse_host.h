@@ -1,0 +1,38 @@
+/*
+ * fse_host.h -- host-only helpers exported by libfse_b200.so (not on the GPU
+ * hot path): deterministic input generators.
+ */
+#ifndef FSE_HOST_H
+#define FSE_HOST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Replaces fse::generate_system (harness.cpp:47-66): std::mt19937_64(seed),
+ * u = (rng() >> 11) 2^-53; all positions L*u first, then strengths 2u-1.
+ * kind 1 (stresslet) draws 9 components per point, else 3.  Returns 0 on success. */
+int fse_generate_system(int kind, int64_t n, double L, uint64_t seed, double* pos, double* str);
+
+/* SURVEY.md 8(d) workload generators, unit box, std::mt19937_64(seed),
+ * normals by Box-Muller (u1 = ((rng()>>11)+1) 2^-53):
+ *   FSE_WL_UNIFORM          positions U[0,1)^3, then N(0,1) 3-vector strengths (cfg1, cfg2)
+ *   FSE_WL_SPHERE           sphere radius 0.5 about the box centre, f = n q^T, q ~ N(0,1)^3 (cfg3)
+ *   FSE_WL_CLUSTERED        32 blobs, sigma 0.03, clamped to [0, 1) (cfg4)
+ *   FSE_WL_UNIFORM_TARGETS  as UNIFORM plus n distinct U[0,1)^3 targets (cfg5) */
+enum {
+    FSE_WL_UNIFORM = 1,
+    FSE_WL_SPHERE = 3,
+    FSE_WL_CLUSTERED = 4,
+    FSE_WL_UNIFORM_TARGETS = 5
+};
+int fse_generate_workload(int which, int64_t n, uint64_t seed, double* pos, double* str,
+                          double* tgt);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

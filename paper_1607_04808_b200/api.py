@@ -1,0 +1,589 @@
+"""Python mirror of the reference's fse:: hot-path API over the C-ABI.
+
+Names, argument order, argument meaning and error behaviour follow the
+reference C++ library (/root/reference/proj/include/fse/*.hpp):
+
+    make_config(L, xi, rc, M, P, sf=0)                      ewald.hpp:37
+    precompute_mollified_green(kind, Ltilde, Mtilde, sf)     greens.hpp:71-72
+    spread(system, cfg, kind)                                ewald.hpp:45-46
+    kspace_scale(ghat, cfg, kind, green)                     ewald.hpp:51-53
+    fourier_sum(system, cfg, kind, targets, green, timings)  ewald.hpp:69-71
+    total_sum(system, kind, cfg, targets, green, timings)    ewald.hpp:75-77
+    real_space_sum(system, kind, xi, rc, targets)            realspace.hpp:35-36
+    build_cell_list(system, rc, domain_pad=0)                realspace.hpp:31
+    direct_sum(system, kind, targets, exclude_self)          kernels.hpp:78-79
+    fft3d_forward / fft3d_inverse                            fft.hpp:11,14
+    save_mollified_green / load_mollified_green              greens.hpp:79-80
+
+std::invalid_argument -> InvalidArgument (a ValueError), std::domain_error ->
+DomainError (an ArithmeticError), everything else -> FseRuntimeError.
+
+All computation runs in libfse_b200.so on the GPU (sm_100a); there is no CPU
+fallback: importing this module without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfse_b200.so")
+
+
+class FseError(Exception):
+    pass
+
+
+class InvalidArgument(FseError, ValueError):
+    """std::invalid_argument"""
+
+
+class DomainError(FseError, ArithmeticError):
+    """std::domain_error"""
+
+
+class FseRuntimeError(FseError, RuntimeError):
+    """std::runtime_error (I/O) and CUDA / cuFFT / allocation failures"""
+
+
+class KernelKind(enum.IntEnum):  # kernels.hpp:16
+    Stokeslet = 0
+    Stresslet = 1
+    Rotlet = 2
+
+
+class GreenKind(enum.IntEnum):  # greens.hpp:19
+    Harmonic = 0
+    Biharmonic = 1
+
+
+def strength_arity(kind) -> int:  # kernels.hpp:19-21
+    return 9 if int(kind) == KernelKind.Stresslet else 3
+
+
+def green_kind_for(kind) -> GreenKind:  # ewald.hpp:80-82
+    return GreenKind.Harmonic if int(kind) == KernelKind.Rotlet else GreenKind.Biharmonic
+
+
+class EwaldConfig(C.Structure):
+    """Bitwise mirror of fse::EwaldConfig (ewald.hpp:16-35) / fse_config."""
+
+    _fields_ = [("L", C.c_double), ("xi", C.c_double), ("rc", C.c_double), ("M", C.c_int32),
+                ("P", C.c_int32), ("h", C.c_double), ("d", C.c_double), ("m", C.c_double),
+                ("eta", C.c_double), ("deltaL", C.c_double), ("Ltilde", C.c_double),
+                ("Mtilde", C.c_int32), ("_pad0", C.c_int32), ("kinf", C.c_double),
+                ("R", C.c_double), ("sf", C.c_double), ("deterministic", C.c_uint8),
+                ("_pad1", C.c_uint8 * 7)]
+
+    @property
+    def D(self) -> int:
+        return 2 * self.Mtilde
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+
+    def __repr__(self):
+        return "EwaldConfig(" + ", ".join(f"{k}={v!r}" for k, v in self.as_dict().items()) + ")"
+
+
+assert C.sizeof(EwaldConfig) == 120
+
+
+class StageTimings(C.Structure):
+    """Mirror of fse::StageTimings (ewald.hpp:56-64), seconds; calls accumulate."""
+
+    _fields_ = [(k, C.c_double) for k in
+                ("precompute", "spread", "fft", "scale", "quadrature", "realspace", "total")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+@dataclass
+class SourceSystem:
+    """fse::SourceSystem (kernels.hpp:59-66): positions (N,3), strengths (N,a)."""
+
+    positions: np.ndarray
+    strengths: np.ndarray
+    box_side: float = 1.0
+
+    def __post_init__(self):
+        self.positions = np.ascontiguousarray(self.positions, dtype=np.float64).reshape(-1, 3)
+        s = np.ascontiguousarray(self.strengths, dtype=np.float64)
+        self.strengths = s.reshape(self.positions.shape[0], -1) if s.size else s.reshape(0, 3)
+
+    def size(self) -> int:
+        return self.positions.shape[0]
+
+
+@dataclass
+class CellList:
+    """fse::CellList (realspace.hpp:14-24) in bucket-contiguous form:
+    bucket b holds perm[bstart[b]:bstart[b+1]] (ascending source indices)."""
+
+    cell_side: float
+    origin: float
+    dims: tuple
+    bstart: np.ndarray
+    perm: np.ndarray
+
+    @property
+    def buckets(self):
+        return [self.perm[self.bstart[b]:self.bstart[b + 1]].tolist()
+                for b in range(len(self.bstart) - 1)]
+
+    def cell_of(self, coord: float, axis: int) -> int:  # realspace.cpp:60-63
+        c = int(np.floor((coord - self.origin) / self.cell_side))
+        return min(max(c, 0), self.dims[axis] - 1)
+
+
+# --------------------------------------------------------------------- library
+_dp = C.POINTER(C.c_double)
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback)")
+        lib = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        i64 = C.c_int64
+        lib.fse_cuda_last_error.restype = C.c_char_p
+        lib.fse_cuda_last_error.argtypes = [vp]
+        lib.fse_cuda_create.argtypes = [C.c_int, C.POINTER(vp)]
+        lib.fse_cuda_destroy.argtypes = [vp]
+        lib.fse_cuda_launch_count.restype = C.c_uint64
+        lib.fse_cuda_launch_count.argtypes = [vp]
+        lib.fse_make_config.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                        C.c_double, C.POINTER(EwaldConfig), C.c_char_p, C.c_size_t]
+        lib.fse_cuda_green_precompute.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_double,
+                                                  C.POINTER(vp)]
+        lib.fse_cuda_green_upload.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_double,
+                                              C.c_double, _dp, C.POINTER(vp)]
+        lib.fse_cuda_green_download.argtypes = [vp, vp, _dp]
+        lib.fse_cuda_green_info.argtypes = [vp, C.POINTER(C.c_int), _dp, _dp, _dp,
+                                            C.POINTER(C.c_int)]
+        lib.fse_cuda_green_free.argtypes = [vp]
+        lib.fse_cuda_green_save.argtypes = [vp, vp, C.c_char_p]
+        lib.fse_cuda_green_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+        lib.fse_cuda_total_sum.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
+                                           C.c_double, _dp, i64, C.c_int, vp, _dp,
+                                           C.POINTER(StageTimings)]
+        lib.fse_cuda_total_sum_dev.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
+                                               C.c_double, vp, i64, C.c_int, vp, vp,
+                                               C.POINTER(StageTimings)]
+        lib.fse_cuda_fourier_sum.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
+                                             C.c_double, _dp, i64, vp, _dp,
+                                             C.POINTER(StageTimings)]
+        lib.fse_cuda_real_space_sum.argtypes = [vp, C.c_int, _dp, _dp, i64, C.c_double,
+                                                C.c_double, C.c_double, _dp, i64, _dp]
+        lib.fse_cuda_spread.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
+                                        C.c_double, _dp]
+        lib.fse_cuda_kspace_scale.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, _dp, _dp]
+        lib.fse_cuda_build_cell_list.argtypes = [vp, _dp, i64, C.c_double, C.c_double,
+                                                 C.c_double, C.POINTER(C.c_int), _dp, _dp,
+                                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        lib.fse_cuda_support_index.argtypes = [vp, C.POINTER(EwaldConfig), _dp, i64,
+                                               C.POINTER(C.c_int32)]
+        lib.fse_cuda_direct_sum.argtypes = [vp, C.c_int, _dp, _dp, i64, _dp, i64, C.c_int, _dp]
+        lib.fse_cuda_fft3d.argtypes = [vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int]
+        lib.fse_cuda_host_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
+        lib.fse_cuda_host_free.argtypes = [vp]
+        lib.fse_cuda_dev_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
+        lib.fse_cuda_dev_free.argtypes = [vp, vp]
+        lib.fse_cuda_memcpy.argtypes = [vp, vp, vp, C.c_size_t]
+        lib.fse_cuda_mark.argtypes = [vp]
+        lib.fse_cuda_elapsed_ms.argtypes = [vp, _dp]
+        lib.fse_cuda_trim.argtypes = [vp]
+        lib.fse_generate_system.argtypes = [C.c_int, i64, C.c_double, C.c_uint64, _dp, _dp]
+        lib.fse_generate_workload.argtypes = [C.c_int, i64, C.c_uint64, _dp, _dp, _dp]
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _load()
+
+
+_ERRORS = {1: InvalidArgument, 2: DomainError}
+
+
+def _raise(status: int, msg: str):
+    raise _ERRORS.get(status, FseRuntimeError)(f"[fse status {status}] {msg}")
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+# ------------------------------------------------------------------ config
+def make_config(L, xi, rc, M, P, sf=0.0) -> EwaldConfig:
+    cfg = EwaldConfig()
+    err = C.create_string_buffer(256)
+    st = _load().fse_make_config(float(L), float(xi), float(rc), int(M), int(P), float(sf),
+                                 C.byref(cfg), err, 256)
+    if st:
+        _raise(st, err.value.decode())
+    return cfg
+
+
+# ------------------------------------------------------------------ context
+class MollifiedGreen:
+    """Device-resident fse::MollifiedGreen (greens.hpp:57-66).  `fourier`
+    downloads the (2 Mtilde)^3 table in the reference layout."""
+
+    def __init__(self, ctx: "Context", handle):
+        self._ctx = ctx
+        self._h = handle
+        k, lt, h, R, mt = C.c_int(), C.c_double(), C.c_double(), C.c_double(), C.c_int()
+        _load().fse_cuda_green_info(handle, C.byref(k), C.byref(lt), C.byref(h), C.byref(R),
+                                    C.byref(mt))
+        self.kind = GreenKind(k.value)
+        self.Ltilde, self.h, self.R, self.Mtilde = lt.value, h.value, R.value, mt.value
+
+    def doubled(self) -> int:
+        return 2 * self.Mtilde
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def fourier(self) -> np.ndarray:
+        D = self.doubled()
+        out = np.empty((D, D, D))
+        self._ctx._call(_load().fse_cuda_green_download, self._h, _p(out))
+        return out
+
+    def free(self):
+        if self._h:
+            _load().fse_cuda_green_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One GPU context (streams, cached buffers, cuFFT plans).  Thread-safe."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = _load().fse_cuda_create(int(device), C.byref(h))
+        if st:
+            _raise(st, f"fse_cuda_create(device={device}) failed")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _load().fse_cuda_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _call(self, fn, *args):
+        st = fn(self._h, *args)
+        if st:
+            _raise(st, _load().fse_cuda_last_error(self._h).decode())
+
+    @property
+    def launch_count(self) -> int:
+        return int(_load().fse_cuda_launch_count(self._h))
+
+    def trim(self):
+        self._call(_load().fse_cuda_trim)
+
+    # -- Green's functions
+    def precompute_mollified_green(self, kind, Ltilde, Mtilde, sf) -> MollifiedGreen:
+        h = C.c_void_p()
+        self._call(_load().fse_cuda_green_precompute, int(kind), float(Ltilde), int(Mtilde),
+                   float(sf), C.byref(h))
+        return MollifiedGreen(self, h)
+
+    def upload_mollified_green(self, kind, Ltilde, Mtilde, h, R, fourier) -> MollifiedGreen:
+        f = _f64(fourier).reshape(-1)
+        D = 2 * int(Mtilde)
+        if f.size != D ** 3:
+            raise InvalidArgument("green table must hold (2 Mtilde)^3 values")
+        hd = C.c_void_p()
+        self._call(_load().fse_cuda_green_upload, int(kind), float(Ltilde), int(Mtilde),
+                   float(h), float(R), _p(f), C.byref(hd))
+        return MollifiedGreen(self, hd)
+
+    def save_mollified_green(self, green: MollifiedGreen, path: str):
+        self._call(_load().fse_cuda_green_save, green.handle, path.encode())
+
+    def load_mollified_green(self, path: str) -> MollifiedGreen:
+        hd = C.c_void_p()
+        self._call(_load().fse_cuda_green_load, path.encode(), C.byref(hd))
+        return MollifiedGreen(self, hd)
+
+    # -- hot path
+    def total_sum(self, system: SourceSystem, kind, cfg: EwaldConfig, targets, green,
+                  timings: StageTimings | None = None, targets_are_sources: int = -1):
+        t = _f64(targets, (-1, 3))
+        u = np.empty((t.shape[0], 3))
+        self._call(_load().fse_cuda_total_sum, C.byref(cfg), int(kind),
+                   _p(system.positions), _p(system.strengths), system.size(),
+                   float(system.box_side), _p(t), t.shape[0], int(targets_are_sources),
+                   green.handle, _p(u), C.byref(timings) if timings is not None else None)
+        return u
+
+    def total_sum_dev(self, cfg, kind, d_pos, d_str, n, box_side, d_tgt, nt, green, d_u,
+                      targets_are_sources=-1, timings=None):
+        """Device-pointer variant (ints holding device addresses)."""
+        self._call(_load().fse_cuda_total_sum_dev, C.byref(cfg), int(kind), C.c_void_p(d_pos),
+                   C.c_void_p(d_str), int(n), float(box_side), C.c_void_p(d_tgt), int(nt),
+                   int(targets_are_sources), green.handle, C.c_void_p(d_u),
+                   C.byref(timings) if timings is not None else None)
+
+    def fourier_sum(self, system: SourceSystem, cfg: EwaldConfig, kind, targets, green,
+                    timings: StageTimings | None = None):
+        t = _f64(targets, (-1, 3))
+        u = np.empty((t.shape[0], 3))
+        self._call(_load().fse_cuda_fourier_sum, C.byref(cfg), int(kind), _p(system.positions),
+                   _p(system.strengths), system.size(), float(system.box_side), _p(t),
+                   t.shape[0], green.handle, _p(u),
+                   C.byref(timings) if timings is not None else None)
+        return u
+
+    def real_space_sum(self, system: SourceSystem, kind, xi, rc, targets):
+        t = _f64(targets, (-1, 3))
+        u = np.empty((t.shape[0], 3))
+        self._call(_load().fse_cuda_real_space_sum, int(kind), _p(system.positions),
+                   _p(system.strengths), system.size(), float(system.box_side), float(xi),
+                   float(rc), _p(t), t.shape[0], _p(u))
+        return u
+
+    def spread(self, system: SourceSystem, cfg: EwaldConfig, kind):
+        a = strength_arity(kind)
+        Mt = cfg.Mtilde
+        grid = np.empty((a, Mt, Mt, Mt))
+        self._call(_load().fse_cuda_spread, C.byref(cfg), int(kind), _p(system.positions),
+                   _p(system.strengths), system.size(), float(system.box_side), _p(grid))
+        return grid
+
+    def kspace_scale(self, ghat, cfg: EwaldConfig, kind, green):
+        a = strength_arity(kind)
+        D = cfg.D
+        gh = np.ascontiguousarray(ghat, dtype=np.complex128)
+        if gh.shape != (a, D, D, D):
+            raise InvalidArgument("kspace_scale: component count / plane size does not match")
+        out = np.empty((3, D, D, D), np.complex128)
+        self._call(_load().fse_cuda_kspace_scale, C.byref(cfg), int(kind), green.handle,
+                   gh.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
+        return out
+
+    def build_cell_list(self, system: SourceSystem, rc, domain_pad=0.0) -> CellList:
+        dims = (C.c_int * 3)()
+        side, origin = C.c_double(), C.c_double()
+        n = system.size()
+        fn = _load().fse_cuda_build_cell_list
+        self._call(fn, _p(system.positions), n, float(system.box_side), float(rc),
+                   float(domain_pad), dims, C.byref(side), C.byref(origin), None, None)
+        ncell = dims[0] * dims[1] * dims[2]
+        bstart = np.empty(ncell + 1, np.int64)
+        perm = np.empty(max(n, 1), np.int64)
+        self._call(fn, _p(system.positions), n, float(system.box_side), float(rc),
+                   float(domain_pad), dims, C.byref(side), C.byref(origin),
+                   bstart.ctypes.data_as(C.POINTER(C.c_int64)),
+                   perm.ctypes.data_as(C.POINTER(C.c_int64)))
+        return CellList(side.value, origin.value, tuple(dims), bstart, perm[:n])
+
+    def support_index(self, cfg: EwaldConfig, points):
+        p = _f64(points, (-1, 3))
+        i0 = np.empty((p.shape[0], 3), np.int32)
+        self._call(_load().fse_cuda_support_index, C.byref(cfg), _p(p), p.shape[0],
+                   i0.ctypes.data_as(C.POINTER(C.c_int32)))
+        return i0
+
+    def direct_sum(self, system: SourceSystem, kind, targets, exclude_self: bool):
+        t = _f64(targets, (-1, 3))
+        u = np.empty((t.shape[0], 3))
+        self._call(_load().fse_cuda_direct_sum, int(kind), _p(system.positions),
+                   _p(system.strengths), system.size(), _p(t), t.shape[0], int(exclude_self),
+                   _p(u))
+        return u
+
+    def fft3d(self, data, inverse=False):
+        d = np.ascontiguousarray(data, dtype=np.complex128).copy()
+        n0, n1, n2 = d.shape
+        self._call(_load().fse_cuda_fft3d, d.ctypes.data_as(_dp), n0, n1, n2, int(inverse))
+        return d
+
+    # -- device memory helpers (bench)
+    def dev_alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        self._call(_load().fse_cuda_dev_alloc, int(nbytes), C.byref(p))
+        return p.value
+
+    def dev_free(self, ptr: int):
+        _load().fse_cuda_dev_free(self._h, C.c_void_p(ptr))
+
+    def host_alloc(self, shape, dtype=np.float64) -> np.ndarray:
+        """Pinned host array (kept alive by the returned object)."""
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        self._call(_load().fse_cuda_host_alloc, n, C.byref(p))
+        buf = (C.c_char * max(n, 1)).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+        _PINNED[id(arr)] = (p.value, buf)
+        return arr
+
+    def memcpy(self, dst: int, src: int, nbytes: int):
+        self._call(_load().fse_cuda_memcpy, C.c_void_p(dst), C.c_void_p(src), int(nbytes))
+
+    def mark(self):
+        self._call(_load().fse_cuda_mark)
+
+    def elapsed_ms(self) -> float:
+        v = C.c_double()
+        self._call(_load().fse_cuda_elapsed_ms, C.byref(v))
+        return v.value
+
+
+_PINNED: dict = {}
+
+# ---------------------------------------------------------- default context
+_default = None
+_default_lock = threading.Lock()
+
+
+def default_context() -> Context:
+    global _default
+    with _default_lock:
+        if _default is None:
+            _default = Context(int(os.environ.get("FSE_CUDA_DEVICE", "0")))
+        return _default
+
+
+def precompute_mollified_green(kind, Ltilde, Mtilde, sf) -> MollifiedGreen:
+    return default_context().precompute_mollified_green(kind, Ltilde, Mtilde, sf)
+
+
+def spread(system, cfg, kind):
+    return default_context().spread(system, cfg, kind)
+
+
+def kspace_scale(ghat, cfg, kind, green):
+    return default_context().kspace_scale(ghat, cfg, kind, green)
+
+
+def fourier_sum(system, cfg, kind, targets, green, timings=None):
+    return default_context().fourier_sum(system, cfg, kind, targets, green, timings)
+
+
+def total_sum(system, kind, cfg, targets, green, timings=None):
+    return default_context().total_sum(system, kind, cfg, targets, green, timings)
+
+
+def real_space_sum(system, kind, xi, rc, targets):
+    return default_context().real_space_sum(system, kind, xi, rc, targets)
+
+
+def build_cell_list(system, rc, domain_pad=0.0):
+    return default_context().build_cell_list(system, rc, domain_pad)
+
+
+def direct_sum(system, kind, targets, exclude_self):
+    return default_context().direct_sum(system, kind, targets, exclude_self)
+
+
+def fft3d_forward(data):
+    return default_context().fft3d(data, inverse=False)
+
+
+def fft3d_inverse(data):
+    return default_context().fft3d(data, inverse=True)
+
+
+def save_mollified_green(green, path):
+    green._ctx.save_mollified_green(green, path)
+
+
+def load_mollified_green(path):
+    return default_context().load_mollified_green(path)
+
+
+# ---------------------------------------------------------- host helpers
+def self_interaction(xi, f, kind):  # kernels.cpp:84-89
+    if not xi > 0:
+        raise InvalidArgument("self_interaction: xi must be positive")
+    if int(kind) != KernelKind.Stokeslet:
+        return np.zeros(3)
+    return (-4.0 * xi / np.sqrt(np.pi)) * np.asarray(f, dtype=np.float64)[:3]
+
+
+def rms_error(u, u_ref, relative):  # kernels.cpp:91-103
+    u, u_ref = np.asarray(u, dtype=np.float64), np.asarray(u_ref, dtype=np.float64)
+    if u.shape != u_ref.shape:
+        raise InvalidArgument("rms_error: length mismatch")
+    num = float(((u - u_ref) ** 2).sum())
+    den = float((u_ref ** 2).sum())
+    n = u.shape[0]
+    ab = np.sqrt(num / n)
+    if not relative:
+        return ab
+    if den == 0:
+        raise DomainError("rms_error: relative error of zero reference")
+    return ab / np.sqrt(den / n)
+
+
+def strength_quadratic_sum(system: SourceSystem) -> float:  # kernels.cpp:105-110
+    return float((system.strengths ** 2).sum())
+
+
+def generate_system(kind, n, L, seed) -> SourceSystem:
+    """fse::generate_system (harness.cpp:47-66), bit-identical stream."""
+    pos = np.empty((n, 3))
+    st = np.empty((n, strength_arity(kind)))
+    if _load().fse_generate_system(int(kind), int(n), float(L), int(seed), _p(pos), _p(st)):
+        raise InvalidArgument("generate_system: need N >= 1, L > 0")
+    return SourceSystem(pos, st, float(L))
+
+
+WL_UNIFORM, WL_SPHERE, WL_CLUSTERED, WL_UNIFORM_TARGETS = 1, 3, 4, 5
+
+
+def generate_workload(which: int, n: int, seed: int):
+    """SURVEY.md 8(d) generators; returns (SourceSystem, targets or None)."""
+    a = 9 if which == WL_SPHERE else 3
+    pos = np.empty((n, 3))
+    st = np.empty((n, a))
+    tgt = np.empty((n, 3)) if which == WL_UNIFORM_TARGETS else None
+    if _load().fse_generate_workload(int(which), int(n), int(seed), _p(pos), _p(st), _p(tgt)):
+        raise InvalidArgument("generate_workload: bad arguments")
+    return SourceSystem(pos, st, 1.0), tgt

@@ -1,0 +1,1068 @@
+// fse_capi.cu -- host orchestration and the C-ABI (include/fse_cuda.h).
+//
+// One evaluation of fse::total_sum (ewald.cpp:394-415) on one B200:
+//
+//   stream s0 (Fourier part, ewald.cpp:295-392)
+//     support starts + tile keys -> stable radix sort -> tile starts
+//     -> FGG weights in sorted order -> memset spectrum buffer
+//     -> k_spread (tile-owned, register accumulation)           [spread]
+//     -> cuFFT 2D D2Z over the Mtilde non-zero x-planes
+//     -> cuFFT 1D Z2Z along x (the 7/8 zero padding is never transformed
+//        along y/z: pruned R2C of the D = 2 Mtilde grid)          [fft]
+//     -> k_kscale_half (Nyquist-exact multiplier, 1/D^3 folded)   [scale]
+//     -> cuFFT 1D Z2Z inverse along x -> 2D Z2D over Mtilde planes [fft]
+//     -> target prep (reuses the source sort when targets == sources)
+//     -> k_gather (warp groups of 8 targets)                     [quadrature]
+//   stream s1 (real part, realspace.cpp:86-149), concurrent with s0
+//     cell ids -> stable radix sort -> bucket starts (the reference CellList)
+//     -> SoA permute -> k_realspace                               [realspace]
+//   s0 waits for s1 -> k_epilogue: u = (uF + uR) + self term
+//
+// Device buffers are cached per context and grow on demand; cuFFT plans are
+// cached per (D, Mtilde) and share one work area.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "fse_internal.cuh"
+
+namespace fsecu {
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    throw Error(e == cudaErrorMemoryAllocation ? FSE_ENOMEM : FSE_ECUDA, buf);
+}
+
+[[noreturn]] void throw_cufft(cufftResult r, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "cuFFT error %d in %s at %s:%d", static_cast<int>(r), what,
+                  file, line);
+    throw Error(r == CUFFT_ALLOC_FAILED ? FSE_ENOMEM : FSE_ECUFFT, buf);
+}
+
+GridParams make_grid_params(const fse_config& c) {
+    GridParams g{};
+    g.P = c.P;
+    g.Mt = c.Mtilde;
+    g.D = 2 * c.Mtilde;
+    g.Dh = g.D / 2 + 1;
+    g.plane = static_cast<int64_t>(g.D) * (g.D + 2);
+    g.comp = static_cast<int64_t>(g.D) * g.plane;
+    g.h = c.h;
+    g.origin = -c.deltaL / 2;                                     // ewald.cpp:147
+    g.alpha = 2.0 * c.xi * c.xi / c.eta;                          // ewald.cpp:152
+    g.prefac = std::pow(2.0 * c.xi * c.xi / (M_PI * c.eta), 1.5);  // ewald.cpp:153
+    g.L = c.L;
+    g.dk = M_PI / c.Ltilde;                                       // ewald.cpp:232
+    g.inv4xi2 = 1.0 / (4.0 * c.xi * c.xi);                        // ewald.cpp:233
+    g.eta = c.eta;
+    g.invD3 = 1.0 / (static_cast<double>(g.D) * g.D * g.D);        // fft.cpp:34
+    g.ncx = (g.Mt + 7) / 8;
+    g.ncy = (g.Mt + 7) / 8;
+    g.ncz = (g.Mt + 15) / 16;
+    g.nkeys = static_cast<int64_t>(g.ncx) * g.ncy * g.ncz * 8;
+    return g;
+}
+
+namespace {
+__global__ void k_not_equal(const double* a, const double* b, int64_t n, int* flag) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q < n && !(a[q] == b[q])) atomicOr(flag, 1);
+}
+}  // namespace
+
+}  // namespace fsecu
+
+using namespace fsecu;
+
+struct fse_green {
+    int kind;
+    double Ltilde, h, R;
+    int Mtilde;
+    int device;
+    double* d_half;  // [D][D][D/2+1]
+};
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+constexpr int NEV = 12;
+
+}  // namespace
+
+struct fse_cuda_ctx {
+    int device = 0;
+    cudaStream_t s0 = nullptr, s1 = nullptr;
+    cudaEvent_t ev[NEV] = {};
+    cudaEvent_t mark[2] = {};
+    int mark_n = 0;
+    std::mutex mu;
+    std::string err;
+    uint64_t launches = 0;
+    std::map<std::string, DevBuf> bufs;
+    std::map<std::tuple<int, int, int>, cufftHandle> plans;
+    DevBuf work;
+    int* d_flags = nullptr;  // [0] s0 flags, [1] s1 flags, [2] equality flag
+    int* h_flags = nullptr;  // pinned
+};
+
+namespace {
+
+struct Guard {
+    explicit Guard(fse_cuda_ctx* c) : lk(c->mu) { FSE_CU(cudaSetDevice(c->device)); }
+    std::unique_lock<std::mutex> lk;
+};
+
+template <class F>
+fse_status api(fse_cuda_ctx* ctx, F&& f) {
+    if (!ctx) return FSE_EINVAL;
+    try {
+        Guard g(ctx);
+        ctx->err.clear();
+        f();
+        return FSE_OK;
+    } catch (const Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "host allocation failed";
+        return FSE_ENOMEM;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return FSE_ERUNTIME;
+    }
+}
+
+[[noreturn]] void invalid(const std::string& m) { throw Error(FSE_EINVAL, m); }
+
+void sync_all(fse_cuda_ctx* c) { FSE_CU(cudaDeviceSynchronize()); }
+
+template <class T>
+T* buf(fse_cuda_ctx* c, const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    DevBuf& b = c->bufs[name];
+    if (b.bytes < bytes) {
+        sync_all(c);
+        if (b.p) FSE_CU(cudaFree(b.p));
+        b.p = nullptr;
+        b.bytes = 0;
+        const size_t alloc = bytes + bytes / 8;  // headroom for neighbouring sizes
+        FSE_CU(cudaMalloc(&b.p, alloc));
+        b.bytes = alloc;
+    }
+    return static_cast<T*>(b.p);
+}
+
+void release_plans(fse_cuda_ctx* c) {
+    for (auto& kv : c->plans) cufftDestroy(kv.second);
+    c->plans.clear();
+}
+
+Launch L0(fse_cuda_ctx* c) { return Launch{c->s0, &c->launches}; }
+Launch L1(fse_cuda_ctx* c) { return Launch{c->s1, &c->launches}; }
+
+// which: 0 = 2D D2Z batch Mt, 1 = 2D Z2D batch Mt, 2 = 1D Z2Z along x
+cufftHandle plan(fse_cuda_ctx* c, int which, int D, int Mt) {
+    const auto key = std::make_tuple(which, D, which == 2 ? 0 : Mt);
+    auto it = c->plans.find(key);
+    if (it != c->plans.end()) return it->second;
+    cufftHandle h;
+    FSE_CUFFT(cufftCreate(&h));
+    FSE_CUFFT(cufftSetAutoAllocation(h, 0));
+    size_t ws = 0;
+    const long long Dh = D / 2 + 1;
+    if (which == 0 || which == 1) {
+        long long n[2] = {D, D};
+        FSE_CUFFT(cufftMakePlanMany64(h, 2, n, nullptr, 1, 0, nullptr, 1, 0,
+                                      which == 0 ? CUFFT_D2Z : CUFFT_Z2D, Mt, &ws));
+    } else {
+        long long n[1] = {D};
+        long long emb[1] = {D};
+        const long long stride = static_cast<long long>(D) * Dh;
+        FSE_CUFFT(cufftMakePlanMany64(h, 1, n, emb, stride, 1, emb, stride, 1, CUFFT_Z2Z,
+                                      stride, &ws));
+    }
+    if (ws > c->work.bytes) {
+        sync_all(c);
+        if (c->work.p) FSE_CU(cudaFree(c->work.p));
+        c->work.p = nullptr;
+        FSE_CU(cudaMalloc(&c->work.p, ws));
+        c->work.bytes = ws;
+        for (auto& kv : c->plans) FSE_CUFFT(cufftSetWorkArea(kv.second, c->work.p));
+    }
+    FSE_CUFFT(cufftSetWorkArea(h, c->work.p));
+    FSE_CUFFT(cufftSetStream(h, c->s0));
+    c->plans[key] = h;
+    return h;
+}
+
+void check_cfg(const fse_config* cfg) {
+    if (!cfg) invalid("null config");
+    if (!(cfg->L > 0) || !(cfg->xi > 0) || !(cfg->rc > 0) || cfg->M < 1 || cfg->P < 2 ||
+        cfg->P % 2 || cfg->Mtilde < cfg->P || !(cfg->h > 0) || !(cfg->eta > 0))
+        invalid("config was not produced by make_config");
+}
+
+void check_kind(int kind) {
+    if (kind < FSE_STOKESLET || kind > FSE_ROTLET) invalid("unknown kernel kind");
+}
+
+// ewald.cpp:93-99
+void check_green(const fse_config* cfg, int kind, const fse_green* g) {
+    if (!g) invalid("fourier_sum: null green");
+    const int want = kind == FSE_ROTLET ? FSE_HARMONIC : FSE_BIHARMONIC;
+    if (g->kind != want) invalid("fourier_sum: green kind does not match kernel");
+    if (g->Mtilde != cfg->Mtilde || std::abs(g->Ltilde - cfg->Ltilde) > 1e-12 * cfg->Ltilde)
+        invalid("fourier_sum: green grid does not match config");
+}
+
+void exclusive_scan(fse_cuda_ctx* c, cudaStream_t s, const char* tag, const int32_t* in,
+                    int32_t* out, int64_t n) {
+    size_t tb = 0;
+    FSE_CU(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int>(n), s));
+    void* tmp = buf<char>(c, std::string("cubtmp_") + tag, tb);
+    FSE_CU(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, static_cast<int>(n), s));
+}
+
+void sort_pairs(fse_cuda_ctx* c, cudaStream_t s, const char* tag, const uint32_t* kin,
+                uint32_t* kout, const uint32_t* vin, uint32_t* vout, int64_t n, int bits) {
+    size_t tb = 0;
+    FSE_CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, static_cast<int>(n),
+                                           0, bits, s));
+    void* tmp = buf<char>(c, std::string("cubtmp_") + tag, tb);
+    FSE_CU(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, static_cast<int>(n), 0,
+                                           bits, s));
+}
+
+int bits_for(int64_t nkeys) {
+    int b = 1;
+    while ((int64_t{1} << b) < nkeys) ++b;
+    return b;
+}
+
+// Sorted point set for the Fourier stages (support-tile order).
+struct Sorted {
+    uint32_t* perm = nullptr;
+    int32_t* tstart = nullptr;  // nkeys + 1
+    int32_t* i0s = nullptr;
+    double* w = nullptr;
+    double* fs = nullptr;
+};
+
+Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
+                   const double* d_pos, const double* d_str, int a, int64_t n, int check_box,
+                   const double* qtab) {
+    Launch L = L0(c);
+    Sorted s;
+    uint32_t* keys = buf<uint32_t>(c, tag + "keys", n);
+    uint32_t* keys2 = buf<uint32_t>(c, tag + "keys2", n);
+    uint32_t* iota = buf<uint32_t>(c, tag + "iota", n);
+    s.perm = buf<uint32_t>(c, tag + "perm", n);
+    int32_t* counts = buf<int32_t>(c, tag + "counts", g.nkeys + 1);
+    s.tstart = buf<int32_t>(c, tag + "tstart", g.nkeys + 1);
+    s.i0s = buf<int32_t>(c, tag + "i0s", 3 * n);
+    s.w = buf<double>(c, tag + "w", 3 * g.P * n);
+    s.fs = d_str ? buf<double>(c, tag + "fs", a * n) : nullptr;
+    launch_support_keys(L, g, d_pos, n, check_box, keys, nullptr, c->d_flags);
+    launch_iota(L, iota, n);
+    if (n > 0) sort_pairs(c, c->s0, "s0", keys, keys2, iota, s.perm, n, bits_for(g.nkeys));
+    FSE_CU(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (g.nkeys + 1), c->s0));
+    launch_histogram(L, keys2, n, counts);
+    exclusive_scan(c, c->s0, "s0", counts, s.tstart, g.nkeys + 1);
+    launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true);
+    return s;
+}
+
+// Reference CellList geometry (realspace.cpp:65-76), computed on the host
+// with the same libm calls so dims and cell_side are bit-identical.
+CellGrid cell_grid(int64_t n, double box_side, double rc, double pad) {
+    if (!(rc > 0)) invalid("build_cell_list: rc must be positive");
+    CellGrid cg;
+    cg.origin = -pad;
+    const double extent = box_side + 2.0 * pad;
+    const int cap =
+        1 + static_cast<int>(std::cbrt(8.0 * static_cast<double>(std::max<int64_t>(n, 1))));
+    const int want = std::max(1, static_cast<int>(std::floor(extent / rc)));
+    cg.dim = std::min(want, cap);
+    cg.side = extent / cg.dim;
+    cg.ncell = static_cast<int64_t>(cg.dim) * cg.dim * cg.dim;
+    return cg;
+}
+
+struct Cells {
+    uint32_t* perm = nullptr;
+    int32_t* start = nullptr;  // ncell + 1
+    double *px = nullptr, *py = nullptr, *pz = nullptr, *fs = nullptr;
+};
+
+Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, const double* d_pos,
+                const double* d_str, int a, int64_t n) {
+    Launch L = L1(c);
+    Cells r;
+    uint32_t* cell = buf<uint32_t>(c, tag + "cell", n);
+    uint32_t* cell2 = buf<uint32_t>(c, tag + "cell2", n);
+    uint32_t* iota = buf<uint32_t>(c, tag + "iota", n);
+    r.perm = buf<uint32_t>(c, tag + "perm", n);
+    int32_t* counts = buf<int32_t>(c, tag + "counts", cg.ncell + 1);
+    r.start = buf<int32_t>(c, tag + "start", cg.ncell + 1);
+    launch_cell_ids(L, d_pos, n, cg.origin, cg.side, cg.dim, cell);
+    launch_iota(L, iota, n);
+    if (n > 0) sort_pairs(c, c->s1, "s1", cell, cell2, iota, r.perm, n, bits_for(cg.ncell));
+    FSE_CU(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (cg.ncell + 1), c->s1));
+    launch_histogram(L, cell2, n, counts);
+    exclusive_scan(c, c->s1, "s1", counts, r.start, cg.ncell + 1);
+    r.px = buf<double>(c, tag + "px", n);
+    r.py = buf<double>(c, tag + "py", n);
+    r.pz = buf<double>(c, tag + "pz", n);
+    r.fs = d_str ? buf<double>(c, tag + "fs", a * n) : nullptr;
+    launch_permute_soa(L, d_pos, d_str, a, r.perm, n, r.px, r.py, r.pz, r.fs);
+    return r;
+}
+
+// real-space pair sum on s1 into d_uR (caller order)
+void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_str, int64_t n,
+               double box_side, double xi, double rc, const double* d_tgt, int64_t nt, bool tas,
+               double* d_uR) {
+    if (!(xi > 0) || !(rc > 0)) invalid("real_space_sum: xi and rc must be positive");
+    const int a = arity_of(kind);
+    const CellGrid cg = cell_grid(n, box_side, rc, 0.0);
+    Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n);
+    Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt);
+    Launch L = L1(c);
+    int32_t* icnt = buf<int32_t>(c, "rs_icnt", cg.ncell + 1);
+    int32_t* ioff = buf<int32_t>(c, "rs_ioff", cg.ncell + 1);
+    launch_item_counts(L, tgt.start, cg.ncell, 128, icnt);
+    exclusive_scan(c, c->s1, "s1", icnt, ioff, cg.ncell + 1);
+    int32_t nitems = 0;
+    FSE_CU(cudaMemcpyAsync(&c->h_flags[4], ioff + cg.ncell, sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, c->s1));
+    FSE_CU(cudaStreamSynchronize(c->s1));
+    nitems = c->h_flags[4];
+    int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(nitems));
+    launch_fill_items(L, tgt.start, ioff, cg.ncell, 128, items);
+    if (nt > 0 && n > 0)
+        launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
+                         tgt.pz, tgt.start, items, nitems, tgt.perm, xi, rc, d_uR);
+    else if (nt > 0)
+        FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
+}
+
+double ev_sec(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    FSE_CU(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+}
+
+enum { EV_START, EV_SPREAD, EV_FFT1, EV_SCALE, EV_FFT2, EV_QUAD, EV_R0, EV_R1, EV_JOIN, EV_END };
+
+void raise_flags(fse_cuda_ctx* c) {
+    FSE_CU(cudaMemcpyAsync(c->h_flags, c->d_flags, 3 * sizeof(int), cudaMemcpyDeviceToHost,
+                           c->s0));
+    FSE_CU(cudaStreamSynchronize(c->s0));
+    const int f = c->h_flags[0] | c->h_flags[1];
+    if (f & FLAG_TARGET_BOX) invalid("fourier_sum: target outside [0,L]^3");
+    if (f & FLAG_SUPPORT) invalid("spread/quadrature: point support exceeds grid");
+    if (f & FLAG_COINCIDENT) throw Error(FSE_EDOMAIN, "direct_sum: coincident target/source point");
+}
+
+bool detect_tas_dev(fse_cuda_ctx* c, const double* a, const double* b, int64_t n, int64_t nt) {
+    if (n != nt) return false;
+    if (a == b || n == 0) return true;
+    FSE_CU(cudaMemsetAsync(c->d_flags + 2, 0, sizeof(int), c->s0));
+    k_not_equal<<<static_cast<unsigned>((3 * n + 255) / 256), 256, 0, c->s0>>>(a, b, 3 * n,
+                                                                                c->d_flags + 2);
+    FSE_LAUNCH_CHECK();
+    ++c->launches;
+    FSE_CU(cudaMemcpyAsync(c->h_flags + 2, c->d_flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->s0));
+    FSE_CU(cudaStreamSynchronize(c->s0));
+    return c->h_flags[2] == 0;
+}
+
+// The whole hot path on device pointers.  u (caller order) = fourier (if
+// want_f) + real (if want_r) + self (stokeslet, targets == sources, full sum).
+void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_pos,
+             const double* d_str, int64_t n, double box_side, const double* d_tgt, int64_t nt,
+             int tas_flag, const fse_green* green, double* d_u, fse_timings* tm, bool want_f,
+             bool want_r) {
+    check_kind(kind);
+    if (n < 0 || nt < 0) invalid("negative point count");
+    const int a = arity_of(kind);
+    if (want_f) {
+        check_cfg(cfg);
+        check_green(cfg, kind, green);
+        if (green->device != c->device) invalid("green lives on another device");
+    }
+    const bool tas = tas_flag < 0 ? detect_tas_dev(c, d_pos, d_tgt, n, nt) : tas_flag != 0;
+    FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+    FSE_CU(cudaEventRecord(c->ev[EV_START], c->s0));
+    FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_START], 0));
+
+    double* uR = nullptr;
+    if (want_r) {
+        uR = want_f ? buf<double>(c, "uR", 3 * nt) : d_u;
+        FSE_CU(cudaEventRecord(c->ev[EV_R0], c->s1));
+        real_part(c, kind, d_pos, d_str, n, box_side, cfg->xi, cfg->rc, d_tgt, nt, tas, uR);
+        FSE_CU(cudaEventRecord(c->ev[EV_R1], c->s1));
+    }
+
+    double* uF = nullptr;
+    if (want_f) {
+        if (std::abs(box_side - cfg->L) > 1e-12 * cfg->L)
+            invalid("spread: config box does not match system");
+        const GridParams g = make_grid_params(*cfg);
+        Launch L = L0(c);
+        double* qtab = buf<double>(c, "qtab", g.P);
+        launch_quad_table(L, g, qtab);
+        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, tas ? 1 : 0, qtab);
+        // spectrum buffer: a components of [D][D][D+2] doubles (= [D][D][Dh] complex)
+        double* X = buf<double>(c, "X", static_cast<size_t>(a) * g.comp);
+        FSE_CU(cudaMemsetAsync(X, 0, sizeof(double) * a * g.comp, c->s0));
+        for (int c0 = 0; c0 < a; c0 += 3)
+            launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
+        FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
+
+        const cufftHandle p2r = plan(c, 0, g.D, g.Mt);
+        const cufftHandle px = plan(c, 2, g.D, g.Mt);
+        const cufftHandle p2c = plan(c, 1, g.D, g.Mt);
+        auto comp_ptr = [&](int cc) { return X + cc * g.comp; };
+        for (int cc = 0; cc < a; ++cc) {
+            double* xr = comp_ptr(cc);
+            auto* xc = reinterpret_cast<cufftDoubleComplex*>(xr);
+            FSE_CUFFT(cufftExecD2Z(p2r, xr, xc));
+            FSE_CUFFT(cufftExecZ2Z(px, xc, xc, CUFFT_FORWARD));
+        }
+        FSE_CU(cudaEventRecord(c->ev[EV_FFT1], c->s0));
+        launch_kscale_half(L, g, kind, green->d_half, reinterpret_cast<double2*>(X),
+                           g.comp / 2);
+        FSE_CU(cudaEventRecord(c->ev[EV_SCALE], c->s0));
+        for (int cc = 0; cc < 3; ++cc) {
+            double* xr = comp_ptr(cc);
+            auto* xc = reinterpret_cast<cufftDoubleComplex*>(xr);
+            FSE_CUFFT(cufftExecZ2Z(px, xc, xc, CUFFT_INVERSE));
+            FSE_CUFFT(cufftExecZ2D(p2c, xc, xr));
+        }
+        FSE_CU(cudaEventRecord(c->ev[EV_FFT2], c->s0));
+
+        Sorted tg = tas ? src : prep_points(c, g, "ft_", d_tgt, nullptr, 0, nt, 1, qtab);
+        int32_t* gcnt = buf<int32_t>(c, "gcnt", g.nkeys + 1);
+        int32_t* goff = buf<int32_t>(c, "goff", g.nkeys + 1);
+        launch_group_counts(L, tg.tstart, g.nkeys, gcnt);
+        exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
+        FSE_CU(cudaMemcpyAsync(&c->h_flags[5], goff + g.nkeys, sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, c->s0));
+        FSE_CU(cudaStreamSynchronize(c->s0));
+        const int64_t ngroups = c->h_flags[5];
+        int32_t* gkey = buf<int32_t>(c, "gkey", ngroups);
+        launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
+        uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
+        const double h3 = g.h * g.h * g.h;
+        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, ngroups, X, tg.perm, h3, uF);
+        FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
+    }
+
+    if (want_r) {
+        FSE_CU(cudaEventRecord(c->ev[EV_JOIN], c->s1));
+        FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_JOIN], 0));
+    }
+    if (want_f && want_r) {
+        const bool self = tas && kind == FSE_STOKESLET;
+        launch_epilogue(L0(c), nt, uF, uR, self ? d_str : nullptr,
+                        self ? -4.0 * cfg->xi / std::sqrt(M_PI) : 0.0, d_u);
+    }
+    FSE_CU(cudaEventRecord(c->ev[EV_END], c->s0));
+    raise_flags(c);
+    if (tm) {
+        FSE_CU(cudaEventSynchronize(c->ev[EV_END]));
+        if (want_f) {
+            tm->spread += ev_sec(c->ev[EV_START], c->ev[EV_SPREAD]);
+            tm->fft += ev_sec(c->ev[EV_SPREAD], c->ev[EV_FFT1]) +
+                       ev_sec(c->ev[EV_SCALE], c->ev[EV_FFT2]);
+            tm->scale += ev_sec(c->ev[EV_FFT1], c->ev[EV_SCALE]);
+            tm->quadrature += ev_sec(c->ev[EV_FFT2], c->ev[EV_QUAD]);
+        }
+        if (want_r) tm->realspace += ev_sec(c->ev[EV_R0], c->ev[EV_R1]);
+        tm->total += ev_sec(c->ev[EV_START], c->ev[EV_END]);
+    }
+}
+
+// host-pointer front end: H2D (pinned or pageable), run, D2H
+bool host_equal(const double* a, const double* b, int64_t n) {
+    if (a == b) return true;
+    for (int64_t q = 0; q < 3 * n; ++q)
+        if (!(a[q] == b[q])) return false;
+    return true;
+}
+
+void h2d(fse_cuda_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) FSE_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s0));
+}
+
+void d2h(fse_cuda_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) FSE_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->s0));
+    FSE_CU(cudaStreamSynchronize(c->s0));
+}
+
+void run_sum_host(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* pos,
+                  const double* str, int64_t n, double box_side, const double* tgt, int64_t nt,
+                  int tas_flag, const fse_green* green, double* u, fse_timings* tm, bool want_f,
+                  bool want_r) {
+    check_kind(kind);
+    if (n < 0 || nt < 0) invalid("negative point count");
+    if ((n > 0 && (!pos || !str)) || (nt > 0 && (!tgt || !u))) invalid("null pointer");
+    const int a = arity_of(kind);
+    const bool tas = tas_flag < 0 ? (n == nt && host_equal(pos, tgt, n)) : tas_flag != 0;
+    double* d_pos = buf<double>(c, "in_pos", 3 * n);
+    double* d_str = buf<double>(c, "in_str", a * n);
+    double* d_tgt = tas ? d_pos : buf<double>(c, "in_tgt", 3 * nt);
+    double* d_u = buf<double>(c, "in_u", 3 * nt);
+    h2d(c, d_pos, pos, sizeof(double) * 3 * n);
+    h2d(c, d_str, str, sizeof(double) * a * n);
+    if (!tas) h2d(c, d_tgt, tgt, sizeof(double) * 3 * nt);
+    run_sum(c, cfg, kind, d_pos, d_str, n, box_side, d_tgt, nt, tas ? 1 : 0, green, d_u, tm,
+            want_f, want_r);
+    d2h(c, u, d_u, sizeof(double) * 3 * nt);
+}
+
+// ---------------------------------------------------------------- Green
+fse_green* new_green(fse_cuda_ctx* c, int kind, double Ltilde, int Mt, double h, double R) {
+    auto* g = new fse_green;
+    g->kind = kind;
+    g->Ltilde = Ltilde;
+    g->Mtilde = Mt;
+    g->h = h;
+    g->R = R;
+    g->device = c->device;
+    g->d_half = nullptr;
+    const int64_t D = 2 * static_cast<int64_t>(Mt);
+    cudaError_t e = cudaMalloc(&g->d_half, sizeof(double) * D * D * (D / 2 + 1));
+    if (e != cudaSuccess) {
+        delete g;
+        throw_cuda(e, "cudaMalloc(green)", __FILE__, __LINE__);
+    }
+    return g;
+}
+
+// greens.cpp:48-113 on the GPU: Ghat on the sM^3 wavenumber grid (half
+// spectrum, the grid is real and even) -> Z2D -> scale 1/sM^3 and window to
+// the (2 Mt)^3 offsets in [-Mt, Mt) -> D2Z -> real part.
+fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, double sf) {
+    const double sf_min = 1.0 + std::sqrt(3.0);
+    if (!(Ltilde > 0) || Mt < 1) invalid("precompute_mollified_green: bad domain");
+    if (sf < sf_min - 1e-12) invalid("precompute_mollified_green: sf below 1 + sqrt(3)");
+    if (gkind != FSE_HARMONIC && gkind != FSE_BIHARMONIC) invalid("unknown green kind");
+    const double h = Ltilde / Mt;
+    const double R = std::sqrt(3.0) * Ltilde;
+    int sM = static_cast<int>(std::ceil(sf * Mt));
+    if (sM % 2 != 0) ++sM;
+    const double dk = 2.0 * M_PI / (sM * h);
+    const int D = 2 * Mt;
+    Launch L = L0(c);
+    fse_green* g = new_green(c, gkind, Ltilde, Mt, h, R);
+    try {
+        const int64_t sMp = sM + 2;
+        double* S = buf<double>(c, "green_S", static_cast<size_t>(sM) * sM * sMp);
+        launch_green_fill(L, gkind, sM, dk, R, reinterpret_cast<double2*>(S));
+        cufftHandle pi;
+        size_t ws = 0;
+        FSE_CUFFT(cufftCreate(&pi));
+        FSE_CUFFT(cufftMakePlan3d(pi, sM, sM, sM, CUFFT_Z2D, &ws));
+        FSE_CUFFT(cufftSetStream(pi, c->s0));
+        FSE_CUFFT(cufftExecZ2D(pi, reinterpret_cast<cufftDoubleComplex*>(S), S));
+        const double scale = 1.0 / (static_cast<double>(sM) * sM * sM);
+        double* T = buf<double>(c, "green_T", static_cast<size_t>(D) * D * (D + 2));
+        launch_green_window(L, sM, sMp, Mt, S, scale, T);
+        FSE_CU(cudaStreamSynchronize(c->s0));
+        cufftDestroy(pi);
+        cufftHandle pf;
+        FSE_CUFFT(cufftCreate(&pf));
+        FSE_CUFFT(cufftMakePlan3d(pf, D, D, D, CUFFT_D2Z, &ws));
+        FSE_CUFFT(cufftSetStream(pf, c->s0));
+        FSE_CUFFT(cufftExecD2Z(pf, T, reinterpret_cast<cufftDoubleComplex*>(T)));
+        launch_green_real(L, reinterpret_cast<const double2*>(T),
+                          static_cast<int64_t>(D) * D * (D / 2 + 1), g->d_half);
+        FSE_CU(cudaStreamSynchronize(c->s0));
+        cufftDestroy(pf);
+        // the scratch is large (sM^3): give it back
+        for (const char* nm : {"green_S", "green_T"}) {
+            DevBuf& b = c->bufs[nm];
+            if (b.p) FSE_CU(cudaFree(b.p));
+            b = DevBuf{};
+        }
+    } catch (...) {
+        cudaFree(g->d_half);
+        delete g;
+        throw;
+    }
+    return g;
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+extern "C" {
+
+int fse_cuda_abi_version(void) { return FSE_CUDA_ABI_VERSION; }
+int fse_arity(int kind) { return arity_of(kind); }
+
+fse_status fse_cuda_create(int device, fse_cuda_ctx** out) {
+    if (!out) return FSE_EINVAL;
+    *out = nullptr;
+    auto* c = new fse_cuda_ctx;
+    c->device = device;
+    try {
+        FSE_CU(cudaSetDevice(device));
+        FSE_CU(cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking));
+        FSE_CU(cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking));
+        for (auto& e : c->ev) FSE_CU(cudaEventCreate(&e));
+        for (auto& e : c->mark) FSE_CU(cudaEventCreate(&e));
+        FSE_CU(cudaMalloc(&c->d_flags, 8 * sizeof(int)));
+        FSE_CU(cudaMallocHost(&c->h_flags, 8 * sizeof(int)));
+    } catch (const Error& e) {
+        fse_status st = e.code;
+        fse_cuda_destroy(c);
+        return st;
+    }
+    *out = c;
+    return FSE_OK;
+}
+
+void fse_cuda_destroy(fse_cuda_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    release_plans(c);
+    for (auto& kv : c->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    if (c->work.p) cudaFree(c->work.p);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->mark)
+        if (e) cudaEventDestroy(e);
+    if (c->d_flags) cudaFree(c->d_flags);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->s0) cudaStreamDestroy(c->s0);
+    if (c->s1) cudaStreamDestroy(c->s1);
+    delete c;
+}
+
+const char* fse_cuda_last_error(const fse_cuda_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+fse_status fse_cuda_trim(fse_cuda_ctx* c) {
+    return api(c, [&] {
+        sync_all(c);
+        release_plans(c);
+        for (auto& kv : c->bufs)
+            if (kv.second.p) FSE_CU(cudaFree(kv.second.p));
+        c->bufs.clear();
+        if (c->work.p) FSE_CU(cudaFree(c->work.p));
+        c->work = DevBuf{};
+    });
+}
+
+fse_status fse_cuda_host_alloc(fse_cuda_ctx* c, size_t bytes, void** out) {
+    return api(c, [&] { FSE_CU(cudaMallocHost(out, std::max<size_t>(bytes, 1))); });
+}
+void fse_cuda_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+fse_status fse_cuda_dev_alloc(fse_cuda_ctx* c, size_t bytes, void** out) {
+    return api(c, [&] { FSE_CU(cudaMalloc(out, std::max<size_t>(bytes, 1))); });
+}
+void fse_cuda_dev_free(fse_cuda_ctx* c, void* p) {
+    if (c && p) {
+        cudaSetDevice(c->device);
+        cudaFree(p);
+    }
+}
+fse_status fse_cuda_memcpy(fse_cuda_ctx* c, void* dst, const void* src, size_t bytes) {
+    return api(c, [&] {
+        FSE_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->s0));
+        FSE_CU(cudaStreamSynchronize(c->s0));
+    });
+}
+fse_status fse_cuda_mark(fse_cuda_ctx* c) {
+    return api(c, [&] {
+        FSE_CU(cudaEventRecord(c->mark[c->mark_n & 1], c->s0));
+        ++c->mark_n;
+    });
+}
+fse_status fse_cuda_elapsed_ms(fse_cuda_ctx* c, double* ms) {
+    return api(c, [&] {
+        if (c->mark_n < 2) invalid("need two marks");
+        cudaEvent_t a = c->mark[(c->mark_n - 2) & 1], b = c->mark[(c->mark_n - 1) & 1];
+        FSE_CU(cudaEventSynchronize(b));
+        float f = 0;
+        FSE_CU(cudaEventElapsedTime(&f, a, b));
+        *ms = f;
+    });
+}
+uint64_t fse_cuda_launch_count(const fse_cuda_ctx* c) { return c ? c->launches : 0; }
+
+// ewald.cpp:103-134
+fse_status fse_make_config(double L, double xi, double rc, int M, int P, double sf,
+                           fse_config* out, char* err, size_t errlen) {
+    auto fail = [&](const char* m) {
+        if (err && errlen) std::snprintf(err, errlen, "%s", m);
+        return FSE_EINVAL;
+    };
+    if (!out) return fail("null output");
+    if (!(L > 0) || !(xi > 0) || !(rc > 0) || M < 1 || P < 2)
+        return fail("make_config: all parameters must be positive");
+    if (P % 2 != 0) return fail("make_config: P must be even");
+    fse_config c;
+    std::memset(&c, 0, sizeof c);
+    c.L = L;
+    c.xi = xi;
+    c.rc = rc;
+    c.M = M;
+    c.P = P;
+    c.h = L / M;
+    c.d = c.h * P;
+    c.m = 0.976 * std::sqrt(M_PI * P);
+    c.eta = (xi * c.d / c.m) * (xi * c.d / c.m);
+    double raw = c.d;
+    if (c.eta < 1.0) raw = std::max(c.d, std::sqrt(2.0 * (1.0 - c.eta)) * c.m / xi);
+    const int pad = static_cast<int>(std::ceil(raw / c.h - 1e-12));
+    c.deltaL = pad * c.h;
+    c.Mtilde = M + pad;
+    c.Ltilde = c.Mtilde * c.h;
+    c.kinf = M_PI * c.Mtilde / c.Ltilde;
+    c.R = std::sqrt(3.0) * c.Ltilde;
+    c.sf = sf > 0 ? sf : 1.0 + std::sqrt(3.0);
+    if (c.sf < 1.0 + std::sqrt(3.0) - 1e-12) return fail("make_config: sf below 1 + sqrt(3)");
+    if (P > c.Mtilde) return fail("make_config: Gaussian support exceeds grid");
+    *out = c;
+    return FSE_OK;
+}
+
+fse_status fse_cuda_green_precompute(fse_cuda_ctx* c, int green_kind, double Ltilde, int Mtilde,
+                                     double sf, fse_green** out) {
+    return api(c, [&] {
+        if (!out) invalid("null output");
+        *out = green_precompute(c, green_kind, Ltilde, Mtilde, sf);
+    });
+}
+
+fse_status fse_cuda_green_upload(fse_cuda_ctx* c, int green_kind, double Ltilde, int Mtilde,
+                                 double h, double R, const double* full, fse_green** out) {
+    return api(c, [&] {
+        if (!out || !full) invalid("null pointer");
+        if (Mtilde < 1 || !(Ltilde > 0)) invalid("bad green geometry");
+        if (green_kind != FSE_HARMONIC && green_kind != FSE_BIHARMONIC)
+            invalid("unknown green kind");
+        fse_green* g = new_green(c, green_kind, Ltilde, Mtilde, h, R);
+        try {
+            const int D = 2 * Mtilde;
+            const size_t n = static_cast<size_t>(D) * D * D;
+            double* tmp = buf<double>(c, "green_full", n);
+            h2d(c, tmp, full, n * sizeof(double));
+            launch_green_full_to_half(L0(c), D, tmp, g->d_half);
+            FSE_CU(cudaStreamSynchronize(c->s0));
+        } catch (...) {
+            cudaFree(g->d_half);
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+fse_status fse_cuda_green_download(fse_cuda_ctx* c, const fse_green* g, double* full) {
+    return api(c, [&] {
+        if (!g || !full) invalid("null pointer");
+        const int D = 2 * g->Mtilde;
+        const size_t n = static_cast<size_t>(D) * D * D;
+        double* tmp = buf<double>(c, "green_full", n);
+        launch_green_half_to_full(L0(c), D, g->d_half, tmp);
+        d2h(c, full, tmp, n * sizeof(double));
+    });
+}
+
+fse_status fse_cuda_green_info(const fse_green* g, int* kind, double* Ltilde, double* h,
+                               double* R, int* Mtilde) {
+    if (!g) return FSE_EINVAL;
+    if (kind) *kind = g->kind;
+    if (Ltilde) *Ltilde = g->Ltilde;
+    if (h) *h = g->h;
+    if (R) *R = g->R;
+    if (Mtilde) *Mtilde = g->Mtilde;
+    return FSE_OK;
+}
+
+void fse_cuda_green_free(fse_green* g) {
+    if (!g) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    cudaFree(g->d_half);
+    cudaSetDevice(cur);
+    delete g;
+}
+
+// greens.cpp:141-171: "FSEG", u32 version 1, u8 kind, f64 Ltilde/h/R, u64 x3 extents, payload
+fse_status fse_cuda_green_save(fse_cuda_ctx* c, const fse_green* g, const char* path) {
+    return api(c, [&] {
+        if (!g || !path) invalid("null pointer");
+        const uint64_t D = 2 * static_cast<uint64_t>(g->Mtilde);
+        std::vector<double> full(D * D * D);
+        double* tmp = buf<double>(c, "green_full", full.size());
+        launch_green_half_to_full(L0(c), static_cast<int>(D), g->d_half, tmp);
+        d2h(c, full.data(), tmp, full.size() * sizeof(double));
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw Error(FSE_ERUNTIME, std::string("save_mollified_green: cannot open ") + path);
+        const uint32_t version = 1;
+        const uint8_t kind = static_cast<uint8_t>(g->kind);
+        os.write("FSEG", 4);
+        os.write(reinterpret_cast<const char*>(&version), 4);
+        os.write(reinterpret_cast<const char*>(&kind), 1);
+        os.write(reinterpret_cast<const char*>(&g->Ltilde), 8);
+        os.write(reinterpret_cast<const char*>(&g->h), 8);
+        os.write(reinterpret_cast<const char*>(&g->R), 8);
+        for (int k = 0; k < 3; ++k) os.write(reinterpret_cast<const char*>(&D), 8);
+        os.write(reinterpret_cast<const char*>(full.data()),
+                 static_cast<std::streamsize>(full.size() * sizeof(double)));
+        if (!os) throw Error(FSE_ERUNTIME, std::string("save_mollified_green: write failed for ") + path);
+    });
+}
+
+// greens.cpp:173-203
+fse_status fse_cuda_green_load(fse_cuda_ctx* c, const char* path, fse_green** out) {
+    return api(c, [&] {
+        if (!path || !out) invalid("null pointer");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw Error(FSE_ERUNTIME, std::string("load_mollified_green: cannot open ") + path);
+        char magic[4];
+        is.read(magic, 4);
+        if (!is || std::memcmp(magic, "FSEG", 4) != 0)
+            throw Error(FSE_ERUNTIME, std::string("load_mollified_green: bad magic in ") + path);
+        uint32_t version = 0;
+        is.read(reinterpret_cast<char*>(&version), 4);
+        if (version != 1) throw Error(FSE_ERUNTIME, "load_mollified_green: unsupported version");
+        uint8_t kind = 0;
+        double Lt = 0, h = 0, R = 0;
+        uint64_t d[3] = {0, 0, 0};
+        is.read(reinterpret_cast<char*>(&kind), 1);
+        is.read(reinterpret_cast<char*>(&Lt), 8);
+        is.read(reinterpret_cast<char*>(&h), 8);
+        is.read(reinterpret_cast<char*>(&R), 8);
+        is.read(reinterpret_cast<char*>(d), 24);
+        if (!is || d[0] != d[1] || d[0] != d[2] || d[0] == 0 || d[0] % 2 != 0)
+            throw Error(FSE_ERUNTIME, "load_mollified_green: bad extents");
+        std::vector<double> full(d[0] * d[1] * d[2]);
+        is.read(reinterpret_cast<char*>(full.data()),
+                static_cast<std::streamsize>(full.size() * sizeof(double)));
+        if (!is) throw Error(FSE_ERUNTIME, "load_mollified_green: truncated payload");
+        const int Mt = static_cast<int>(d[0] / 2);
+        fse_green* g = new_green(c, kind, Lt, Mt, h, R);
+        double* tmp = buf<double>(c, "green_full", full.size());
+        h2d(c, tmp, full.data(), full.size() * sizeof(double));
+        launch_green_full_to_half(L0(c), static_cast<int>(d[0]), tmp, g->d_half);
+        FSE_CU(cudaStreamSynchronize(c->s0));
+        *out = g;
+    });
+}
+
+fse_status fse_cuda_total_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* pos,
+                              const double* str, int64_t n, double box_side, const double* targets,
+                              int64_t nt, int tas, const fse_green* green, double* u,
+                              fse_timings* tm) {
+    return api(c, [&] {
+        run_sum_host(c, cfg, kind, pos, str, n, box_side, targets, nt, tas, green, u, tm, true,
+                     true);
+    });
+}
+
+fse_status fse_cuda_total_sum_dev(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                  const double* d_pos, const double* d_str, int64_t n,
+                                  double box_side, const double* d_tgt, int64_t nt, int tas,
+                                  const fse_green* green, double* d_u, fse_timings* tm) {
+    return api(c, [&] {
+        run_sum(c, cfg, kind, d_pos, d_str, n, box_side, d_tgt, nt, tas, green, d_u, tm, true,
+                true);
+    });
+}
+
+fse_status fse_cuda_fourier_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                const double* pos, const double* str, int64_t n, double box_side,
+                                const double* targets, int64_t nt, const fse_green* green,
+                                double* u, fse_timings* tm) {
+    return api(c, [&] {
+        run_sum_host(c, cfg, kind, pos, str, n, box_side, targets, nt, -1, green, u, tm, true,
+                     false);
+    });
+}
+
+fse_status fse_cuda_real_space_sum(fse_cuda_ctx* c, int kind, const double* pos,
+                                   const double* str, int64_t n, double box_side, double xi,
+                                   double rc, const double* targets, int64_t nt, double* u) {
+    return api(c, [&] {
+        if (!(xi > 0) || !(rc > 0)) invalid("real_space_sum: xi and rc must be positive");
+        fse_config cfg;
+        std::memset(&cfg, 0, sizeof cfg);
+        cfg.xi = xi;
+        cfg.rc = rc;
+        run_sum_host(c, &cfg, kind, pos, str, n, box_side, targets, nt, -1, nullptr, u, nullptr,
+                     false, true);
+    });
+}
+
+fse_status fse_cuda_spread(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* pos,
+                           const double* str, int64_t n, double box_side, double* grid) {
+    return api(c, [&] {
+        check_kind(kind);
+        check_cfg(cfg);
+        if (std::abs(box_side - cfg->L) > 1e-12 * cfg->L)
+            invalid("spread: config box does not match system");
+        if (n < 0 || (n > 0 && (!pos || !str)) || !grid) invalid("null pointer");
+        const int a = arity_of(kind);
+        const GridParams g = make_grid_params(*cfg);
+        double* d_pos = buf<double>(c, "in_pos", 3 * n);
+        double* d_str = buf<double>(c, "in_str", a * n);
+        h2d(c, d_pos, pos, sizeof(double) * 3 * n);
+        h2d(c, d_str, str, sizeof(double) * a * n);
+        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+        double* qtab = buf<double>(c, "qtab", g.P);
+        launch_quad_table(L0(c), g, qtab);
+        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
+        double* X = buf<double>(c, "X", static_cast<size_t>(a) * g.comp);
+        FSE_CU(cudaMemsetAsync(X, 0, sizeof(double) * a * g.comp, c->s0));
+        for (int c0 = 0; c0 < a; c0 += 3)
+            launch_spread(L0(c), g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
+        const size_t vol = static_cast<size_t>(g.Mt) * g.Mt * g.Mt;
+        double* out = buf<double>(c, "grid_out", a * vol);
+        launch_extract_grid(L0(c), g, X, a, out);
+        raise_flags(c);
+        d2h(c, grid, out, sizeof(double) * a * vol);
+    });
+}
+
+fse_status fse_cuda_kspace_scale(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                 const fse_green* green, const double* ghat, double* out) {
+    return api(c, [&] {
+        check_kind(kind);
+        check_cfg(cfg);
+        check_green(cfg, kind, green);
+        if (!ghat || !out) invalid("null pointer");
+        const int a = arity_of(kind);
+        const GridParams g = make_grid_params(*cfg);
+        const size_t T = static_cast<size_t>(g.D) * g.D * g.D;
+        double* Gf = buf<double>(c, "ks_G", T);
+        double2* gh = buf<double2>(c, "ks_in", a * T);
+        double2* o = buf<double2>(c, "ks_out", 3 * T);
+        launch_green_half_to_full(L0(c), g.D, green->d_half, Gf);
+        h2d(c, gh, ghat, sizeof(double2) * a * T);
+        launch_kscale_full(L0(c), g, kind, Gf, gh, o);
+        d2h(c, out, o, sizeof(double2) * 3 * T);
+    });
+}
+
+fse_status fse_cuda_build_cell_list(fse_cuda_ctx* c, const double* pos, int64_t n,
+                                    double box_side, double rc, double pad, int* dims,
+                                    double* cell_side, double* origin, int64_t* bstart,
+                                    int64_t* perm) {
+    return api(c, [&] {
+        if (n < 0 || (n > 0 && !pos) || !dims || !cell_side || !origin) invalid("null pointer");
+        const CellGrid cg = cell_grid(n, box_side, rc, pad);
+        dims[0] = dims[1] = dims[2] = cg.dim;
+        *cell_side = cg.side;
+        *origin = cg.origin;
+        if (!bstart) return;
+        double* d_pos = buf<double>(c, "in_pos", 3 * n);
+        FSE_CU(cudaMemcpyAsync(d_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->s1));
+        Cells cl = bin_cells(c, cg, "rs_", d_pos, nullptr, 0, n);
+        int64_t* b64 = buf<int64_t>(c, "cl_b64", cg.ncell + 1);
+        int64_t* p64 = buf<int64_t>(c, "cl_p64", n);
+        launch_i32_to_i64(L1(c), cl.start, b64, cg.ncell + 1);
+        launch_u32_to_i64(L1(c), cl.perm, p64, n);
+        FSE_CU(cudaMemcpyAsync(bstart, b64, sizeof(int64_t) * (cg.ncell + 1),
+                               cudaMemcpyDeviceToHost, c->s1));
+        if (n > 0 && perm)
+            FSE_CU(cudaMemcpyAsync(perm, p64, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->s1));
+        FSE_CU(cudaStreamSynchronize(c->s1));
+    });
+}
+
+fse_status fse_cuda_support_index(fse_cuda_ctx* c, const fse_config* cfg, const double* pos,
+                                  int64_t n, int32_t* i0) {
+    return api(c, [&] {
+        check_cfg(cfg);
+        if (n < 0 || (n > 0 && (!pos || !i0))) invalid("null pointer");
+        const GridParams g = make_grid_params(*cfg);
+        double* d_pos = buf<double>(c, "in_pos", 3 * n);
+        int32_t* d_i0 = buf<int32_t>(c, "si_i0", 3 * n);
+        h2d(c, d_pos, pos, sizeof(double) * 3 * n);
+        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+        launch_support_keys(L0(c), g, d_pos, n, 0, nullptr, d_i0, c->d_flags);
+        d2h(c, i0, d_i0, sizeof(int32_t) * 3 * n);
+        raise_flags(c);
+    });
+}
+
+fse_status fse_cuda_direct_sum(fse_cuda_ctx* c, int kind, const double* pos, const double* str,
+                               int64_t n, const double* targets, int64_t nt, int exclude_self,
+                               double* u) {
+    return api(c, [&] {
+        check_kind(kind);
+        if (n < 0 || nt < 0 || (n > 0 && (!pos || !str)) || (nt > 0 && (!targets || !u)))
+            invalid("null pointer");
+        const int a = arity_of(kind);
+        double* d_pos = buf<double>(c, "in_pos", 3 * n);
+        double* d_str = buf<double>(c, "in_str", a * n);
+        double* d_tgt = buf<double>(c, "in_tgt", 3 * nt);
+        double* d_u = buf<double>(c, "in_u", 3 * nt);
+        h2d(c, d_pos, pos, sizeof(double) * 3 * n);
+        h2d(c, d_str, str, sizeof(double) * a * n);
+        h2d(c, d_tgt, targets, sizeof(double) * 3 * nt);
+        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+        launch_direct(L0(c), kind, d_pos, d_str, n, d_tgt, nt, exclude_self, d_u, c->d_flags);
+        raise_flags(c);
+        d2h(c, u, d_u, sizeof(double) * 3 * nt);
+    });
+}
+
+// fft.cpp:13-37 over cuFFT Z2Z (in place, inverse scaled by 1/(n0 n1 n2))
+fse_status fse_cuda_fft3d(fse_cuda_ctx* c, double* data, int n0, int n1, int n2, int inverse) {
+    return api(c, [&] {
+        if (!data || n0 < 1 || n1 < 1 || n2 < 1) invalid("fft3d: bad arguments");
+        const size_t n = static_cast<size_t>(n0) * n1 * n2;
+        double2* d = buf<double2>(c, "fft_data", n);
+        h2d(c, d, data, n * sizeof(double2));
+        cufftHandle p;
+        FSE_CUFFT(cufftPlan3d(&p, n0, n1, n2, CUFFT_Z2Z));
+        cufftSetStream(p, c->s0);
+        const cufftResult r = cufftExecZ2Z(p, reinterpret_cast<cufftDoubleComplex*>(d),
+                                           reinterpret_cast<cufftDoubleComplex*>(d),
+                                           inverse ? CUFFT_INVERSE : CUFFT_FORWARD);
+        if (r != CUFFT_SUCCESS) {
+            cufftDestroy(p);
+            throw_cufft(r, "cufftExecZ2Z", __FILE__, __LINE__);
+        }
+        if (inverse) launch_scale_complex(L0(c), d, static_cast<int64_t>(n), 1.0 / static_cast<double>(n));
+        d2h(c, data, d, n * sizeof(double2));
+        cufftDestroy(p);
+    });
+}
+
+}  // extern "C"
+
+static_assert(sizeof(fse_config) == 120, "fse_config must mirror fse::EwaldConfig (120 bytes)");
+static_assert(offsetof(fse_config, Mtilde) == 80, "EwaldConfig layout");
+static_assert(offsetof(fse_config, kinf) == 88, "EwaldConfig layout");
+static_assert(offsetof(fse_config, deterministic) == 112, "EwaldConfig layout");

@@ -1,0 +1,170 @@
+// fse_internal.cuh -- shared declarations of the B200 (sm_100a) free-space
+// Spectral Ewald library.  Host orchestration lives in fse_capi.cu; kernels
+// live in one .cu per stage.  Only plain device pointers cross these
+// interfaces; the C-ABI (include/fse_cuda.h) is the only public surface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "fse_cuda.h"
+
+namespace fsecu {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    fse_status code;
+    Error(fse_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+[[noreturn]] void throw_cufft(cufftResult r, const char* what, const char* file, int line);
+
+#define FSE_CU(x)                                                             \
+    do {                                                                      \
+        cudaError_t e_ = (x);                                                 \
+        if (e_ != cudaSuccess) ::fsecu::throw_cuda(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+#define FSE_CUFFT(x)                                                              \
+    do {                                                                          \
+        cufftResult r_ = (x);                                                     \
+        if (r_ != CUFFT_SUCCESS) ::fsecu::throw_cufft(r_, #x, __FILE__, __LINE__); \
+    } while (0)
+#define FSE_LAUNCH_CHECK() FSE_CU(cudaGetLastError())
+
+// device-side error flags (bit set => condition hit)
+enum : int {
+    FLAG_SUPPORT = 1,      // ewald.cpp:87-91 point support exceeds grid
+    FLAG_TARGET_BOX = 2,   // ewald.cpp:299-302 target outside [0,L]^3
+    FLAG_COINCIDENT = 4,   // kernels.cpp:79-80 coincident target/source
+};
+
+inline int arity_of(int kind) { return kind == FSE_STRESSLET ? 9 : 3; }
+
+// ------------------------------------------------------------ grid params
+// Everything a Fourier-stage kernel needs, derived once per evaluation from
+// fse_config exactly as the reference derives it (ewald.cpp:147,152-157,
+// 232-235, 351-357).
+struct GridParams {
+    int P;          // support
+    int Mt;         // Mtilde
+    int D;          // 2 Mtilde (FFT size, exact: SURVEY 8a A6)
+    int Dh;         // D/2 + 1 (half spectrum)
+    int64_t plane;  // doubles per x-plane of the real view: D * (D + 2)
+    int64_t comp;   // doubles per component buffer: D * D * (D + 2)
+    double h, origin, alpha, prefac, L;
+    double dk, inv4xi2, eta, invD3;
+    // spread/gather tiling of the support-start space (i0x, i0y, i0z)
+    int ncx, ncy, ncz;  // coarse tiles: 8 x 8 x 16
+    int64_t nkeys;      // ncx*ncy*ncz*8 fine keys (4 x 4 x 8 sub-tiles)
+};
+
+GridParams make_grid_params(const fse_config& cfg);
+
+// Device-side constant tables (per call, small): q[p] = exp(-alpha (p h)^2)
+// (ewald.cpp:154-156) lives in a device buffer passed to the weight kernel.
+
+// --------------------------------------------------------------- launches
+// Every launcher enqueues on `s` and bumps *launches by the number of kernels.
+struct Launch {
+    cudaStream_t s;
+    uint64_t* launches;
+};
+
+// k_particles.cu ------------------------------------------------------------
+// support start + tile key per point; flags FLAG_SUPPORT / FLAG_TARGET_BOX
+void launch_support_keys(const Launch& L, const GridParams& g, const double* pos, int64_t n,
+                         int check_box, uint32_t* key, int32_t* i0, int* flags);
+// q[p] table
+void launch_quad_table(const Launch& L, const GridParams& g, double* q);
+// sorted payload: i0s (n x 3), weights (n x 3P, prefac folded into x when
+// fold_prefac), strengths (a x n SoA), from perm
+void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
+                           const double* str, int a, const uint32_t* perm, int64_t n,
+                           const double* qtab, int32_t* i0s, double* w, double* fs,
+                           bool fold_prefac);
+// histogram of keys into counts (size nkeys, zeroed by caller)
+void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts);
+// cell ids of points for the reference cell list (realspace.cpp:60-63,80)
+void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
+                     int dim, uint32_t* cell);
+// SoA permute of positions (+ strengths) by perm
+void launch_permute_soa(const Launch& L, const double* pos, const double* str, int a,
+                        const uint32_t* perm, int64_t n, double* px, double* py, double* pz,
+                        double* fs);
+void launch_iota(const Launch& L, uint32_t* v, int64_t n);
+void launch_u32_to_i64(const Launch& L, const uint32_t* in, int64_t* out, int64_t n);
+void launch_i32_to_i64(const Launch& L, const int32_t* in, int64_t* out, int64_t n);
+
+// k_spread.cu ---------------------------------------------------------------
+// writes the Mt^3 grid of components [c0, c0+3) into X (real view, x-planes
+// of pitch plane, rows of pitch D+2)
+void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
+                   const double* fs, int64_t n, int a, int c0, const int32_t* tstart,
+                   double* X);
+// Mt^3 compact copy out of the real view (for the fse::spread API)
+void launch_extract_grid(const Launch& L, const GridParams& g, const double* X, int a,
+                         double* out);
+
+// k_kscale.cu ---------------------------------------------------------------
+// half-spectrum, Hermitian-exact (Nyquist-averaged) multiplier, 1/D^3 folded;
+// in place on X (a components in, 3 out)
+void launch_kscale_half(const Launch& L, const GridParams& g, int kind, const double* G,
+                        double2* X, int64_t comp_c);
+// full D^3 C2C, reference multiplier verbatim (ewald.cpp:216-293)
+void launch_kscale_full(const Launch& L, const GridParams& g, int kind, const double* Gfull,
+                        const double2* ghat, double2* out);
+void launch_scale_complex(const Launch& L, double2* data, int64_t n, double s);
+
+// k_gather.cu ---------------------------------------------------------------
+// groups of <= 8 targets per fine tile; group table built by caller
+void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
+                   const int32_t* tstart, const int32_t* gkey, const int32_t* goff,
+                   int64_t ngroups, const double* X, const uint32_t* perm, double scale,
+                   double* u);
+void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount);
+void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* goff,
+                        int64_t nkeys, int32_t* gkey);
+
+// k_realspace.cu ------------------------------------------------------------
+struct CellGrid {
+    int dim;
+    double origin, side;
+    int64_t ncell;
+};
+void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const double* spx,
+                      const double* spy, const double* spz, const double* sfs, int64_t ns,
+                      const int32_t* bstart, const double* tpx, const double* tpy,
+                      const double* tpz, const int32_t* tcell_start, const int32_t* items,
+                      int64_t nitems, const uint32_t* tperm, double xi, double rc, double* uR);
+void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
+                        int32_t* cnt);
+void launch_fill_items(const Launch& L, const int32_t* start, const int32_t* off, int64_t ncell,
+                       int per, int32_t* items);
+
+// epilogue: u[perm] = uF + uR (+ self) -------------------------------------
+// u = uF + uR (+ self_coef * f for the stokeslet self term), caller order
+void launch_epilogue(const Launch& L, int64_t nt, const double* uF, const double* uR,
+                     const double* str_self, double self_coef, double* u);
+
+// k_green.cu ----------------------------------------------------------------
+// fill the half spectrum (sM x sM x (sM/2+1)) of Hhat^R / Bhat^R (greens.cpp:62-79)
+void launch_green_fill(const Launch& L, int gkind, int sM, double dk, double R, double2* half);
+// window the (scaled) real sM^3 grid into the D^3 real view (pitch D+2) (greens.cpp:84-104)
+void launch_green_window(const Launch& L, int sM, int64_t sMpitch, int Mt, const double* grid,
+                         double scale, double* trunc);
+// keep the real part of the half spectrum
+void launch_green_real(const Launch& L, const double2* spec, int64_t n, double* G);
+// full <-> half conversions of the reference layout
+void launch_green_full_to_half(const Launch& L, int D, const double* full, double* half);
+void launch_green_half_to_full(const Launch& L, int D, const double* half, double* full);
+
+// k_direct.cu ---------------------------------------------------------------
+void launch_direct(const Launch& L, int kind, const double* pos, const double* str, int64_t n,
+                   const double* tgt, int64_t nt, int exclude_self, double* u, int* flags);
+
+}  // namespace fsecu

@@ -1,0 +1,295 @@
+// k_misc.cu -- epilogue of total_sum (ewald.cpp:403-410), the O(N NT)
+// direct sum (kernels.cpp:27-82), and the GPU precompute of the mollified
+// Green's function (greens.cpp:22-113).
+#include "fse_internal.cuh"
+
+namespace fsecu {
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline unsigned blocks_for(int64_t n, int tpb = TPB) {
+    return static_cast<unsigned>((n + tpb - 1) / tpb);
+}
+
+// u = (uF + uR) + self, in the reference's order (ewald.cpp:403, 408-410)
+__global__ void k_epilogue(int64_t nt, const double* __restrict__ uF,
+                           const double* __restrict__ uR, const double* __restrict__ str,
+                           double coef, double* __restrict__ u) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= 3 * nt) return;
+    double v = uF ? uF[q] : 0.0;
+    if (uR) v += uR[q];
+    if (str) v += coef * str[q];
+    u[q] = v;
+}
+
+// ---------------------------------------------------------------- direct sum
+template <int KIND>
+__device__ __forceinline__ void bare(double rx, double ry, double rz, const double* f,
+                                     double acc[3]) {
+    const double r2 = rx * rx + ry * ry + rz * rz;
+    const double rn = sqrt(r2);
+    if (KIND == FSE_STOKESLET) {
+        const double rf = rx * f[0] + ry * f[1] + rz * f[2];
+        const double a = 1.0 / rn, b = rf / (r2 * rn);
+        acc[0] += a * f[0] + b * rx;
+        acc[1] += a * f[1] + b * ry;
+        acc[2] += a * f[2] + b * rz;
+    } else if (KIND == FSE_STRESSLET) {
+        const double r[3] = {rx, ry, rz};
+        double rfr = 0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) rfr += r[l] * f[3 * l + m] * r[m];
+        const double c = -6.0 * rfr / (r2 * r2 * rn);
+        acc[0] += c * rx;
+        acc[1] += c * ry;
+        acc[2] += c * rz;
+    } else {
+        const double inv_r3 = 1.0 / (r2 * rn);
+        acc[0] += (f[1] * rz - f[2] * ry) * inv_r3;
+        acc[1] += (f[2] * rx - f[0] * rz) * inv_r3;
+        acc[2] += (f[0] * ry - f[1] * rx) * inv_r3;
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(TPB) k_direct(const double* __restrict__ pos,
+                                                const double* __restrict__ str, int64_t n,
+                                                const double* __restrict__ tgt, int64_t nt,
+                                                int exclude_self, double* __restrict__ u,
+                                                int* flags) {
+    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    __shared__ double sp[TPB][3];
+    __shared__ double sf[TPB][A];
+    const int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool valid = m < nt;
+    double x = 0, y = 0, z = 0;
+    if (valid) {
+        x = tgt[3 * m];
+        y = tgt[3 * m + 1];
+        z = tgt[3 * m + 2];
+    }
+    double acc[3] = {0, 0, 0};
+    bool coincident = false;
+    for (int64_t base = 0; base < n; base += TPB) {
+        const int64_t s = base + threadIdx.x;
+        if (s < n) {
+            sp[threadIdx.x][0] = pos[3 * s];
+            sp[threadIdx.x][1] = pos[3 * s + 1];
+            sp[threadIdx.x][2] = pos[3 * s + 2];
+#pragma unroll
+            for (int c = 0; c < A; ++c) sf[threadIdx.x][c] = str[s * A + c];
+        }
+        __syncthreads();
+        const int cnt = static_cast<int>(n - base < TPB ? n - base : TPB);
+        if (valid)
+            for (int j = 0; j < cnt; ++j) {
+                if (exclude_self && base + j == m) continue;
+                const double rx = x - sp[j][0], ry = y - sp[j][1], rz = z - sp[j][2];
+                if (rx == 0 && ry == 0 && rz == 0) {
+                    coincident = true;
+                    continue;
+                }
+                bare<KIND>(rx, ry, rz, sf[j], acc);
+            }
+        __syncthreads();
+    }
+    if (coincident) atomicOr(flags, FLAG_COINCIDENT);
+    if (valid) {
+        u[3 * m] = acc[0];
+        u[3 * m + 1] = acc[1];
+        u[3 * m + 2] = acc[2];
+    }
+}
+
+// ------------------------------------------------------------------- Green
+__device__ double d_sinc(double x) {
+    if (fabs(x) < 1e-8) return 1.0 - x * x / 6.0;
+    return sin(x) / x;
+}
+
+// greens.cpp:22-26
+__device__ double d_hhat(double k, double R) {
+    const double s = d_sinc(0.5 * R * k);
+    return 2.0 * M_PI * R * R * s * s;
+}
+
+// greens.cpp:28-46.  The reference evaluates Rk >= 0.5 in x87 long double;
+// there is no long double on the GPU, so 0.5 <= Rk < 2 uses the convergent
+// alternating series  Bhat/(pi R^4) = sum_m c_m (Rk)^{2m},
+//   c_m = 4 (-1)^m (2m+3)(2m+2)/(2m+4)!  (c_0..c_6 are the reference's own
+// coefficients), which has no cancellation there, and Rk >= 2 the closed form
+// in double (cancellation <= 2 bits).  Rk < 0.5 is the reference's series.
+__device__ double d_bhat(double k, double R) {
+    const double t = R * k;
+    const double piR4 = M_PI * R * R * R * R;
+    if (t < 0.5) {
+        const double t2 = t * t;
+        return piR4 * (1.0 + t2 * (-1.0 / 9.0 + t2 * (1.0 / 240.0 +
+                       t2 * (-1.0 / 12600.0 + t2 * (1.0 / 1088640.0 +
+                       t2 * (-1.0 / 139708800.0 + t2 / 24908083200.0))))));
+    }
+    if (t < 2.0) {
+        constexpr int NT = 16;
+        double c[NT];
+        c[0] = 1.0;
+        for (int m = 0; m + 1 < NT; ++m)
+            c[m + 1] = -c[m] * (2.0 * m + 4.0) / ((2.0 * m + 2.0) * (2.0 * m + 3.0) * (2.0 * m + 6.0));
+        const double t2 = t * t;
+        double acc = c[NT - 1];
+        for (int m = NT - 2; m >= 0; --m) acc = acc * t2 + c[m];
+        return piR4 * acc;
+    }
+    const double num = (2.0 - t * t) * cos(t) + 2.0 * t * sin(t) - 2.0;
+    return 4.0 * M_PI * num / (t * t * t * t) * (R * R * R * R);
+}
+
+// half spectrum of the sM^3 grid, (greens.cpp:62-79): k2(a) = (dk n_a)^2,
+// k = sqrt((k2(i) + k2(j)) + k2(l))
+__global__ void k_green_fill(int gkind, int sM, double dk, double R, double2* __restrict__ half) {
+    const int sh = sM / 2 + 1;
+    const int64_t tot = static_cast<int64_t>(sM) * sM * sh;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
+         q += stride) {
+        const int l = static_cast<int>(q % sh);
+        const int j = static_cast<int>((q / sh) % sM);
+        const int i = static_cast<int>(q / (static_cast<int64_t>(sh) * sM));
+        const int ni = i < sM / 2 ? i : i - sM, nj = j < sM / 2 ? j : j - sM,
+                  nl = l < sM / 2 ? l : l - sM;
+        const double ki = dk * ni, kj = dk * nj, kl = dk * nl;
+        const double k2ij = ki * ki + kj * kj;
+        const double k = sqrt(k2ij + kl * kl);
+        half[q] = make_double2(gkind == FSE_HARMONIC ? d_hhat(k, R) : d_bhat(k, R), 0.0);
+    }
+}
+
+// (greens.cpp:94-104): doubled-grid index p -> signed offset (p < Mt ? p : p - D)
+// -> oversampled index; real sM^3 grid has row pitch sMpitch
+__global__ void k_green_window(int sM, int64_t sMpitch, int Mt, const double* __restrict__ grid,
+                               double scale, double* __restrict__ trunc) {
+    const int D = 2 * Mt;
+    const int64_t tot = static_cast<int64_t>(D) * D * D;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
+         q += stride) {
+        const int l = static_cast<int>(q % D);
+        const int j = static_cast<int>((q / D) % D);
+        const int i = static_cast<int>(q / (static_cast<int64_t>(D) * D));
+        auto src = [&](int p) {
+            const int off = p < Mt ? p : p - D;
+            return off >= 0 ? off : off + sM;
+        };
+        const double v = grid[(static_cast<int64_t>(src(i)) * sM + src(j)) * sMpitch + src(l)];
+        trunc[(static_cast<int64_t>(i) * D + j) * (D + 2) + l] = v * scale;
+    }
+}
+
+__global__ void k_green_real(const double2* __restrict__ spec, int64_t n, double* __restrict__ G) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
+         q += stride)
+        G[q] = spec[q].x;
+}
+
+__global__ void k_full_to_half(int D, const double* __restrict__ full, double* __restrict__ half) {
+    const int Dh = D / 2 + 1;
+    const int64_t tot = static_cast<int64_t>(D) * D * Dh;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
+         q += stride) {
+        const int64_t l = q % Dh, ij = q / Dh;
+        half[q] = full[ij * D + l];
+    }
+}
+
+// the table is even in k, so entries with l > D/2 mirror (-i, -j, -l)
+__global__ void k_half_to_full(int D, const double* __restrict__ half, double* __restrict__ full) {
+    const int Dh = D / 2 + 1;
+    const int64_t tot = static_cast<int64_t>(D) * D * D;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
+         q += stride) {
+        int l = static_cast<int>(q % D);
+        int j = static_cast<int>((q / D) % D);
+        int i = static_cast<int>(q / (static_cast<int64_t>(D) * D));
+        if (l >= Dh) {
+            l = D - l;
+            j = (D - j) % D;
+            i = (D - i) % D;
+        }
+        full[q] = half[(static_cast<int64_t>(i) * D + j) * Dh + l];
+    }
+}
+
+unsigned grid_stride_blocks(int64_t n) {
+    int64_t b = (n + TPB - 1) / TPB;
+    const int64_t cap = 148 * 32;
+    return static_cast<unsigned>(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+
+void launch_epilogue(const Launch& L, int64_t nt, const double* uF, const double* uR,
+                     const double* str_self, double self_coef, double* u) {
+    if (nt <= 0) return;
+    k_epilogue<<<blocks_for(3 * nt), TPB, 0, L.s>>>(nt, uF, uR, str_self, self_coef, u);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_direct(const Launch& L, int kind, const double* pos, const double* str, int64_t n,
+                   const double* tgt, int64_t nt, int exclude_self, double* u, int* flags) {
+    if (nt <= 0) return;
+    const unsigned b = blocks_for(nt);
+    if (kind == FSE_STOKESLET)
+        k_direct<FSE_STOKESLET><<<b, TPB, 0, L.s>>>(pos, str, n, tgt, nt, exclude_self, u, flags);
+    else if (kind == FSE_STRESSLET)
+        k_direct<FSE_STRESSLET><<<b, TPB, 0, L.s>>>(pos, str, n, tgt, nt, exclude_self, u, flags);
+    else
+        k_direct<FSE_ROTLET><<<b, TPB, 0, L.s>>>(pos, str, n, tgt, nt, exclude_self, u, flags);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_green_fill(const Launch& L, int gkind, int sM, double dk, double R, double2* half) {
+    const int64_t tot = static_cast<int64_t>(sM) * sM * (sM / 2 + 1);
+    k_green_fill<<<grid_stride_blocks(tot), TPB, 0, L.s>>>(gkind, sM, dk, R, half);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_green_window(const Launch& L, int sM, int64_t sMpitch, int Mt, const double* grid,
+                         double scale, double* trunc) {
+    const int64_t D = 2 * Mt;
+    k_green_window<<<grid_stride_blocks(D * D * D), TPB, 0, L.s>>>(sM, sMpitch, Mt, grid, scale,
+                                                                   trunc);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_green_real(const Launch& L, const double2* spec, int64_t n, double* G) {
+    k_green_real<<<grid_stride_blocks(n), TPB, 0, L.s>>>(spec, n, G);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_green_full_to_half(const Launch& L, int D, const double* full, double* half) {
+    const int64_t n = static_cast<int64_t>(D) * D * (D / 2 + 1);
+    k_full_to_half<<<grid_stride_blocks(n), TPB, 0, L.s>>>(D, full, half);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_green_half_to_full(const Launch& L, int D, const double* half, double* full) {
+    const int64_t n = static_cast<int64_t>(D) * D * D;
+    k_half_to_full<<<grid_stride_blocks(n), TPB, 0, L.s>>>(D, half, full);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+}  // namespace fsecu

@@ -1,0 +1,216 @@
+// k_particles.cu -- per-point preparation kernels (HBM-bound, one thread per
+// point): support start indices and tile keys, the FGG axis weights in
+// tile-sorted order, cell ids for the real-space cell list, SoA permutes.
+//
+// Bit-exactness: i0 = (int)ceil((x - origin)/h - P/2) (ewald.cpp:38-39) and
+// cell = clamp(floor((x - origin)/side)) (realspace.cpp:60-63) are computed
+// with explicitly rounded IEEE ops (__dsub_rn/__ddiv_rn), so they match the
+// reference's x86-64 doubles exactly.
+#include "fse_internal.cuh"
+
+namespace fsecu {
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline unsigned blocks_for(int64_t n, int tpb = TPB) {
+    return static_cast<unsigned>((n + tpb - 1) / tpb);
+}
+
+__device__ __forceinline__ int support_start(double x, double origin, double h, int P) {
+    const double s = __ddiv_rn(__dsub_rn(x, origin), h);
+    return static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
+}
+
+__global__ void k_support_keys(GridParams g, const double* __restrict__ pos, int64_t n,
+                               int check_box, uint32_t* __restrict__ key,
+                               int32_t* __restrict__ i0out, int* __restrict__ flags) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= n) return;
+    int ii[3];
+    bool bad = false, outside = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = pos[3 * q + a];
+        if (!(x >= 0.0 && x <= g.L)) outside = true;
+        int f = support_start(x, g.origin, g.h, g.P);
+        if (f < 0 || f + g.P > g.Mt || x != x) {
+            bad = true;
+            f = f < 0 ? 0 : g.Mt - g.P;
+        }
+        ii[a] = f;
+    }
+    if (check_box && outside) atomicOr(flags, FLAG_TARGET_BOX);
+    if (bad) atomicOr(flags, FLAG_SUPPORT);
+    if (i0out) {
+        i0out[3 * q] = ii[0];
+        i0out[3 * q + 1] = ii[1];
+        i0out[3 * q + 2] = ii[2];
+    }
+    if (key) {
+        const uint32_t cx = ii[0] >> 3, cy = ii[1] >> 3, cz = ii[2] >> 4;
+        const uint32_t coarse = (cx * g.ncy + cy) * g.ncz + cz;
+        const uint32_t fine = (((ii[0] >> 2) & 1) << 2) | (((ii[1] >> 2) & 1) << 1) |
+                              ((ii[2] >> 3) & 1);
+        key[q] = coarse * 8u + fine;
+    }
+}
+
+__global__ void k_quad_table(GridParams g, double* q) {
+    const int p = threadIdx.x;
+    if (p < g.P) q[p] = exp(-g.alpha * (p * g.h) * (p * g.h));  // ewald.cpp:154-156
+}
+
+// FGG axis weights (ewald.cpp:33-51) for point perm[q], stored at sorted slot q.
+__global__ void k_payload(GridParams g, const double* __restrict__ pos,
+                          const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
+                          int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
+                          double* __restrict__ w, double* __restrict__ fs, bool fold_prefac) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= n) return;
+    const int64_t idx = perm[q];
+    const int P = g.P;
+    double* wq = w + q * 3 * P;
+#pragma unroll 1
+    for (int ax = 0; ax < 3; ++ax) {
+        const double x = pos[3 * idx + ax];
+        const double s = __ddiv_rn(__dsub_rn(x, g.origin), g.h);
+        int first = static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
+        const double x0 = (first - s) * g.h;
+        const double e0 = exp(-g.alpha * x0 * x0);
+        const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
+        const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
+        double r = 1.0;
+        for (int p = 0; p < P; ++p) {
+            wq[ax * P + p] = scale * (e0 * r * qtab[p]);
+            r *= ratio;
+        }
+        if (first < 0) first = 0;
+        if (first + P > g.Mt) first = g.Mt - P;
+        i0s[3 * q + ax] = first;
+    }
+    if (fs)
+        for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
+}
+
+__global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q < n) atomicAdd(&counts[keys[q]], 1);
+}
+
+__global__ void k_cell_ids(const double* __restrict__ pos, int64_t n, double origin, double side,
+                           int dim, uint32_t* __restrict__ cell) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= n) return;
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int v = static_cast<int>(floor(__ddiv_rn(__dsub_rn(pos[3 * q + a], origin), side)));
+        c[a] = v < 0 ? 0 : (v > dim - 1 ? dim - 1 : v);
+    }
+    cell[q] = (static_cast<uint32_t>(c[0]) * dim + c[1]) * dim + c[2];
+}
+
+__global__ void k_permute_soa(const double* __restrict__ pos, const double* __restrict__ str,
+                              int a, const uint32_t* __restrict__ perm, int64_t n,
+                              double* __restrict__ px, double* __restrict__ py,
+                              double* __restrict__ pz, double* __restrict__ fs) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= n) return;
+    const int64_t idx = perm[q];
+    px[q] = pos[3 * idx];
+    py[q] = pos[3 * idx + 1];
+    pz[q] = pos[3 * idx + 2];
+    if (fs)
+        for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
+}
+
+__global__ void k_iota(uint32_t* v, int64_t n) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q < n) v[q] = static_cast<uint32_t>(q);
+}
+
+__global__ void k_u32_to_i64(const uint32_t* in, int64_t* out, int64_t n) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q < n) out[q] = in[q];
+}
+
+__global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q < n) out[q] = in[q];
+}
+
+}  // namespace
+
+void launch_support_keys(const Launch& L, const GridParams& g, const double* pos, int64_t n,
+                         int check_box, uint32_t* key, int32_t* i0, int* flags) {
+    if (n <= 0) return;
+    k_support_keys<<<blocks_for(n), TPB, 0, L.s>>>(g, pos, n, check_box, key, i0, flags);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_quad_table(const Launch& L, const GridParams& g, double* q) {
+    k_quad_table<<<1, 128, 0, L.s>>>(g, q);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
+                           const double* str, int a, const uint32_t* perm, int64_t n,
+                           const double* qtab, int32_t* i0s, double* w, double* fs,
+                           bool fold_prefac) {
+    if (n <= 0) return;
+    k_payload<<<blocks_for(n, 128), 128, 0, L.s>>>(g, pos, str, a, perm, n, qtab, i0s, w, fs,
+                                                   fold_prefac);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts) {
+    if (n <= 0) return;
+    k_histogram<<<blocks_for(n), TPB, 0, L.s>>>(keys, n, counts);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
+                     int dim, uint32_t* cell) {
+    if (n <= 0) return;
+    k_cell_ids<<<blocks_for(n), TPB, 0, L.s>>>(pos, n, origin, side, dim, cell);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_permute_soa(const Launch& L, const double* pos, const double* str, int a,
+                        const uint32_t* perm, int64_t n, double* px, double* py, double* pz,
+                        double* fs) {
+    if (n <= 0) return;
+    k_permute_soa<<<blocks_for(n), TPB, 0, L.s>>>(pos, str, a, perm, n, px, py, pz, fs);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_iota(const Launch& L, uint32_t* v, int64_t n) {
+    if (n <= 0) return;
+    k_iota<<<blocks_for(n), TPB, 0, L.s>>>(v, n);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_u32_to_i64(const Launch& L, const uint32_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    k_u32_to_i64<<<blocks_for(n), TPB, 0, L.s>>>(in, out, n);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_i32_to_i64(const Launch& L, const int32_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    k_i32_to_i64<<<blocks_for(n), TPB, 0, L.s>>>(in, out, n);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+}  // namespace fsecu
