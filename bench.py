@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 free-space Spectral Ewald hot path (fse::total_sum).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2] [--no-cpu-baseline]
+
+A step = one fse::total_sum (spread -> FFT -> k-space scale -> IFFT ->
+quadrature, plus the real-space pair sum and the self term) over the whole
+synthetic workload.  Default workload: BASELINE.json configs[1] ("cfg2"):
+stokeslet, N = NT = 1e6 uniform in [0,1)^3, N(0,1) forces, xi=110, rc=0.045,
+M=288, P=24 (Mtilde=312, FFT grid D=624).
+
+value : targets/s, inputs resident in HBM, CUDA events on the context stream
+        over exactly K steps (fse_cuda_total_sum_dev), max over ranks;
+e2e   : targets/s through the reference-facing C-ABI call with HOST buffers
+        (fse_cuda_total_sum, pinned inputs): H2D of positions+forces and D2H
+        of the velocities inside the timed region, wall clock;
+roofline : the dominant kernel of the step, achieved = algorithmic bytes or
+        flops per launch / its CUDA-event duration;
+cpu_baseline : the reference compiled from its own sources (oracle/_ref) on a
+        bounded same-density sample, rank 0, N=1 only.
+
+N > 1 (torchrun): every rank runs the full workload on its own GPU (replicas,
+weak scaling; the z-slab decomposition is the next multi-GPU step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs (kind, generator, N, xi, rc, M, P, distinct targets)
+WORKLOADS = {
+    "cfg1": dict(kind=0, wl=1, n=10_000, xi=28.0, rc=0.15, M=80, P=16, tol=1e-8,
+                 desc="stokeslet N=1e4 uniform [0,1)^3, xi=28 rc=0.15 M=80 P=16"),
+    "cfg2": dict(kind=0, wl=1, n=1_000_000, xi=110.0, rc=0.045, M=288, P=24, tol=1e-10,
+                 desc="stokeslet N=1e6 uniform [0,1)^3, xi=110 rc=0.045 M=288 P=24"),
+    "cfg3": dict(kind=1, wl=3, n=100_000, xi=40.0, rc=0.12, M=128, P=20, tol=1e-8,
+                 desc="stresslet N=1e5 on the sphere r=0.5, xi=40 rc=0.12 M=128 P=20"),
+    "cfg4": dict(kind=2, wl=4, n=1_000_000, xi=110.0, rc=0.045, M=288, P=24, tol=1e-10,
+                 desc="rotlet N=1e6 in 32 Gaussian blobs sigma=0.03, xi=110 rc=0.045 M=288 P=24"),
+    "cfg5": dict(kind=0, wl=5, n=8_000_000, xi=220.0, rc=0.022, M=576, P=24, tol=1e-10,
+                 desc="stokeslet N=8e6 + 8e6 distinct targets uniform, xi=220 rc=0.022 M=576 P=24"),
+}
+KIND_NAMES = ["stokeslet", "stresslet", "rotlet"]
+SEED = 20260101
+
+
+def metric_name(w):
+    return (f"{KIND_NAMES[w['kind']]} targets/sec at N={w['n']:.0e}, fp64 tol {w['tol']:.0e}, "
+            "1/2/4/8 B200; % of roofline")
+
+
+# ------------------------------------------------------------------ dist
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as td
+            self.torch, self.td = torch, td
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            td.init_process_group(backend=backend)
+            self.dev = torch.device("cuda", self.local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ roofline
+def peaks():
+    p = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        if m.get("hbm_gbs"):
+            p = {"hbm_gbs": float(m["hbm_gbs"]), "hbm_src": "measured (MEASURED_PEAKS.json)"}
+    return p
+
+
+def stage_models(w, cfg, n, nt):
+    """Algorithmic work per launch: flops or bytes."""
+    a = 9 if w["kind"] == 1 else 3
+    P, D = cfg.P, cfg.D
+    H = D * D * (D // 2 + 1)
+    Mt = cfg.Mtilde
+    return {
+        # FP64 FMA-bound: 2 a P^3 flops per source, 2*3 P^3 per target
+        "spread": ("fp64", 2.0 * a * P ** 3 * n),
+        "gather": ("fp64", 2.0 * 3 * P ** 3 * nt),
+        # HBM-bound: one read+write per transform of the real grid and half spectrum,
+        # pruned forward (only Mtilde of D x-planes carry data in the 2D pass)
+        "fft_forward": ("hbm", a * (8.0 * Mt * D * (D + 2) * 2 + 16.0 * H * 2)),
+        "fft_inverse": ("hbm", 3 * (8.0 * Mt * D * (D + 2) * 2 + 16.0 * H * 2)),
+        "kscale": ("hbm", H * (16.0 * a + 8 + 48)),
+    }
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, dist: Dist):
+    import paper_1607_04808_b200 as fse
+
+    w = WORKLOADS[args.workload]
+    ctx = fse.Context(dist.local)
+    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED + dist.rank)
+    targets = system.positions if tgt is None else tgt
+    n, nt = system.size(), targets.shape[0]
+    tas = 1 if tgt is None else 0
+    cfg = fse.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    t0 = time.perf_counter()
+    green = ctx.precompute_mollified_green(int(fse.green_kind_for(w["kind"])), cfg.Ltilde,
+                                           cfg.Mtilde, cfg.sf)
+    precompute_s = time.perf_counter() - t0
+
+    # inputs resident in HBM
+    a = system.strengths.shape[1]
+    d_pos = ctx.dev_alloc(system.positions.nbytes)
+    d_str = ctx.dev_alloc(system.strengths.nbytes)
+    d_tgt = d_pos if tas else ctx.dev_alloc(targets.nbytes)
+    d_u = ctx.dev_alloc(8 * 3 * nt)
+    ctx.memcpy(d_pos, system.positions.ctypes.data, system.positions.nbytes)
+    ctx.memcpy(d_str, system.strengths.ctypes.data, system.strengths.nbytes)
+    if not tas:
+        ctx.memcpy(d_tgt, targets.ctypes.data, targets.nbytes)
+
+    def step(tm=None):
+        ctx.total_sum_dev(cfg, w["kind"], d_pos, d_str, n, 1.0, d_tgt, nt, green, d_u,
+                          targets_are_sources=tas, timings=tm)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.launch_count
+    kms = np.zeros(11)
+    tm = fse.StageTimings()
+    ctx.mark()
+    for _ in range(args.steps):
+        step(tm)
+        kms += np.array(ctx.kernel_ms())
+    ctx.mark()
+    dev_ms = ctx.elapsed_ms()
+    launches = ctx.launch_count - launches0
+    clk = clocks.stop()
+    dist.barrier()
+    max_ms = dist.max(dev_ms)
+    kms /= args.steps
+
+    # e2e through the host-buffer C-ABI call, pinned inputs
+    hp = ctx.host_alloc(system.positions.shape)
+    hs = ctx.host_alloc(system.strengths.shape)
+    hp[...] = system.positions
+    hs[...] = system.strengths
+    hsys = fse.SourceSystem(hp, hs, 1.0)
+    ht = hp if tas else ctx.host_alloc(targets.shape)
+    if not tas:
+        ht[...] = targets
+    ctx.total_sum(hsys, w["kind"], cfg, ht, green, targets_are_sources=tas)  # warm
+    dist.barrier()
+    e2e_steps = max(1, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        u_host = ctx.total_sum(hsys, w["kind"], cfg, ht, green, targets_are_sources=tas)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    h2d = hp.nbytes + hs.nbytes + (0 if tas else ht.nbytes)
+    d2h = u_host.nbytes
+
+    # roofline of the dominant kernel
+    names = ["spread", "fft_forward", "kscale", "fft_inverse", "gather", "realspace"]
+    stage_ms = {"source_prep": kms[0], "spectrum_memset": kms[1], "spread": kms[2],
+                "fft_forward": kms[3], "kscale": kms[4], "fft_inverse": kms[5],
+                "target_prep": kms[6], "gather": kms[7], "realspace_binning": kms[8],
+                "realspace": kms[9], "call": kms[10]}
+    models = stage_models(w, cfg, n, nt)
+    pk = peaks()
+    fp64_peak = args.fp64_peak
+    if fp64_peak is None:
+        fp64_peak = ctx.measure_fp64_peak()
+    stage_roof = {}
+    for nm in names:
+        if nm not in models or stage_ms[nm] <= 0:
+            continue
+        bound, work = models[nm]
+        if bound == "hbm":
+            ach = work / (stage_ms[nm] * 1e-3) / 1e9
+            stage_roof[nm] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"],
+                              "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
+        else:
+            ach = work / (stage_ms[nm] * 1e-3) / 1e12
+            stage_roof[nm] = {"bound": "fp64", "achieved": ach, "peak": fp64_peak,
+                              "unit": "TFLOP/s", "frac": ach / fp64_peak}
+    dom = max((nm for nm in names if stage_ms.get(nm, 0) > 0 and nm in stage_roof),
+              key=lambda k: stage_ms[k])
+    roof = dict(stage_roof[dom])
+    roof["kernel"] = dom
+    roof["ms"] = stage_ms[dom]
+    roof["peak_src"] = pk["hbm_src"] if roof["bound"] == "hbm" else \
+        "measured in this run (DFMA loop, fse_cuda_fp64_peak)"
+    roof["traffic"] = traffic_for(dom)
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(w, frac=8, threads=None)
+
+    value = dist.world * nt * args.steps / (max_ms * 1e-3)
+    line = {
+        "metric": metric_name(w), "value": value, "unit": "targets/s", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}+rank), "
+                "no dataset",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
+                   "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
+                   "eta": round(cfg.eta, 4), "parallelism": f"replicas x{dist.world}",
+                   "l2": "working set (3 x 1.95 GB spectrum + 0.6 GB weights) >> 126 MB L2; "
+                         "no flush needed",
+                   "green_precompute_s": round(precompute_s, 3)},
+        "e2e": {"value": nt * e2e_steps * dist.world / e2e_s, "unit": "targets/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "fse_cuda_total_sum (host buffers, pinned)"},
+        "roofline": roof,
+        "stage_roofline": stage_roof,
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "stage_timings_s": {k: v / args.steps for k, v in tm.as_dict().items()},
+        "gpu_launches": int(launches),
+        "gpu_launches_note": "our kernels (cuFFT library launches not counted)",
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    if dist.rank == 0:
+        print(json.dumps(line))
+    for p in (d_pos, d_str, d_u) + (() if tas else (d_tgt,)):
+        ctx.dev_free(p)
+
+
+def traffic_for(kernel: str):
+    """dram bytes per launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        t = json.load(f)
+    return t.get(kernel)
+
+
+# ------------------------------------------------------------------ reference CPU
+def _avail_bytes():
+    try:
+        import psutil
+        return psutil.virtual_memory().available
+    except Exception:
+        return 16 << 30
+
+
+def cpu_reference_sample(w, frac: int, threads):
+    """Time the reference (oracle/_ref: its own sources, OpenMP) on a same-density
+    sub-box of the workload: N/frac points in a box of side L/frac^(1/3) with the same
+    h, xi, rc, P (so spreading, quadrature and real-space work per point are those of
+    the full run) and extrapolate each StageTimings field: per-point stages x frac,
+    FFT x (D^3 log D^3 ratio), scale x (D^3 ratio)."""
+    from oracle import refimpl as R
+    if not R.available():
+        return {"value": None, "unit": "targets/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    side = frac ** (-1.0 / 3.0)
+    Ms = int(round(w["M"] * side))
+    side = Ms / w["M"]  # keep h identical
+    kind = w["kind"]
+    import paper_1607_04808_b200 as fse
+    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED)
+    pos = system.positions
+    inside = np.all(pos < side, axis=1)
+    pos = pos[inside]
+    st = system.strengths[inside]
+    nts = pos.shape[0]
+    cfg_s = R.make_config(side, w["xi"], w["rc"], Ms, w["P"])
+    cfg_f = R.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    cores = os.cpu_count() or 1
+    grid_bytes = 8 * (9 if kind == 1 else 3) * cfg_s.Mtilde ** 3
+    cap = max(1, int(0.4 * _avail_bytes() / max(grid_bytes, 1)))
+    nthr = threads or min(cores, cap)
+    R.set_threads(nthr)
+    green = np.zeros((cfg_s.D,) * 3)
+    green[0, 0, 0] = 1.0  # timing only: the table's values do not change the work
+    tsum = {}
+    tgt_s = pos if tgt is None else np.ascontiguousarray(tgt[np.all(tgt < side, axis=1)])
+    R.total_sum(cfg_s, kind, pos, st, tgt_s, green, timings=tsum)
+    Ds, Df = cfg_s.D, cfg_f.D
+    fft_scale = (Df ** 3 * math.log(Df ** 3)) / (Ds ** 3 * math.log(Ds ** 3))
+    n_full = w["n"]
+    per_pt = n_full / nts
+    est = (tsum["spread"] * per_pt + tsum["quadrature"] * (n_full / tgt_s.shape[0]) +
+           tsum["realspace"] * (n_full / tgt_s.shape[0]) + tsum["fft"] * fft_scale +
+           tsum["scale"] * (Df / Ds) ** 3)
+    return {"value": n_full / est, "unit": "targets/s", "cores": nthr, "kind": "reference",
+            "sample": (f"reference total_sum on a same-density sub-box: N={nts} points, "
+                       f"L={side:.4f}, M={Ms} (Mtilde={cfg_s.Mtilde}, D={Ds}), same h/xi/rc/P; "
+                       f"stages extrapolated to N={n_full}, D={Df}: per-point x{per_pt:.2f}, "
+                       f"fft x{fft_scale:.2f} (n log n), scale x{(Df / Ds) ** 3:.2f}; "
+                       "FFT single-threaded as the reference is written (FFTW-API shim)"),
+            "sample_seconds": tsum["total"],
+            "stages_s_extrapolated": {"spread": tsum["spread"] * per_pt,
+                                      "fft": tsum["fft"] * fft_scale,
+                                      "scale": tsum["scale"] * (Df / Ds) ** 3,
+                                      "quadrature": tsum["quadrature"] * per_pt,
+                                      "realspace": tsum["realspace"] * per_pt},
+            "est_total_s": est}
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(w, frac=args.ref_frac, threads=None)
+        if r["value"] is None:
+            print(json.dumps({"impl": "reference", "unavailable": r["sample"]}))
+            return
+        if i >= args.warmup:
+            vals.append(r["est_total_s"])
+        info = r
+    t = float(np.mean(vals))
+    v = w["n"] / t
+    info = dict(info)
+    info["value"] = v
+    line = {
+        "impl": "reference", "metric": metric_name(w), "value": v, "unit": "targets/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (seed {SEED})",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
+                   "parallelism": "host CPU (OpenMP), rank 0 only"},
+        "cpu_baseline": info,
+        "e2e": {"value": v, "unit": "targets/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-frac", type=int, default=64,
+                    help="--impl reference: sample = 1/ref_frac of the points per step")
+    ap.add_argument("--fp64-peak", type=float, default=None,
+                    help="TFLOP/s; default: measured in-run with a DFMA loop")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

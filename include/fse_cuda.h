@@ -90,6 +90,13 @@ fse_status fse_cuda_mark(fse_cuda_ctx* ctx);
 fse_status fse_cuda_elapsed_ms(fse_cuda_ctx* ctx, double* ms);
 /* number of kernels this library launched on the context since creation */
 uint64_t fse_cuda_launch_count(const fse_cuda_ctx* ctx);
+/* device time (ms) of the stages of the last total/fourier/real sum, CUDA events on the
+ * launching streams: [0] source prep (support keys, sort, weights) [1] spectrum memset
+ * [2] spread kernel [3] forward FFTs [4] k-space scale [5] inverse FFTs [6] target prep
+ * [7] gather kernel [8] real-space binning [9] real-space pair kernel [10] whole call */
+fse_status fse_cuda_kernel_ms(fse_cuda_ctx* ctx, double* out, int n);
+/* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
+fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);
 
 /* ---- config: replaces fse::make_config (ewald.cpp:103-134) -------------- */
 fse_status fse_make_config(double L, double xi, double rc, int M, int P, double sf,

@@ -211,6 +211,8 @@ def _load():
         lib.fse_cuda_mark.argtypes = [vp]
         lib.fse_cuda_elapsed_ms.argtypes = [vp, _dp]
         lib.fse_cuda_trim.argtypes = [vp]
+        lib.fse_cuda_kernel_ms.argtypes = [vp, _dp, C.c_int]
+        lib.fse_cuda_fp64_peak.argtypes = [vp, _dp]
         lib.fse_generate_system.argtypes = [C.c_int, i64, C.c_double, C.c_uint64, _dp, _dp]
         lib.fse_generate_workload.argtypes = [C.c_int, i64, C.c_uint64, _dp, _dp, _dp]
         _lib = lib
@@ -325,6 +327,17 @@ class Context:
 
     def trim(self):
         self._call(_load().fse_cuda_trim)
+
+    def kernel_ms(self):
+        """Per-stage device ms of the last sum (see fse_cuda_kernel_ms)."""
+        out = np.zeros(11)
+        self._call(_load().fse_cuda_kernel_ms, _p(out), 11)
+        return out.tolist()
+
+    def measure_fp64_peak(self) -> float:
+        v = C.c_double()
+        self._call(_load().fse_cuda_fp64_peak, C.byref(v))
+        return v.value
 
     # -- Green's functions
     def precompute_mollified_green(self, kind, Ltilde, Mtilde, sf) -> MollifiedGreen:

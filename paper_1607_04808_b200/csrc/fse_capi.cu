@@ -102,7 +102,8 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
-constexpr int NEV = 12;
+constexpr int NEV = 16;
+constexpr int NKMS = 11;
 
 }  // namespace
 
@@ -115,6 +116,7 @@ struct fse_cuda_ctx {
     std::mutex mu;
     std::string err;
     uint64_t launches = 0;
+    double kms[NKMS] = {};  // per-kernel device ms of the last evaluation
     std::map<std::string, DevBuf> bufs;
     std::map<std::tuple<int, int, int>, cufftHandle> plans;
     DevBuf work;
@@ -335,7 +337,15 @@ Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, con
     return r;
 }
 
-// real-space pair sum on s1 into d_uR (caller order)
+enum {
+    EV_START, EV_PREP, EV_MEMSET, EV_SPREAD, EV_FFT1, EV_SCALE, EV_FFT2, EV_TPREP, EV_QUAD,
+    EV_R0, EV_RPAIR, EV_R1, EV_JOIN, EV_END, EV_COUNT
+};
+static_assert(EV_COUNT <= NEV, "event pool");
+
+// real-space pair sum on s1 into d_uR (caller order).  No host sync: the
+// pair kernel is launched over an upper bound of work items and reads the
+// true count from device memory.
 void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_str, int64_t n,
                double box_side, double xi, double rc, const double* d_tgt, int64_t nt, bool tas,
                double* d_uR) {
@@ -349,16 +359,14 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     int32_t* ioff = buf<int32_t>(c, "rs_ioff", cg.ncell + 1);
     launch_item_counts(L, tgt.start, cg.ncell, 128, icnt);
     exclusive_scan(c, c->s1, "s1", icnt, ioff, cg.ncell + 1);
-    int32_t nitems = 0;
-    FSE_CU(cudaMemcpyAsync(&c->h_flags[4], ioff + cg.ncell, sizeof(int32_t),
-                           cudaMemcpyDeviceToHost, c->s1));
-    FSE_CU(cudaStreamSynchronize(c->s1));
-    nitems = c->h_flags[4];
-    int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(nitems));
+    const int64_t max_items = std::min<int64_t>(cg.ncell, nt) + (nt + 127) / 128;
+    int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(max_items));
     launch_fill_items(L, tgt.start, ioff, cg.ncell, 128, items);
+    FSE_CU(cudaEventRecord(c->ev[EV_RPAIR], c->s1));
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
-                         tgt.pz, tgt.start, items, nitems, tgt.perm, xi, rc, d_uR);
+                         tgt.pz, tgt.start, items, max_items, ioff + cg.ncell, tgt.perm, xi, rc,
+                         d_uR);
     else if (nt > 0)
         FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
 }
@@ -369,7 +377,6 @@ double ev_sec(cudaEvent_t a, cudaEvent_t b) {
     return ms * 1e-3;
 }
 
-enum { EV_START, EV_SPREAD, EV_FFT1, EV_SCALE, EV_FFT2, EV_QUAD, EV_R0, EV_R1, EV_JOIN, EV_END };
 
 void raise_flags(fse_cuda_ctx* c) {
     FSE_CU(cudaMemcpyAsync(c->h_flags, c->d_flags, 3 * sizeof(int), cudaMemcpyDeviceToHost,
@@ -431,9 +438,11 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         double* qtab = buf<double>(c, "qtab", g.P);
         launch_quad_table(L, g, qtab);
         Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, tas ? 1 : 0, qtab);
+        FSE_CU(cudaEventRecord(c->ev[EV_PREP], c->s0));
         // spectrum buffer: a components of [D][D][D+2] doubles (= [D][D][Dh] complex)
         double* X = buf<double>(c, "X", static_cast<size_t>(a) * g.comp);
         FSE_CU(cudaMemsetAsync(X, 0, sizeof(double) * a * g.comp, c->s0));
+        FSE_CU(cudaEventRecord(c->ev[EV_MEMSET], c->s0));
         for (int c0 = 0; c0 < a; c0 += 3)
             launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
         FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
@@ -465,15 +474,14 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         int32_t* goff = buf<int32_t>(c, "goff", g.nkeys + 1);
         launch_group_counts(L, tg.tstart, g.nkeys, gcnt);
         exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
-        FSE_CU(cudaMemcpyAsync(&c->h_flags[5], goff + g.nkeys, sizeof(int32_t),
-                               cudaMemcpyDeviceToHost, c->s0));
-        FSE_CU(cudaStreamSynchronize(c->s0));
-        const int64_t ngroups = c->h_flags[5];
-        int32_t* gkey = buf<int32_t>(c, "gkey", ngroups);
+        // upper bound on groups: one partial group per non-empty key + nt/8
+        const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + 7) / 8;
+        int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
         launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
         uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
-        const double h3 = g.h * g.h * g.h;
-        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, ngroups, X, tg.perm, h3, uF);
+        const double h3 = g.h * g.h * g.h;  // prefac is folded into the x weights
+        FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
+        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, uF);
         FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
     }
 
@@ -488,6 +496,23 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
     }
     FSE_CU(cudaEventRecord(c->ev[EV_END], c->s0));
     raise_flags(c);
+    for (double& v : c->kms) v = 0;
+    auto ms = [&](int a0, int b0) { return 1e3 * ev_sec(c->ev[a0], c->ev[b0]); };
+    if (want_f) {
+        c->kms[0] = ms(EV_START, EV_PREP);
+        c->kms[1] = ms(EV_PREP, EV_MEMSET);
+        c->kms[2] = ms(EV_MEMSET, EV_SPREAD);
+        c->kms[3] = ms(EV_SPREAD, EV_FFT1);
+        c->kms[4] = ms(EV_FFT1, EV_SCALE);
+        c->kms[5] = ms(EV_SCALE, EV_FFT2);
+        c->kms[6] = ms(EV_FFT2, EV_TPREP);
+        c->kms[7] = ms(EV_TPREP, EV_QUAD);
+    }
+    if (want_r) {
+        c->kms[8] = ms(EV_R0, EV_RPAIR);
+        c->kms[9] = ms(EV_RPAIR, EV_R1);
+    }
+    c->kms[10] = ms(EV_START, EV_END);
     if (tm) {
         FSE_CU(cudaEventSynchronize(c->ev[EV_END]));
         if (want_f) {
@@ -714,6 +739,20 @@ fse_status fse_cuda_elapsed_ms(fse_cuda_ctx* c, double* ms) {
     });
 }
 uint64_t fse_cuda_launch_count(const fse_cuda_ctx* c) { return c ? c->launches : 0; }
+
+fse_status fse_cuda_fp64_peak(fse_cuda_ctx* c, double* tflops) {
+    return api(c, [&] {
+        if (!tflops) invalid("null pointer");
+        *tflops = measure_dfma_tflops(L0(c), buf<double>(c, "peak_scratch", 1));
+    });
+}
+
+fse_status fse_cuda_kernel_ms(fse_cuda_ctx* c, double* out, int n) {
+    return api(c, [&] {
+        if (!out) invalid("null pointer");
+        for (int k = 0; k < n && k < NKMS; ++k) out[k] = c->kms[k];
+    });
+}
 
 // ewald.cpp:103-134
 fse_status fse_make_config(double L, double xi, double rc, int M, int P, double sf,

@@ -124,7 +124,7 @@ void launch_scale_complex(const Launch& L, double2* data, int64_t n, double s);
 // groups of <= 8 targets per fine tile; group table built by caller
 void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                    const int32_t* tstart, const int32_t* gkey, const int32_t* goff,
-                   int64_t ngroups, const double* X, const uint32_t* perm, double scale,
+                   int64_t max_groups, const double* X, const uint32_t* perm, double scale,
                    double* u);
 void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount);
 void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* goff,
@@ -140,7 +140,8 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const double* spy, const double* spz, const double* sfs, int64_t ns,
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
-                      int64_t nitems, const uint32_t* tperm, double xi, double rc, double* uR);
+                      int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
+                      double xi, double rc, double* uR);
 void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
                         int32_t* cnt);
 void launch_fill_items(const Launch& L, const int32_t* start, const int32_t* off, int64_t ncell,
@@ -164,6 +165,7 @@ void launch_green_full_to_half(const Launch& L, int D, const double* full, doubl
 void launch_green_half_to_full(const Launch& L, int D, const double* half, double* full);
 
 // k_direct.cu ---------------------------------------------------------------
+double measure_dfma_tflops(const Launch& L, double* scratch);
 void launch_direct(const Launch& L, int kind, const double* pos, const double* str, int64_t n,
                    const double* tgt, int64_t nt, int exclude_self, double* u, int* flags);
 

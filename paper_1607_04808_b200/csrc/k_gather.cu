@@ -34,12 +34,13 @@ struct GatherWarp {
 __global__ void __launch_bounds__(WPB * 32) k_gather(
     GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ gkey,
-    const int32_t* __restrict__ goff, int64_t ngroups, const double* __restrict__ X,
+    const int32_t* __restrict__ goff, const int32_t* __restrict__ ngroups_dev,
+    const double* __restrict__ X,
     const uint32_t* __restrict__ perm, double scale, double* __restrict__ u) {
     __shared__ GatherWarp smw[WPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t grp = static_cast<int64_t>(blockIdx.x) * WPB + warp;
-    if (grp >= ngroups) return;
+    if (grp >= *ngroups_dev) return;  // grid is an upper bound (no host sync)
     GatherWarp& s = smw[warp];
     const int P = g.P;
     const int key = gkey[grp];
@@ -205,11 +206,11 @@ void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* g
 
 void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                    const int32_t* tstart, const int32_t* gkey, const int32_t* goff,
-                   int64_t ngroups, const double* X, const uint32_t* perm, double scale,
+                   int64_t max_groups, const double* X, const uint32_t* perm, double scale,
                    double* u) {
-    if (ngroups <= 0) return;
-    const unsigned blocks = static_cast<unsigned>((ngroups + WPB - 1) / WPB);
-    k_gather<<<blocks, WPB * 32, 0, L.s>>>(g, i0s, w, tstart, gkey, goff, ngroups, X, perm,
+    if (max_groups <= 0) return;
+    const unsigned blocks = static_cast<unsigned>((max_groups + WPB - 1) / WPB);
+    k_gather<<<blocks, WPB * 32, 0, L.s>>>(g, i0s, w, tstart, gkey, goff, goff + g.nkeys, X, perm,
                                            scale, u);
     FSE_LAUNCH_CHECK();
     ++*L.launches;

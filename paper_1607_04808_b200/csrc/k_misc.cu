@@ -1,6 +1,8 @@
 // k_misc.cu -- epilogue of total_sum (ewald.cpp:403-410), the O(N NT)
 // direct sum (kernels.cpp:27-82), and the GPU precompute of the mollified
 // Green's function (greens.cpp:22-113).
+#include <algorithm>
+
 #include "fse_internal.cuh"
 
 namespace fsecu {
@@ -226,6 +228,23 @@ __global__ void k_half_to_full(int D, const double* __restrict__ half, double* _
     }
 }
 
+// DFMA throughput probe (roofline denominator for the FP64-bound stages):
+// 8 independent FMA chains per thread, no memory traffic.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double seed) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.999999999, c = 1e-12;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 unsigned grid_stride_blocks(int64_t n) {
     int64_t b = (n + TPB - 1) / TPB;
     const int64_t cap = 148 * 32;
@@ -233,6 +252,33 @@ unsigned grid_stride_blocks(int64_t n) {
 }
 
 }  // namespace
+
+double measure_dfma_tflops(const Launch& L, double* scratch) {
+    int sms = 148;
+    int dev = 0;
+    FSE_CU(cudaGetDevice(&dev));
+    FSE_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned blocks = static_cast<unsigned>(sms) * 8;
+    const int iters = 1 << 14;
+    cudaEvent_t a, b;
+    FSE_CU(cudaEventCreate(&a));
+    FSE_CU(cudaEventCreate(&b));
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+        FSE_CU(cudaEventRecord(a, L.s));
+        k_dfma_peak<<<blocks, 256, 0, L.s>>>(scratch, iters, 1.0 + rep);
+        FSE_CU(cudaEventRecord(b, L.s));
+        FSE_CU(cudaEventSynchronize(b));
+        float ms = 0;
+        FSE_CU(cudaEventElapsedTime(&ms, a, b));
+        const double flops = 2.0 * 8.0 * iters * 256.0 * blocks;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *L.launches += 4;
+    return best;
+}
 
 void launch_epilogue(const Launch& L, int64_t nt, const double* uF, const double* uR,
                      const double* str_self, double self_coef, double* u) {

@@ -74,12 +74,14 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
     const double* __restrict__ tpy, const double* __restrict__ tpz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
-    const uint32_t* __restrict__ tperm, double xi, double rc2, double* __restrict__ u) {
+    const uint32_t* __restrict__ tperm, const int32_t* __restrict__ nitems_dev, double xi,
+    double rc2, double* __restrict__ u) {
     constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
     __shared__ double sx[CH], sy[CH], sz[CH];
     __shared__ double sf[CH][A];
     __shared__ int nb_start[27], nb_pref[28];
 
+    if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // grid is an upper bound
     const int cell = items[2 * blockIdx.x];
     const int sub = items[2 * blockIdx.x + 1];
     const int tid = threadIdx.x;
@@ -202,23 +204,24 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const double* spy, const double* spz, const double* sfs, int64_t ns,
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
-                      int64_t nitems, const uint32_t* tperm, double xi, double rc,
-                      double* uR) {
+                      int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
+                      double xi, double rc, double* uR) {
     (void)ns;
+    const int64_t nitems = max_items;
     if (nitems <= 0) return;
     const double rc2 = rc * rc;
     const unsigned b = static_cast<unsigned>(nitems);
     if (kind == FSE_STOKESLET)
         k_realspace<FSE_STOKESLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx,
-                                                       tpy, tpz, tcell_start, items, tperm, xi,
-                                                       rc2, uR);
+                                                       tpy, tpz, tcell_start, items, tperm, nitems_dev,
+                                                       xi, rc2, uR);
     else if (kind == FSE_STRESSLET)
         k_realspace<FSE_STRESSLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx,
-                                                       tpy, tpz, tcell_start, items, tperm, xi,
-                                                       rc2, uR);
+                                                       tpy, tpz, tcell_start, items, tperm, nitems_dev,
+                                                       xi, rc2, uR);
     else
         k_realspace<FSE_ROTLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy,
-                                                    tpz, tcell_start, items, tperm, xi, rc2, uR);
+                                                    tpz, tcell_start, items, tperm, nitems_dev, xi, rc2, uR);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
