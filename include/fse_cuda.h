@@ -168,6 +168,9 @@ fse_status fse_cuda_direct_sum(fse_cuda_ctx* ctx, int kind, const double* pos,
 /* the FFT seam (fft.hpp:11,14): in-place 3D C2C on interleaved complex host data;
  * inverse scales by 1/(n0 n1 n2) */
 fse_status fse_cuda_fft3d(fse_cuda_ctx* ctx, double* data, int n0, int n1, int n2, int inverse);
+/* diagnostics: the hand-written fp64 FFT engine of the hot path on `ncols` contiguous
+ * interleaved-complex columns of length D, in place, unnormalised (sign -1 / +1) */
+fse_status fse_cuda_fft_columns(fse_cuda_ctx* ctx, int D, int ncols, double* data, int inverse);
 
 #ifdef __cplusplus
 }

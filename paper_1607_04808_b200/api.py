@@ -203,6 +203,7 @@ def _load():
                                                C.POINTER(C.c_int32)]
         lib.fse_cuda_direct_sum.argtypes = [vp, C.c_int, _dp, _dp, i64, _dp, i64, C.c_int, _dp]
         lib.fse_cuda_fft3d.argtypes = [vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int]
+        lib.fse_cuda_fft_columns.argtypes = [vp, C.c_int, C.c_int, _dp, C.c_int]
         lib.fse_cuda_host_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
         lib.fse_cuda_host_free.argtypes = [vp]
         lib.fse_cuda_dev_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
@@ -450,6 +451,14 @@ class Context:
                    _p(system.strengths), system.size(), _p(t), t.shape[0], int(exclude_self),
                    _p(u))
         return u
+
+    def fft_columns(self, cols, inverse=False):
+        """The hot path's hand-written FFT engine on rows of `cols` (ncols, D)."""
+        d = np.ascontiguousarray(cols, dtype=np.complex128).copy()
+        nc, D = d.shape
+        self._call(_load().fse_cuda_fft_columns, int(D), int(nc), d.ctypes.data_as(_dp),
+                   int(inverse))
+        return d
 
     def fft3d(self, data, inverse=False):
         d = np.ascontiguousarray(data, dtype=np.complex128).copy()

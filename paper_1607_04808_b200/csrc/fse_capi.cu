@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -35,6 +36,7 @@
 #include <vector>
 
 #include "fse_internal.cuh"
+#include "k_fft.cuh"
 
 namespace fsecu {
 
@@ -58,8 +60,9 @@ GridParams make_grid_params(const fse_config& c) {
     g.Mt = c.Mtilde;
     g.D = 2 * c.Mtilde;
     g.Dh = g.D / 2 + 1;
-    g.plane = static_cast<int64_t>(g.D) * (g.D + 2);
-    g.comp = static_cast<int64_t>(g.D) * g.plane;
+    g.rowp = g.Mt;
+    g.plane = static_cast<int64_t>(g.Mt) * g.Mt;
+    g.comp = static_cast<int64_t>(g.Mt) * g.plane;
     g.h = c.h;
     g.origin = -c.deltaL / 2;                                     // ewald.cpp:147
     g.alpha = 2.0 * c.xi * c.xi / c.eta;                          // ewald.cpp:152
@@ -107,8 +110,14 @@ constexpr int NKMS = 11;
 
 }  // namespace
 
+struct FftPlanDev {
+    HostFftPlan host;
+    double2* tw = nullptr;
+};
+
 struct fse_cuda_ctx {
     int device = 0;
+    std::map<int, FftPlanDev> fft_plans;
     cudaStream_t s0 = nullptr, s1 = nullptr;
     cudaEvent_t ev[NEV] = {};
     cudaEvent_t mark[2] = {};
@@ -174,6 +183,21 @@ T* buf(fse_cuda_ctx* c, const std::string& name, size_t count) {
 void release_plans(fse_cuda_ctx* c) {
     for (auto& kv : c->plans) cufftDestroy(kv.second);
     c->plans.clear();
+    for (auto& kv : c->fft_plans)
+        if (kv.second.tw) cudaFree(kv.second.tw);
+    c->fft_plans.clear();
+}
+
+// hand-written FFT plan (radices + long-double twiddle tables), cached per D
+const FftPlanDev& fft_plan(fse_cuda_ctx* c, int D) {
+    auto it = c->fft_plans.find(D);
+    if (it != c->fft_plans.end()) return it->second;
+    FftPlanDev p;
+    p.host = make_fft_plan(D);
+    FSE_CU(cudaMalloc(&p.tw, sizeof(double2) * p.host.tw.size()));
+    FSE_CU(cudaMemcpy(p.tw, p.host.tw.data(), sizeof(double2) * p.host.tw.size(),
+                      cudaMemcpyHostToDevice));
+    return c->fft_plans.emplace(D, std::move(p)).first->second;
 }
 
 Launch L0(fse_cuda_ctx* c) { return Launch{c->s0, &c->launches}; }
@@ -439,34 +463,22 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         launch_quad_table(L, g, qtab);
         Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, tas ? 1 : 0, qtab);
         FSE_CU(cudaEventRecord(c->ev[EV_PREP], c->s0));
-        // spectrum buffer: a components of [D][D][D+2] doubles (= [D][D][Dh] complex)
-        double* X = buf<double>(c, "X", static_cast<size_t>(a) * g.comp);
-        FSE_CU(cudaMemsetAsync(X, 0, sizeof(double) * a * g.comp, c->s0));
+        // R: a compact Mt^3 real grids (every node is written by exactly one
+        // spread tile, so no memset); B, C: pruned spectra (k_fft.cu)
+        const int64_t Dh = g.Dh;
+        double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
+        double2* Bs = buf<double2>(c, "B", static_cast<size_t>(a) * g.Mt * g.Mt * Dh);
+        double2* Cs = buf<double2>(c, "C", static_cast<size_t>(a) * g.Mt * g.D * Dh);
+        const FftPlanDev& fp = fft_plan(c, g.D);
         FSE_CU(cudaEventRecord(c->ev[EV_MEMSET], c->s0));
         for (int c0 = 0; c0 < a; c0 += 3)
             launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
         FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
-
-        const cufftHandle p2r = plan(c, 0, g.D, g.Mt);
-        const cufftHandle px = plan(c, 2, g.D, g.Mt);
-        const cufftHandle p2c = plan(c, 1, g.D, g.Mt);
-        auto comp_ptr = [&](int cc) { return X + cc * g.comp; };
-        for (int cc = 0; cc < a; ++cc) {
-            double* xr = comp_ptr(cc);
-            auto* xc = reinterpret_cast<cufftDoubleComplex*>(xr);
-            FSE_CUFFT(cufftExecD2Z(p2r, xr, xc));
-            FSE_CUFFT(cufftExecZ2Z(px, xc, xc, CUFFT_FORWARD));
-        }
+        launch_fft_forward_zy(L, fp.host, fp.tw, g.Mt, a, X, Bs, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT1], c->s0));
-        launch_kscale_half(L, g, kind, green->d_half, reinterpret_cast<double2*>(X),
-                           g.comp / 2);
+        launch_fft_xscale(L, fp.host, fp.tw, g, kind, green->d_half, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_SCALE], c->s0));
-        for (int cc = 0; cc < 3; ++cc) {
-            double* xr = comp_ptr(cc);
-            auto* xc = reinterpret_cast<cufftDoubleComplex*>(xr);
-            FSE_CUFFT(cufftExecZ2Z(px, xc, xc, CUFFT_INVERSE));
-            FSE_CUFFT(cufftExecZ2D(p2c, xc, xr));
-        }
+        launch_fft_inverse_yz(L, fp.host, fp.tw, g.Mt, 3, Cs, Bs, X);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT2], c->s0));
 
         Sorted tg = tas ? src : prep_points(c, g, "ft_", d_tgt, nullptr, 0, nt, 1, qtab);
@@ -476,12 +488,22 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
         // upper bound on groups: one partial group per non-empty key + nt/8
         const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + 7) / 8;
-        int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
-        launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
         uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
         const double h3 = g.h * g.h * g.h;  // prefac is folded into the x weights
+        // the plane-streamed gather trades L2 traffic for barriers; at uniform
+        // cfg2 density (~21 targets per 8^3 region) the warp-group kernel wins
+        const bool planes = gather_planes_ok(g) && std::getenv("FSE_GATHER_PLANES");
+        int32_t* gkey = nullptr;
+        if (!planes) {
+            gkey = buf<int32_t>(c, "gkey", max_groups);
+            launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
+        }
         FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
-        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, uF);
+        if (planes)
+            launch_gather_planes(L, g, tg.i0s, tg.w, tg.tstart, goff, X, tg.perm, h3, uF);
+        else
+            launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3,
+                          uF);
         FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
     }
 
@@ -980,8 +1002,7 @@ fse_status fse_cuda_spread(fse_cuda_ctx* c, const fse_config* cfg, int kind, con
         double* qtab = buf<double>(c, "qtab", g.P);
         launch_quad_table(L0(c), g, qtab);
         Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
-        double* X = buf<double>(c, "X", static_cast<size_t>(a) * g.comp);
-        FSE_CU(cudaMemsetAsync(X, 0, sizeof(double) * a * g.comp, c->s0));
+        double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
         for (int c0 = 0; c0 < a; c0 += 3)
             launch_spread(L0(c), g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
         const size_t vol = static_cast<size_t>(g.Mt) * g.Mt * g.Mt;
@@ -1077,6 +1098,19 @@ fse_status fse_cuda_direct_sum(fse_cuda_ctx* c, int kind, const double* pos, con
 }
 
 // fft.cpp:13-37 over cuFFT Z2Z (in place, inverse scaled by 1/(n0 n1 n2))
+// diagnostics for the hand-written FFT engine: ncols contiguous length-D columns
+fse_status fse_cuda_fft_columns(fse_cuda_ctx* c, int D, int ncols, double* data, int inverse) {
+    return api(c, [&] {
+        if (!data || D < 1 || ncols < 1) invalid("fft_columns: bad arguments");
+        const FftPlanDev& fp = fft_plan(c, D);
+        const size_t n = static_cast<size_t>(D) * ncols;
+        double2* d = buf<double2>(c, "fftcol", n);
+        h2d(c, d, data, n * sizeof(double2));
+        fft_test_columns(L0(c), fp.host, fp.tw, d, ncols, inverse);
+        d2h(c, data, d, n * sizeof(double2));
+    });
+}
+
 fse_status fse_cuda_fft3d(fse_cuda_ctx* c, double* data, int n0, int n1, int n2, int inverse) {
     return api(c, [&] {
         if (!data || n0 < 1 || n1 < 1 || n2 < 1) invalid("fft3d: bad arguments");

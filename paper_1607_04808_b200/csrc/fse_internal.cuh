@@ -54,8 +54,10 @@ struct GridParams {
     int Mt;         // Mtilde
     int D;          // 2 Mtilde (FFT size, exact: SURVEY 8a A6)
     int Dh;         // D/2 + 1 (half spectrum)
-    int64_t plane;  // doubles per x-plane of the real view: D * (D + 2)
-    int64_t comp;   // doubles per component buffer: D * D * (D + 2)
+    // real grids (spread output R, quadrature input W) are compact Mt^3 per component
+    int64_t rowp;   // doubles per row: Mt
+    int64_t plane;  // doubles per x-plane: Mt * Mt
+    int64_t comp;   // doubles per component: Mt^3
     double h, origin, alpha, prefac, L;
     double dk, inv4xi2, eta, invD3;
     // spread/gather tiling of the support-start space (i0x, i0y, i0z)
@@ -126,6 +128,11 @@ void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    const int32_t* tstart, const int32_t* gkey, const int32_t* goff,
                    int64_t max_groups, const double* X, const uint32_t* perm, double scale,
                    double* u);
+// plane-streamed gather (P + 7 <= 32): no group table needed beyond goff
+bool gather_planes_ok(const GridParams& g);
+void launch_gather_planes(const Launch& L, const GridParams& g, const int32_t* i0s,
+                          const double* w, const int32_t* tstart, const int32_t* goff,
+                          const double* X, const uint32_t* perm, double scale, double* u);
 void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount);
 void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* goff,
                         int64_t nkeys, int32_t* gkey);

@@ -1,0 +1,804 @@
+// k_fft.cu -- hand-written fp64 FFTs for the zero-padded D = 2 Mtilde grid,
+// with the k-space scaling fused into the x-pass.
+//
+// Why not cuFFT: measured on B200 at D = 624 (tools/fft_probe.cu), a 3D
+// D2Z runs at ~0.5 TB/s effective and the strided 1D x-pass the pruned
+// transform needs takes 7.2 ms per component (it transposes through a
+// full-size workspace), while a contiguous batched pass streams at ~6.4 TB/s.
+// Writing the passes ourselves lets every pass touch HBM once and skip the
+// known zeros:
+//
+//   R  [i][j][n]   Mt^3 real   (spread output, compact)
+//   zfwd: rows (i,j), two real rows per complex FFT, Mt inputs    -> B [i][j][kz]  Mt x Mt x Dh
+//   yfwd: columns (i,kz), Mt inputs                               -> C [i][ky][kz] Mt x D  x Dh
+//   xk  : columns (ky,kz): Mt inputs, FFT_x, multiply by A_eff(k) G(k) / D^3 (all a
+//         components at once), inverse FFT_x, keep the Mt outputs -> C (in place, 3 comps)
+//   yinv: columns (i,kz), keep j < Mt                             -> B
+//   zinv: Hermitian rows, two real rows per complex FFT, keep n < Mt -> W [i][j][n] Mt^3 real
+//
+// The planes i >= Mt of the x-pass input and j >= Mt of the y-pass input are
+// zeros that are never stored; outputs outside the window are never written.
+//
+// Engine: a CTA holds NCOL columns of length D in shared memory (column-major,
+// one 16-byte pad every 8 elements against bank conflicts) and runs a Stockham
+// autosort FFT, one __syncthreads-separated stage per radix.  Radices 2/3/4/5/
+// 7/8/11/13 are register butterflies (a thread loads all its butterflies'
+// inputs before the barrier and stores after, so a stage runs in place);
+// any other factor runs as one generic DFT stage through a second buffer.
+// Twiddles W_{Ns p}^{r k} come from host-computed tables (long double).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "fse_internal.cuh"
+#include "k_fft.cuh"
+
+namespace fsecu {
+
+namespace {
+
+__constant__ double c_cos[4][14];  // cos(2 pi t / p) for p = 5, 7, 11, 13
+__constant__ double c_sin[4][14];
+
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// i * s * a  (s = +-1)
+__device__ __forceinline__ double2 cis(double2 a, int s) {
+    return s > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <int P>
+struct Dft;
+
+template <>
+struct Dft<2> {
+    __device__ __forceinline__ static void run(double2* v, int) {
+        const double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    }
+};
+
+template <>
+struct Dft<3> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        const double h = 0.86602540378443864676372317075293618;
+        const double2 t1 = cadd(v[1], v[2]);
+        const double2 t2 = make_double2(v[0].x - 0.5 * t1.x, v[0].y - 0.5 * t1.y);
+        const double2 d = csub(v[1], v[2]);
+        const double2 t3 = cis(make_double2(h * d.x, h * d.y), s);  // i s (sqrt3/2) (v1 - v2)
+        v[0] = cadd(v[0], t1);
+        v[1] = cadd(t2, t3);
+        v[2] = csub(t2, t3);
+    }
+};
+
+template <>
+struct Dft<4> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        const double2 s0 = cadd(v[0], v[2]), d0 = csub(v[0], v[2]);
+        const double2 s1 = cadd(v[1], v[3]), d1 = cis(csub(v[1], v[3]), s);
+        v[0] = cadd(s0, s1);
+        v[2] = csub(s0, s1);
+        v[1] = cadd(d0, d1);
+        v[3] = csub(d0, d1);
+    }
+};
+
+template <>
+struct Dft<8> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        Dft<4>::run(e, s);
+        Dft<4>::run(o, s);
+        const double r = 0.70710678118654752440084436210484904;
+        // o[q] *= w^q, w = exp(s 2 pi i / 8) = r (1 + s i)
+        const double2 o1 = o[1], o3 = o[3];
+        o[1] = make_double2(r * (o1.x - s * o1.y), r * (o1.y + s * o1.x));
+        o[2] = cis(o[2], s);
+        o[3] = make_double2(r * (-o3.x - s * o3.y), r * (-o3.y + s * o3.x));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = cadd(e[q], o[q]);
+            v[q + 4] = csub(e[q], o[q]);
+        }
+    }
+};
+
+// odd prime p via conjugate pairs: y_q = v0 + sum_r s_r cos + i s sum_r d_r sin
+template <int P, int T>
+struct DftOdd {
+    __device__ __forceinline__ static void run(double2* v, int sgn) {
+        constexpr int H = (P - 1) / 2;
+        double2 sr[H], dr[H];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+            sr[r - 1] = cadd(v[r], v[P - r]);
+            dr[r - 1] = csub(v[r], v[P - r]);
+        }
+        const double2 v0 = v[0];
+        double2 y0 = v0;
+#pragma unroll
+        for (int r = 0; r < H; ++r) y0 = cadd(y0, sr[r]);
+#pragma unroll
+        for (int q = 1; q <= H; ++q) {
+            double2 A = v0, B = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 1; r <= H; ++r) {
+                const int t = (r * q) % P;
+                const double c = c_cos[T][t], sn = c_sin[T][t];
+                A.x = fma(sr[r - 1].x, c, A.x);
+                A.y = fma(sr[r - 1].y, c, A.y);
+                B.x = fma(dr[r - 1].x, sn, B.x);
+                B.y = fma(dr[r - 1].y, sn, B.y);
+            }
+            const double2 iB = cis(B, sgn);
+            v[q] = cadd(A, iB);
+            v[P - q] = csub(A, iB);
+        }
+        v[0] = y0;
+    }
+};
+template <>
+struct Dft<5> : DftOdd<5, 0> {};
+template <>
+struct Dft<7> : DftOdd<7, 1> {};
+template <>
+struct Dft<11> : DftOdd<11, 2> {};
+template <>
+struct Dft<13> : DftOdd<13, 3> {};
+
+// register staging per thread: at most ~16 complex values per stage
+template <int P>
+constexpr int maxit() {
+    return (16 + P - 1) / P;
+}
+
+// one in-place Stockham stage over NCOL columns of length D
+template <int P>
+__device__ __forceinline__ void stage_reg(double2* buf, int D, int ncol, int Ns, const FDiv& fnb,
+                                          const FDiv& fNs, const double2* __restrict__ tw, int sgn) {
+    constexpr int MI = maxit<P>();
+    const int nb = static_cast<int>(fnb.d);
+    const int items = nb * ncol;
+    double2 v[MI][P];
+#pragma unroll
+    for (int m = 0; m < MI; ++m) {
+        const int it = threadIdx.x + m * blockDim.x;
+        if (it < items) {
+            const int c = static_cast<int>(fdiv(it, fnb)), b = it - c * nb;
+            const int base = c * D + b;
+#pragma unroll
+            for (int r = 0; r < P; ++r) v[m][r] = buf[pad(base + r * nb)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MI; ++m) {
+        const int it = threadIdx.x + m * blockDim.x;
+        if (it < items) {
+            const int c = static_cast<int>(fdiv(it, fnb)), b = it - c * nb;
+            const int bq = static_cast<int>(fdiv(b, fNs));
+            const int k = b - bq * Ns;
+            if (k != 0) {
+                const double2* t = tw + k * (P - 1);
+#pragma unroll
+                for (int r = 1; r < P; ++r) {
+                    double2 w = t[r - 1];
+                    if (sgn > 0) w.y = -w.y;
+                    v[m][r] = cmul(v[m][r], w);
+                }
+            }
+            Dft<P>::run(v[m], sgn);
+            const int o = c * D + bq * Ns * P + k;
+#pragma unroll
+            for (int r = 0; r < P; ++r) buf[pad(o + r * Ns)] = v[m][r];
+        }
+    }
+    __syncthreads();
+}
+
+// generic radix (any P): out-of-place, each thread computes outputs directly
+__device__ __forceinline__ void stage_gen(const double2* in, double2* out, int D, int ncol, int P,
+                                          int Ns, const FftPlan& pl, int s,
+                                          const double2* __restrict__ W, int sgn) {
+    const int tot = D * ncol, NsP = Ns * P, nb = static_cast<int>(pl.dnb[s].d);
+    for (int o = threadIdx.x; o < tot; o += blockDim.x) {
+        const int c = static_cast<int>(fdiv(o, pl.dD)), e = o - c * D;
+        const int eN = static_cast<int>(fdiv(e, pl.dNs[s]));
+        const int k = e - eN * Ns;
+        const int blk = static_cast<int>(fdiv(e, pl.dNsP[s]));
+        const int q = eN - blk * P;
+        const int b = blk * Ns + k, m = k + q * Ns;
+        double2 acc = make_double2(0.0, 0.0);
+        int t = 0;
+        for (int r = 0; r < P; ++r) {
+            double2 w = W[t];
+            if (sgn > 0) w.y = -w.y;
+            const double2 x = in[pad(c * D + b + r * nb)];
+            acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
+            acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
+            t += m;
+            if (t >= NsP) t -= NsP;
+        }
+        out[pad(o)] = acc;
+    }
+    __syncthreads();
+}
+
+// runs the plan on `ncol` columns in a (scratch b for generic stages);
+// returns the buffer holding the result.  The stage order is fixed by the
+// planner (generic, 8s, 4, 2, 3s, 5s, 7s, 11s, 13s), so every radix has its
+// own straight-line code region and its staging array stays in registers.
+template <int P>
+__device__ __forceinline__ void run_radix(double2* cur, int& s, const FftPlan& pl, int ncol,
+                                          const double2* __restrict__ tw, int sgn) {
+    while (s < pl.nst && pl.p[s] == P) {
+        stage_reg<P>(cur, pl.D, ncol, pl.Ns[s], pl.dnb[s], pl.dNs[s], tw + pl.tw[s], sgn);
+        ++s;
+    }
+}
+
+__device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, const FftPlan& pl,
+                                             const double2* __restrict__ tw, int sgn) {
+    double2* cur = a;
+    int s = 0;
+    if (pl.nst > 0 && pl.p[0] > 13) {  // generic stage (planner puts it first)
+        stage_gen(cur, b, pl.D, ncol, pl.p[0], pl.Ns[0], pl, 0, tw + pl.tw[0], sgn);
+        cur = b;
+        s = 1;
+    }
+    run_radix<8>(cur, s, pl, ncol, tw, sgn);
+    run_radix<4>(cur, s, pl, ncol, tw, sgn);
+    run_radix<2>(cur, s, pl, ncol, tw, sgn);
+    run_radix<3>(cur, s, pl, ncol, tw, sgn);
+    run_radix<5>(cur, s, pl, ncol, tw, sgn);
+    run_radix<7>(cur, s, pl, ncol, tw, sgn);
+    run_radix<11>(cur, s, pl, ncol, tw, sgn);
+    run_radix<13>(cur, s, pl, ncol, tw, sgn);
+    return cur;
+}
+
+extern __shared__ __align__(16) unsigned char fse_smem[];
+
+// the plan's twiddle table lives after the column buffer(s) in shared memory
+__device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPlan& pl,
+                                                         const double2* __restrict__ tw_g) {
+    double2* t = a + pl.buf_elems * (pl.two_bufs ? 2 : 1);
+    for (int e = threadIdx.x; e < pl.tw_elems; e += blockDim.x) t[e] = __ldg(tw_g + e);
+    __syncthreads();
+    return t;
+}
+
+// ------------------------------------------------------------------ test kernel
+__global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
+                                                  double2* data, int ncol_total, int ncol,
+                                                  int sgn) {
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    double2* b = a + pl.buf_elems;
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const int c0 = blockIdx.x * ncol;
+    const int nc = min(ncol, ncol_total - c0);
+    for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
+        a[pad(e)] = data[static_cast<int64_t>(c0) * pl.D + e];  // contiguous columns
+    __syncthreads();
+    double2* r = fft_cols(a, b, nc, pl, tw, sgn);
+    for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
+        data[static_cast<int64_t>(c0) * pl.D + e] = r[pad(e)];
+}
+
+// ------------------------------------------------------------------ z forward
+// column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
+__global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
+                                                 int ncomp, int ncol, const double* __restrict__ R,
+                                                 double2* __restrict__ B) {
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    double2* sb = a + pl.buf_elems;
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
+    const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
+    const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
+    const FDiv fMt = make_fdiv(Mt), fJp = make_fdiv(Jp), fDh = make_fdiv(Dh);
+    // per-column row pointers (<= 64 columns per CTA)
+    __shared__ int64_t row0[64];  // first R/W row of the pair, in doubles
+    __shared__ int64_t brow[64];  // first B row of the pair, in rows of Dh
+    __shared__ int has1[64];
+    if (threadIdx.x < nc) {
+        const int64_t q = q0 + threadIdx.x;
+        const int64_t ci = q / Jp;  // comp * Mt + i
+        const int jp = static_cast<int>(q - ci * Jp);
+        const int64_t comp = ci / Mt, i = ci - comp * Mt;
+        row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
+        brow[threadIdx.x] = ci * Mt + 2 * jp;
+        has1[threadIdx.x] = (2 * jp + 1 < Mt);
+    }
+    __syncthreads();
+    // load: lanes walk n (contiguous in R); zero padding n >= Mt
+    for (int c = 0; c < nc; ++c) {
+        const double* row = R + row0[c];
+        const bool h1 = has1[c];
+        for (int n = threadIdx.x; n < D; n += blockDim.x) {
+            double2 z = make_double2(0.0, 0.0);
+            if (n < Mt) {
+                z.x = row[n];
+                if (h1) z.y = row[Mt + n];
+            }
+            a[pad(c * D + n)] = z;
+        }
+    }
+    __syncthreads();
+    double2* r = fft_cols(a, sb, nc, pl, tw, -1);
+    // split: X0[k] = (Z[k] + conj Z[-k]) / 2, X1[k] = (Z[k] - conj Z[-k]) / (2i)
+    for (int e = threadIdx.x; e < nc * Dh; e += blockDim.x) {
+        const int c = static_cast<int>(fdiv(e, fDh)), k = e - c * Dh;
+        const double2 zk = r[pad(c * D + k)];
+        const double2 zm = r[pad(c * D + (k == 0 ? 0 : D - k))];
+        const double2 x0 = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        const double2 x1 = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+        double2* dst = B + brow[c] * Dh + k;
+        dst[0] = x0;
+        if (has1[c]) dst[Dh] = x1;
+    }
+    (void)fMt;
+    (void)fJp;
+}
+
+// ------------------------------------------------------------------ y passes
+// forward: columns (comp, i, kz-tile of ncol); input B[comp][i][j][kz], j < Mt
+// inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
+template <bool INV>
+__global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
+                                                  int ncomp, int ncol, double2* __restrict__ B,
+                                                  double2* __restrict__ Cb) {
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    double2* sb = a + pl.buf_elems;
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const int D = pl.D, Dh = D / 2 + 1;
+    const int ntz = (Dh + ncol - 1) / ncol;
+    const int ci = blockIdx.x / ntz;  // comp * Mt + i
+    const int tz = blockIdx.x - ci * ntz;
+    const int kz0 = tz * ncol;
+    const int nc = min(ncol, Dh - kz0);
+    const FDiv fnc = make_fdiv(nc);
+    double2* Bp = B + static_cast<int64_t>(ci) * Mt * Dh + kz0;   // [j][kz]
+    double2* Cp = Cb + static_cast<int64_t>(ci) * D * Dh + kz0;   // [ky][kz]
+    const int nin = INV ? D : Mt;
+    const double2* src = INV ? Cp : Bp;
+    for (int e = threadIdx.x; e < nc * nin; e += blockDim.x) {
+        const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;  // lanes walk kz
+        a[pad(c * D + j)] = src[static_cast<int64_t>(j) * Dh + c];
+    }
+    if (!INV)
+        for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
+            const int jj = static_cast<int>(fdiv(e, fnc)), c = e - jj * nc;
+            a[pad(c * D + Mt + jj)] = make_double2(0.0, 0.0);
+        }
+    __syncthreads();
+    double2* r = fft_cols(a, sb, nc, pl, tw, INV ? +1 : -1);
+    const int nout = INV ? Mt : D;
+    double2* dst = INV ? Bp : Cp;
+    for (int e = threadIdx.x; e < nc * nout; e += blockDim.x) {
+        const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;
+        dst[static_cast<int64_t>(j) * Dh + c] = r[pad(c * D + j)];
+    }
+}
+
+// ------------------------------------------------------------------ x pass + scale
+struct C2 {
+    double re, im;
+};
+
+template <int KIND>
+__device__ __forceinline__ void apply(const double k[3], double k2, double gval, double rem,
+                                      double inv4xi2, const double2* g, double2* out) {
+    if (KIND == FSE_STOKESLET) {
+        const double b = -gval * (1.0 + k2 * inv4xi2) * rem;
+        const double kgr = k[0] * g[0].x + k[1] * g[1].x + k[2] * g[2].x;
+        const double kgi = k[0] * g[0].y + k[1] * g[1].y + k[2] * g[2].y;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+            out[p] = make_double2(b * (k2 * g[p].x - k[p] * kgr), b * (k2 * g[p].y - k[p] * kgi));
+    } else if (KIND == FSE_STRESSLET) {
+        const double b = gval * (1.0 + k2 * inv4xi2) * rem;
+        double ar[3] = {0, 0, 0}, ai[3] = {0, 0, 0}, br[3] = {0, 0, 0}, bi[3] = {0, 0, 0};
+        double trr = 0, tri = 0, kgkr = 0, kgki = 0;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            trr += g[3 * p + p].x;
+            tri += g[3 * p + p].y;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                ar[p] += g[3 * p + q].x * k[q];
+                ai[p] += g[3 * p + q].y * k[q];
+                br[q] += k[p] * g[3 * p + q].x;
+                bi[q] += k[p] * g[3 * p + q].y;
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            kgkr += k[p] * ar[p];
+            kgki += k[p] * ai[p];
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const double vr = k2 * (ar[p] + br[p] + k[p] * trr) - 2.0 * k[p] * kgkr;
+            const double vi = k2 * (ai[p] + bi[p] + k[p] * tri) - 2.0 * k[p] * kgki;
+            out[p] = make_double2(b * vi, -b * vr);
+        }
+    } else {
+        const double cm = -gval * rem;
+        const double vr[3] = {g[1].x * k[2] - g[2].x * k[1], g[2].x * k[0] - g[0].x * k[2],
+                              g[0].x * k[1] - g[1].x * k[0]};
+        const double vi[3] = {g[1].y * k[2] - g[2].y * k[1], g[2].y * k[0] - g[0].y * k[2],
+                              g[0].y * k[1] - g[1].y * k[0]};
+#pragma unroll
+        for (int p = 0; p < 3; ++p) out[p] = make_double2(-cm * vi[p], cm * vr[p]);
+    }
+}
+
+__device__ __forceinline__ double kax(int q, int D, double dk) {
+    return dk * (q < D / 2 ? q : q - D);
+}
+
+// columns (ky, kz-tile); smem holds a*nc columns: column (comp*nc + c)
+template <int KIND>
+__global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
+                                                GridParams g, int ncol,
+                                                const double* __restrict__ G,
+                                                double2* __restrict__ Cb) {
+    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    double2* sb = a + pl.buf_elems;
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const int D = pl.D, Dh = D / 2 + 1, Mt = g.Mt;
+    const int ntz = (Dh + ncol - 1) / ncol;
+    const int ky = blockIdx.x / ntz;
+    const int tz = blockIdx.x - ky * ntz;
+    const int kz0 = tz * ncol;
+    const int nc = min(ncol, Dh - kz0);
+    const FDiv fnc = make_fdiv(nc);
+    const int64_t compC = static_cast<int64_t>(Mt) * D * Dh;
+    const int64_t rowoff = static_cast<int64_t>(ky) * Dh + kz0;  // within an i-slab
+    const int64_t slab = static_cast<int64_t>(D) * Dh;
+    // Green's column slice G[kx][ky][kz0 + c] staged with the data
+    double* Gs = reinterpret_cast<double*>(const_cast<double2*>(tw) + pl.tw_elems);
+    for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
+        const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
+        Gs[e] = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0 + c);
+    }
+    for (int comp = 0; comp < A; ++comp) {
+        const double2* src = Cb + comp * compC + rowoff;
+        double2* dst = a + 0;
+        for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
+            const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;  // lanes walk kz
+            dst[pad((comp * nc + c) * D + i)] = src[static_cast<int64_t>(i) * slab + c];
+        }
+        for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
+            const int ii = static_cast<int>(fdiv(e, fnc)), c = e - ii * nc;
+            dst[pad((comp * nc + c) * D + Mt + ii)] = make_double2(0.0, 0.0);
+        }
+    }
+    __syncthreads();
+    double2* r = fft_cols(a, sb, A * nc, pl, tw, -1);
+    // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
+    // Hermitian average (see k_kscale.cu), 1/D^3 folded in
+    const int half = D / 2;
+    for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
+        const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
+        const int kz = kz0 + c;
+        double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
+        const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
+                                    __dmul_rn(k[2], k[2]));
+        const double rem = exp(-(1.0 - g.eta) * k2 * g.inv4xi2);
+        const double gval = Gs[e];
+        double2 gh[A];
+#pragma unroll
+        for (int q = 0; q < A; ++q) gh[q] = r[pad((q * nc + c) * D + kx)];
+        double2 out[3];
+        apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
+        if (kx == half || ky == half || kz == half) {
+            if (kx == half) k[0] = -k[0];
+            if (ky == half) k[1] = -k[1];
+            if (kz == half) k[2] = -k[2];
+            double2 o2[3];
+            apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, o2);
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+                out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+            r[pad((p * nc + c) * D + kx)] = make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
+    }
+    __syncthreads();
+    double2* other = (r == a) ? sb : a;
+    double2* r2 = fft_cols(r, other, 3 * nc, pl, tw, +1);
+    for (int comp = 0; comp < 3; ++comp) {
+        double2* dst = Cb + comp * compC + rowoff;
+        for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
+            const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;
+            dst[static_cast<int64_t>(i) * slab + c] = r2[pad((comp * nc + c) * D + i)];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ z inverse
+// row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
+__global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
+                                                 int ncomp, int ncol, const double2* __restrict__ B,
+                                                 double* __restrict__ W) {
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    double2* sb = a + pl.buf_elems;
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
+    const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
+    const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
+    const FDiv fDh = make_fdiv(Dh);
+    __shared__ int64_t row0[64];  // first R/W row of the pair, in doubles
+    __shared__ int64_t brow[64];  // first B row of the pair, in rows of Dh
+    __shared__ int has1[64];
+    if (threadIdx.x < nc) {
+        const int64_t q = q0 + threadIdx.x;
+        const int64_t ci = q / Jp;  // comp * Mt + i
+        const int jp = static_cast<int>(q - ci * Jp);
+        const int64_t comp = ci / Mt, i = ci - comp * Mt;
+        row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
+        brow[threadIdx.x] = ci * Mt + 2 * jp;
+        has1[threadIdx.x] = (2 * jp + 1 < Mt);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * Dh; e += blockDim.x) {
+        const int c = static_cast<int>(fdiv(e, fDh)), k = e - c * Dh;
+        const double2* src = B + brow[c] * Dh + k;
+        double2 x0 = src[0];
+        double2 x1 = has1[c] ? src[Dh] : make_double2(0.0, 0.0);
+        if (k == 0 || k == D / 2) {  // C2R: self-conjugate bins are real
+            x0.y = 0.0;
+            x1.y = 0.0;
+        }
+        // Z[k] = X0 + i X1 ; Z[D-k] = conj(X0) + i conj(X1)
+        a[pad(c * D + k)] = make_double2(x0.x - x1.y, x0.y + x1.x);
+        if (k != 0 && k != D / 2) a[pad(c * D + D - k)] = make_double2(x0.x + x1.y, -x0.y + x1.x);
+    }
+    __syncthreads();
+    double2* r = fft_cols(a, sb, nc, pl, tw, +1);
+    for (int c = 0; c < nc; ++c) {
+        double* row = W + row0[c];
+        const bool h1 = has1[c];
+        for (int n = threadIdx.x; n < Mt; n += blockDim.x) {
+            const double2 z = r[pad(c * D + n)];
+            row[n] = z.x;
+            if (h1) row[Mt + n] = z.y;
+        }
+    }
+}
+
+int maxit_host(int p) { return (16 + p - 1) / p; }
+bool is_reg_radix(int p) {
+    return p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 11 || p == 13;
+}
+
+bool g_consts_ready = false;
+
+void upload_consts() {
+    if (g_consts_ready) return;
+    double cs[4][14] = {}, sn[4][14] = {};
+    const int ps[4] = {5, 7, 11, 13};
+    for (int k = 0; k < 4; ++k)
+        for (int t = 0; t < ps[k]; ++t) {
+            const long double ang = 2.0L * 3.141592653589793238462643383279502884L * t / ps[k];
+            cs[k][t] = static_cast<double>(cosl(ang));
+            sn[k][t] = static_cast<double>(sinl(ang));
+        }
+    FSE_CU(cudaMemcpyToSymbol(c_cos, cs, sizeof cs));
+    FSE_CU(cudaMemcpyToSymbol(c_sin, sn, sizeof sn));
+    g_consts_ready = true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+HostFftPlan make_fft_plan(int D) {
+    HostFftPlan h;
+    std::memset(&h.dev, 0, sizeof h.dev);
+    h.dev.D = D;
+    std::vector<int> rad;
+    int rem = D;
+    while (rem % 8 == 0) { rad.push_back(8); rem /= 8; }
+    while (rem % 4 == 0) { rad.push_back(4); rem /= 4; }
+    while (rem % 2 == 0) { rad.push_back(2); rem /= 2; }
+    for (int p : {3, 5, 7, 11, 13})
+        while (rem % p == 0) { rad.push_back(p); rem /= p; }
+    if (rem > 1) rad.insert(rad.begin(), rem);  // one generic stage for the rest
+    if (static_cast<int>(rad.size()) > kFftMaxStages) throw Error(FSE_EINVAL, "FFT: too many stages");
+    int Ns = 1;
+    h.generic = false;
+    for (size_t s = 0; s < rad.size(); ++s) {
+        const int p = rad[s];
+        h.dev.p[s] = p;
+        h.dev.Ns[s] = Ns;
+        h.dev.tw[s] = static_cast<int>(h.tw.size());
+        const long double two_pi = 2.0L * 3.141592653589793238462643383279502884L;
+        if (is_reg_radix(p)) {
+            for (int k = 0; k < Ns; ++k)
+                for (int r = 1; r < p; ++r) {
+                    const long long num = (static_cast<long long>(r) * k) % (static_cast<long long>(Ns) * p);
+                    const long double ang = -two_pi * num / (static_cast<long double>(Ns) * p);
+                    h.tw.push_back(make_double2(static_cast<double>(cosl(ang)),
+                                                static_cast<double>(sinl(ang))));
+                }
+        } else {
+            h.generic = true;
+            for (int t = 0; t < Ns * p; ++t) {
+                const long double ang = -two_pi * t / (static_cast<long double>(Ns) * p);
+                h.tw.push_back(make_double2(static_cast<double>(cosl(ang)),
+                                            static_cast<double>(sinl(ang))));
+            }
+        }
+        if (h.tw.empty()) h.tw.push_back(make_double2(1.0, 0.0));
+        Ns *= p;
+    }
+    h.dev.nst = static_cast<int>(rad.size());
+    h.radices = rad;
+    h.dev.dD = make_fdiv(D);
+    for (int s = 0; s < h.dev.nst; ++s) {
+        h.dev.dnb[s] = make_fdiv(D / h.dev.p[s]);
+        h.dev.dNs[s] = make_fdiv(h.dev.Ns[s]);
+        h.dev.dP[s] = make_fdiv(h.dev.p[s]);
+        h.dev.dNsP[s] = make_fdiv(h.dev.Ns[s] * h.dev.p[s]);
+    }
+    return h;
+}
+
+// largest column count for `cols_per_unit` columns per unit that fits smem and
+// the register-staged stages (items per thread <= maxit)
+int fft_units_per_cta(const HostFftPlan& h, int cols_per_unit, int threads, size_t smem_cap) {
+    const int D = h.dev.D;
+    int best = 0;
+    for (int u = 1; u <= 64; ++u) {
+        const int cols = u * cols_per_unit;
+        const size_t elems = static_cast<size_t>(cols) * D + (static_cast<size_t>(cols) * D) / 8 + 8;
+        const size_t bytes = (elems * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
+        if (bytes > smem_cap) break;
+        bool ok = true;
+        for (int p : h.radices)
+            if (is_reg_radix(p) && static_cast<long long>(cols) * (D / p) >
+                                       static_cast<long long>(threads) * maxit_host(p))
+                ok = false;
+        if (!ok) break;
+        best = u;
+    }
+    if (best == 0) throw Error(FSE_EINVAL, "FFT: grid size does not fit the shared-memory engine");
+    return best;
+}
+
+static size_t smem_bytes(const HostFftPlan& h, int cols) {
+    const size_t elems = static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
+    return (elems * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
+}
+
+static void set_buf(FftPlan& p, const HostFftPlan& h, int cols) {
+    p.buf_elems = static_cast<int>(static_cast<size_t>(cols) * h.dev.D +
+                                   (static_cast<size_t>(cols) * h.dev.D) / 8 + 8);
+    p.two_bufs = h.generic ? 1 : 0;
+    p.tw_elems = static_cast<int>(h.tw.size());
+}
+
+template <class K>
+static void allow_smem(K kern, size_t bytes) {
+    FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+}
+
+constexpr int kThreads = 256;
+constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
+
+void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw, double2* data,
+                      int ncols, int inverse) {
+    upload_consts();
+    const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
+    FftPlan p = h.dev;
+    set_buf(p, h, u);
+    const size_t sm = smem_bytes(h, u);
+    allow_smem(k_fft_test, sm);
+    k_fft_test<<<(ncols + u - 1) / u, kThreads, sm, L.s>>>(p, d_tw, data, ncols, u,
+                                                            inverse ? +1 : -1);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
+                           int ncomp, const double* R, double2* B, double2* C) {
+    upload_consts();
+    const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    {
+        const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
+        FftPlan p = h.dev;
+        set_buf(p, h, u);
+        const size_t sm = smem_bytes(h, u);
+        allow_smem(k_zfwd, sm);
+        const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+        k_zfwd<<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(p, d_tw, Mt,
+                                                                                   ncomp, u, R, B);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+    }
+    {
+        const int u = std::min(fft_units_per_cta(h, 1, kThreads, kSmemCap), Dh);
+        FftPlan p = h.dev;
+        set_buf(p, h, u);
+        const size_t sm = smem_bytes(h, u);
+        allow_smem(k_ypass<false>, sm);
+        const int ntz = (Dh + u - 1) / u;
+        k_ypass<false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz), kThreads,
+                         sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+    }
+}
+
+void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                       const GridParams& g, int kind, const double* G, double2* C) {
+    upload_consts();
+    const int A = arity_of(kind);
+    const int D = h.dev.D, Dh = D / 2 + 1;
+    const int u = std::min(fft_units_per_cta(h, A, kThreads, kSmemCap - 16 * D), Dh);
+    FftPlan p = h.dev;
+    set_buf(p, h, A * u);
+    const size_t sm = smem_bytes(h, A * u) + sizeof(double) * u * D;
+    const int ntz = (Dh + u - 1) / u;
+    const unsigned blocks = static_cast<unsigned>(D) * ntz;
+    if (kind == FSE_STOKESLET) {
+        allow_smem(k_xscale<FSE_STOKESLET>, sm);
+        k_xscale<FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+    } else if (kind == FSE_STRESSLET) {
+        allow_smem(k_xscale<FSE_STRESSLET>, sm);
+        k_xscale<FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+    } else {
+        allow_smem(k_xscale<FSE_ROTLET>, sm);
+        k_xscale<FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+    }
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
+                           int ncomp, double2* C, double2* B, double* W) {
+    upload_consts();
+    const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    {
+        const int u = std::min(fft_units_per_cta(h, 1, kThreads, kSmemCap), Dh);
+        FftPlan p = h.dev;
+        set_buf(p, h, u);
+        const size_t sm = smem_bytes(h, u);
+        allow_smem(k_ypass<true>, sm);
+        const int ntz = (Dh + u - 1) / u;
+        k_ypass<true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz), kThreads,
+                        sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+    }
+    {
+        const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
+        FftPlan p = h.dev;
+        set_buf(p, h, u);
+        const size_t sm = smem_bytes(h, u);
+        allow_smem(k_zinv, sm);
+        const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+        k_zinv<<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(p, d_tw, Mt,
+                                                                                   ncomp, u, B, W);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+    }
+}
+
+}  // namespace fsecu

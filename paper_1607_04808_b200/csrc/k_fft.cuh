@@ -1,0 +1,72 @@
+// k_fft.cuh -- the hand-written fp64 FFT engine (k_fft.cu) interface.
+#pragma once
+
+#include <vector>
+
+#include "fse_internal.cuh"
+
+namespace fsecu {
+
+constexpr int kFftMaxStages = 16;
+
+// division by an invariant 32-bit divisor d via multiply-high (n < 2^31):
+// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1
+struct FDiv {
+    uint32_t d, m, l;
+};
+
+inline __host__ __device__ FDiv make_fdiv(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+    return FDiv{d, static_cast<uint32_t>(m), l};
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FDiv& f) {
+    return (__umulhi(n, f.m) + n) >> f.l;
+}
+__device__ __forceinline__ uint32_t fmod_(uint32_t n, uint32_t q, const FDiv& f) { return n - q * f.d; }
+#endif
+
+// device-side plan of a length-D transform (passed by value to kernels)
+struct FftPlan {
+    int D;
+    int nst;
+    int p[kFftMaxStages];   // radix of each stage
+    int Ns[kFftMaxStages];  // product of the earlier radices
+    int tw[kFftMaxStages];  // offset of the stage's twiddle table (double2 units)
+    FDiv dnb[kFftMaxStages];   // D / p
+    FDiv dNs[kFftMaxStages];   // Ns
+    FDiv dP[kFftMaxStages];    // p
+    FDiv dNsP[kFftMaxStages];  // Ns p
+    FDiv dD;                   // D
+    int tw_elems;           // twiddle table length (copied to shared memory)
+    int two_bufs;           // a generic stage needs a second column buffer
+    int buf_elems;          // padded column-buffer length (set per launch)
+};
+
+struct HostFftPlan {
+    FftPlan dev;
+    std::vector<double2> tw;  // concatenated twiddle tables
+    std::vector<int> radices;
+    bool generic = false;     // a non-register (generic DFT) stage is present
+};
+
+HostFftPlan make_fft_plan(int D);
+
+// diagnostics: FFT of ncols contiguous columns of length D (in place, device)
+void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw, double2* data,
+                      int ncols, int inverse);
+
+// R (a x Mt^3 real) -> B (a x Mt x Mt x Dh) -> C (a x Mt x D x Dh)
+void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
+                           int ncomp, const double* R, double2* B, double2* C);
+// C: forward x-FFT, multiply by A_eff(k) G(k) / D^3, inverse x-FFT, in place (3 comps out)
+void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                       const GridParams& g, int kind, const double* G, double2* C);
+// C (3 comps) -> B (j < Mt) -> W (3 x Mt^3 real)
+void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
+                           int ncomp, double2* C, double2* B, double* W);
+
+}  // namespace fsecu

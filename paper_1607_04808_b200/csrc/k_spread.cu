@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128) k_spread(GridParams g, const int32_t* __r
 
     const int y = wy_lo + ly, z = wz_lo + lz;
     if (y >= g.Mt || z >= g.Mt) return;
-    const int64_t rowpitch = g.D + 2;
+    const int64_t rowpitch = g.rowp;
 #pragma unroll
     for (int r = 0; r < TX; ++r) {
         const int x = x0n + r;
@@ -153,7 +153,7 @@ __global__ void k_extract(GridParams g, const double* __restrict__ X, int a,
     if (q >= vol * a) return;
     const int64_t c = q / vol, r = q % vol;
     const int64_t z = r % g.Mt, y = (r / g.Mt) % g.Mt, x = r / (static_cast<int64_t>(g.Mt) * g.Mt);
-    out[q] = X[c * g.comp + x * g.plane + y * (g.D + 2) + z];
+    out[q] = X[c * g.comp + x * g.plane + y * g.rowp + z];
 }
 
 }  // namespace
