@@ -146,8 +146,19 @@ __device__ double d_bhat(double k, double R) {
         for (int m = NT - 2; m >= 0; --m) acc = acc * t2 + c[m];
         return piR4 * acc;
     }
-    const double num = (2.0 - t * t) * cos(t) + 2.0 * t * sin(t) - 2.0;
-    return 4.0 * M_PI * num / (t * t * t * t) * (R * R * R * R);
+    // The reference forms R k in long double: at large Rk the rounding of the
+    // double product (~1e-16 Rk absolute) would move cos/sin by ~1e-13 and
+    // the stresslet multiplier amplifies that.  Carry the exact product as
+    // th + tl (FMA two-product) and correct cos/sin to first order in tl.
+    const double th = R * k;
+    const double tl = fma(R, k, -th);
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double c = cs - sn * tl, s = sn + cs * tl;
+    const double t2 = fma(th, th, 2.0 * th * tl);
+    const double num = (2.0 - t2) * c + 2.0 * th * s + 2.0 * tl * s - 2.0;
+    const double t4 = t2 * t2;
+    return 4.0 * M_PI * num / t4 * (R * R * R * R);
 }
 
 // half spectrum of the sM^3 grid, (greens.cpp:62-79): k2(a) = (dk n_a)^2,

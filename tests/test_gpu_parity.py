@@ -183,3 +183,18 @@ def test_errors(fse, ctx, rng):
     two = fse.SourceSystem([[0.1, 0.2, 0.3], [0.1, 0.2, 0.3]], [[1, 0, 0], [0, 1, 0]], 1.0)
     with pytest.raises(fse.DomainError):
         ctx.direct_sum(two, 0, two.positions, True)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n", [2, 60])
+def test_total_sum_large_support(fse, ctx, oracle, rng, kind, n):
+    """P = 32 (> 25): the gather's multi-chunk z path and wide spread windows."""
+    cfg, ocfg, s, tgt, g, table = _pipeline_case(fse, ctx, oracle, rng, kind,
+                                                 (1.0, 6.0, 1.0, 28, 32), n, False)
+    got = ctx.total_sum(s, kind, cfg, tgt, g)
+    want = oracle.total_sum(ocfg, kind, s.positions, s.strengths, tgt, table)
+    assert rel_max(got, want) <= 1e-11
+    if n == 2:  # accuracy vs O(N^2) matches the oracle's own (test_spectral.cpp:185-196)
+        ref = oracle.direct_sum(kind, s.positions, s.strengths, s.positions, True)
+        e_gpu, e_or = fse.rms_error(got, ref, True), fse.rms_error(want, ref, True)
+        assert e_gpu < max(1e-12, 2 * e_or)
