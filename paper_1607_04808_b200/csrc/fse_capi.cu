@@ -490,20 +490,10 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + 7) / 8;
         uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
         const double h3 = g.h * g.h * g.h;  // prefac is folded into the x weights
-        // the plane-streamed gather trades L2 traffic for barriers; at uniform
-        // cfg2 density (~21 targets per 8^3 region) the warp-group kernel wins
-        const bool planes = gather_planes_ok(g) && std::getenv("FSE_GATHER_PLANES");
-        int32_t* gkey = nullptr;
-        if (!planes) {
-            gkey = buf<int32_t>(c, "gkey", max_groups);
-            launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
-        }
+        int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
+        launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
         FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
-        if (planes)
-            launch_gather_planes(L, g, tg.i0s, tg.w, tg.tstart, goff, X, tg.perm, h3, uF);
-        else
-            launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3,
-                          uF);
+        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, uF);
         FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
     }
 

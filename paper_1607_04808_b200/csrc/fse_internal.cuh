@@ -128,11 +128,6 @@ void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    const int32_t* tstart, const int32_t* gkey, const int32_t* goff,
                    int64_t max_groups, const double* X, const uint32_t* perm, double scale,
                    double* u);
-// plane-streamed gather (P + 7 <= 32): no group table needed beyond goff
-bool gather_planes_ok(const GridParams& g);
-void launch_gather_planes(const Launch& L, const GridParams& g, const int32_t* i0s,
-                          const double* w, const int32_t* tstart, const int32_t* goff,
-                          const double* X, const uint32_t* perm, double scale, double* u);
 void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount);
 void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* goff,
                         int64_t nkeys, int32_t* gkey);

@@ -13,6 +13,8 @@
 // predicating the whole warp on every candidate.
 //
 // Roofline: FP64 (transcendental-heavy pair work).
+#include <cmath>
+
 #include "fse_internal.cuh"
 
 namespace fsecu {
@@ -22,26 +24,48 @@ namespace {
 constexpr int TPB = 128, CH = 128;
 constexpr double kInvSqrtPi = 0.5641895835477562869;
 
+// erfc(x) = exp(-x^2) erfcx(x); erfcx on [0, kErfXMax) from a piecewise
+// Chebyshev fit (kErfNI intervals, degree kErfDeg, monomial in the local
+// t in [-1, 1]) computed on the host in long double from erfcl/expl
+// (|error| < 1e-17 relative).  One exp + a degree-12 Horner replace CUDA's
+// range-branched erfc (~190 SASS instructions) plus the separate exp.
+constexpr int kErfNI = 32, kErfDeg = 12;
+constexpr double kErfXMax = 6.5;
+__constant__ double c_erfcx[kErfDeg + 1][kErfNI];
+
+__device__ __forceinline__ double erfcx_tab(double x, const double (*tab)[kErfNI]) {
+    const double u = x * (kErfNI / kErfXMax);
+    const int iv = min(static_cast<int>(u), kErfNI - 1);
+    const double t = 2.0 * (u - iv) - 1.0;
+    double acc = tab[kErfDeg][iv];
+#pragma unroll
+    for (int j = kErfDeg - 1; j >= 0; --j) acc = fma(acc, t, tab[j][iv]);
+    return acc;
+}
+
+// screened pair kernels of realspace.cpp:13-58, rearranged around
+// inv = 1/r (rsqrt) and erfc = gauss * erfcx: no divisions
 template <int KIND>
 __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2, double xi,
-                                     const double* f, double acc[3]) {
-    const double rn = sqrt(r2);
+                                     const double* f, const double (*tab)[kErfNI], double acc[3]) {
+    const double inv = rsqrt(r2);
+    const double rn = r2 * inv;
     const double xr = xi * rn;
     const double gauss = exp(-xr * xr);
-    const double erfc_xr = erfc(xr);
-    const double inv = 1.0 / rn;
+    const double erfc_xr = xr < kErfXMax ? gauss * erfcx_tab(xr, tab) : erfc(xr);
     const double rh[3] = {inv * rx, inv * ry, inv * rz};
+    const double cg = 2.0 * xi * kInvSqrtPi * gauss;  // 2 xi e^{-x^2} / sqrt(pi)
     if (KIND == FSE_STOKESLET) {
-        const double a = 2.0 * (xi * gauss * kInvSqrtPi + erfc_xr / (2.0 * rn));
-        const double b = 4.0 * xi * kInvSqrtPi * gauss;
-        const double amb = a - b;
+        // a = 2 (xi g/sqrt(pi) + erfc/(2r)), b = 4 xi g/sqrt(pi)
+        const double e_r = erfc_xr * inv;
+        const double a = cg + e_r;
+        const double amb = e_r - cg;
         const double s = a * (rh[0] * f[0] + rh[1] * f[1] + rh[2] * f[2]);
 #pragma unroll
         for (int j = 0; j < 3; ++j) acc[j] += amb * f[j] + s * rh[j];
     } else if (KIND == FSE_STRESSLET) {
-        const double c1 = -(2.0 / rn) *
-            (3.0 * erfc_xr / rn + 2.0 * xi * kInvSqrtPi * (3.0 + 2.0 * xr * xr) * gauss);
-        const double c2 = 4.0 * xi * xi * xi * kInvSqrtPi * gauss * rn;
+        const double c1 = -2.0 * inv * (3.0 * erfc_xr * inv + cg * (3.0 + 2.0 * xr * xr));
+        const double c2 = 2.0 * xi * xi * cg * rn;  // 4 xi^3 g r / sqrt(pi)
         double rfr = 0, f_r[3] = {0, 0, 0}, r_f[3] = {0, 0, 0};
 #pragma unroll
         for (int l = 0; l < 3; ++l)
@@ -56,7 +80,7 @@ __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2,
 #pragma unroll
         for (int j = 0; j < 3; ++j) acc[j] += s * rh[j] + c2 * (f_r[j] + r_f[j]);
     } else {
-        const double c = erfc_xr / r2 + 2.0 * xi * kInvSqrtPi * gauss / rn;
+        const double c = (erfc_xr * inv + cg) * inv;  // erfc/r^2 + 2 xi g/(sqrt(pi) r)
         acc[0] += c * (f[1] * rh[2] - f[2] * rh[1]);
         acc[1] += c * (f[2] * rh[0] - f[0] * rh[2]);
         acc[2] += c * (f[0] * rh[1] - f[1] * rh[0]);
@@ -80,6 +104,9 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     __shared__ double sx[CH], sy[CH], sz[CH];
     __shared__ double sf[CH][A];
     __shared__ int nb_start[27], nb_pref[28];
+    __shared__ double tab[kErfDeg + 1][kErfNI];
+    for (int e = threadIdx.x; e < (kErfDeg + 1) * kErfNI; e += blockDim.x)
+        tab[e / kErfNI][e % kErfNI] = c_erfcx[e / kErfNI][e % kErfNI];
 
     if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // grid is an upper bound
     const int cell = items[2 * blockIdx.x];
@@ -151,7 +178,7 @@ __global__ void __launch_bounds__(TPB) k_realspace(
                 m &= m - 1;
                 const int j = wd * 32 + b;
                 const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
-                pair<KIND>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], acc);
+                pair<KIND>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
             }
         }
         __syncthreads();
@@ -179,6 +206,59 @@ __global__ void k_fill_items(const int32_t* __restrict__ off, int64_t ncell,
         items[2 * it] = static_cast<int32_t>(c);
         items[2 * it + 1] = it - off[c];
     }
+}
+
+// Chebyshev fit of erfcx on each interval, long double, converted to
+// monomial coefficients in the local variable t in [-1, 1]
+void build_erfcx_table(double out[kErfDeg + 1][kErfNI]) {
+    const int n = kErfDeg + 1;
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (int iv = 0; iv < kErfNI; ++iv) {
+        const long double a = kErfXMax * iv / static_cast<long double>(kErfNI);
+        const long double b = kErfXMax * (iv + 1) / static_cast<long double>(kErfNI);
+        long double fv[n], cheb[n];
+        for (int k = 0; k < n; ++k) {
+            const long double t = cosl(PI * (k + 0.5L) / n);
+            const long double x = 0.5L * (a + b) + 0.5L * (b - a) * t;
+            fv[k] = expl(x * x) * erfcl(x);
+        }
+        for (int j = 0; j < n; ++j) {
+            long double sum = 0;
+            for (int k = 0; k < n; ++k) sum += fv[k] * cosl(PI * j * (k + 0.5L) / n);
+            cheb[j] = sum * 2.0L / n;
+        }
+        cheb[0] *= 0.5L;
+        // sum_j cheb_j T_j(t) -> sum_j mono_j t^j
+        long double mono[n] = {}, Tprev[n] = {}, Tcur[n] = {}, Tnext[n];
+        Tprev[0] = 1;            // T0
+        Tcur[1] = 1;             // T1
+        for (int j = 0; j < n; ++j) mono[j] += cheb[0] * Tprev[j];
+        for (int j = 0; j < n; ++j) mono[j] += cheb[1] * Tcur[j];
+        for (int d = 2; d < n; ++d) {
+            for (int j = 0; j < n; ++j) Tnext[j] = -Tprev[j] + (j > 0 ? 2 * Tcur[j - 1] : 0);
+            for (int j = 0; j < n; ++j) mono[j] += cheb[d] * Tnext[j];
+            for (int j = 0; j < n; ++j) {
+                Tprev[j] = Tcur[j];
+                Tcur[j] = Tnext[j];
+            }
+        }
+        for (int j = 0; j < n; ++j) out[j][iv] = static_cast<double>(mono[j]);
+    }
+}
+
+void ensure_erfcx_table() {
+    static bool ready[64] = {};
+    int dev = 0;
+    FSE_CU(cudaGetDevice(&dev));
+    if (dev < 64 && ready[dev]) return;
+    static double tab[kErfDeg + 1][kErfNI];
+    static bool built = false;
+    if (!built) {
+        build_erfcx_table(tab);
+        built = true;
+    }
+    FSE_CU(cudaMemcpyToSymbol(c_erfcx, tab, sizeof tab));
+    if (dev < 64) ready[dev] = true;
 }
 
 }  // namespace
@@ -209,6 +289,7 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
     (void)ns;
     const int64_t nitems = max_items;
     if (nitems <= 0) return;
+    ensure_erfcx_table();
     const double rc2 = rc * rc;
     const unsigned b = static_cast<unsigned>(nitems);
     if (kind == FSE_STOKESLET)
