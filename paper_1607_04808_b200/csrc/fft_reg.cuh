@@ -1,0 +1,252 @@
+// fft_reg.cuh -- register-resident FFT building blocks for k_fft.cu.
+//
+// rfft<N>(v): in-place FFT of N complex values held in registers, decimation
+// in time with a compile-time radix split N = P x M (radices 8, 4, 2, 3, 5,
+// 7, 11, 13), so every index is a constant after unrolling.  Twiddles
+// W_N^t come from a shared-memory table at a compile-time offset
+// (tw_off<N>()), loaded as broadcasts.
+//
+// fft_cols_2l<D1, D2>: the column FFT of length D = D1 D2 ("four-step"):
+//   pass 1: thread (col, n2) holds x[n1 D2 + n2], n1 < D1, does FFT_D1,
+//           multiplies by W_D^{n2 k1} and writes [k1][n2] to shared memory;
+//   pass 2: thread (col, k1) reads the D2 values, does FFT_D2 and writes
+//           X[k1 + D1 k2].
+// Two shared-memory round trips per element instead of one per radix stage.
+#pragma once
+
+#include "fse_internal.cuh"
+
+namespace fsecu {
+namespace freg {
+
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cis(double2 a, int s) {
+    return s > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// ---- small DFTs (sign s: -1 forward, +1 inverse)
+template <int P>
+struct Dft;
+template <>
+struct Dft<2> {
+    __device__ __forceinline__ static void run(double2* v, int) {
+        const double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    }
+};
+template <>
+struct Dft<3> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        const double h = 0.86602540378443864676372317075293618;
+        const double2 t1 = cadd(v[1], v[2]);
+        const double2 t2 = make_double2(fma(-0.5, t1.x, v[0].x), fma(-0.5, t1.y, v[0].y));
+        const double2 d = csub(v[1], v[2]);
+        const double2 t3 = cis(make_double2(h * d.x, h * d.y), s);
+        v[0] = cadd(v[0], t1);
+        v[1] = cadd(t2, t3);
+        v[2] = csub(t2, t3);
+    }
+};
+template <>
+struct Dft<4> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        const double2 s0 = cadd(v[0], v[2]), d0 = csub(v[0], v[2]);
+        const double2 s1 = cadd(v[1], v[3]), d1 = cis(csub(v[1], v[3]), s);
+        v[0] = cadd(s0, s1);
+        v[2] = csub(s0, s1);
+        v[1] = cadd(d0, d1);
+        v[3] = csub(d0, d1);
+    }
+};
+template <>
+struct Dft<8> {
+    __device__ __forceinline__ static void run(double2* v, int s) {
+        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        Dft<4>::run(e, s);
+        Dft<4>::run(o, s);
+        const double r = 0.70710678118654752440084436210484904;
+        const double2 o1 = o[1], o3 = o[3];
+        o[1] = make_double2(r * (o1.x - s * o1.y), r * (o1.y + s * o1.x));
+        o[2] = cis(o[2], s);
+        o[3] = make_double2(r * (-o3.x - s * o3.y), r * (-o3.y + s * o3.x));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = cadd(e[q], o[q]);
+            v[q + 4] = csub(e[q], o[q]);
+        }
+    }
+};
+
+// cos / sin (2 pi t / p) for p = 5, 7, 11, 13, filled by the host
+__constant__ double c_rcos[4][14];
+__constant__ double c_rsin[4][14];
+
+template <int P, int T>
+struct DftOdd {
+    __device__ __forceinline__ static void run(double2* v, int sgn) {
+        constexpr int H = (P - 1) / 2;
+        double2 sr[H], dr[H];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+            sr[r - 1] = cadd(v[r], v[P - r]);
+            dr[r - 1] = csub(v[r], v[P - r]);
+        }
+        const double2 v0 = v[0];
+        double2 y0 = v0;
+#pragma unroll
+        for (int r = 0; r < H; ++r) y0 = cadd(y0, sr[r]);
+#pragma unroll
+        for (int q = 1; q <= H; ++q) {
+            double2 A = v0, B = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 1; r <= H; ++r) {
+                const int t = (r * q) % P;
+                const double c = c_rcos[T][t], sn = c_rsin[T][t];
+                A.x = fma(sr[r - 1].x, c, A.x);
+                A.y = fma(sr[r - 1].y, c, A.y);
+                B.x = fma(dr[r - 1].x, sn, B.x);
+                B.y = fma(dr[r - 1].y, sn, B.y);
+            }
+            const double2 iB = cis(B, sgn);
+            v[q] = cadd(A, iB);
+            v[P - q] = csub(A, iB);
+        }
+        v[0] = y0;
+    }
+};
+template <>
+struct Dft<5> : DftOdd<5, 0> {};
+template <>
+struct Dft<7> : DftOdd<7, 1> {};
+template <>
+struct Dft<11> : DftOdd<11, 2> {};
+template <>
+struct Dft<13> : DftOdd<13, 3> {};
+
+// ---- compile-time radix choice and twiddle-table layout
+__host__ __device__ constexpr bool is_base(int n) {
+    return n == 2 || n == 3 || n == 4 || n == 5 || n == 7 || n == 8 || n == 11 || n == 13;
+}
+__host__ __device__ constexpr int first_radix(int n) {
+    return (n % 8 == 0) ? 8 : (n % 4 == 0) ? 4 : (n % 2 == 0) ? 2 : (n % 3 == 0) ? 3
+         : (n % 5 == 0) ? 5 : (n % 7 == 0) ? 7 : (n % 11 == 0) ? 11 : 13;
+}
+// composite register sizes that own a twiddle table, in table order
+constexpr int kRegSizes[] = {6, 9, 10, 12, 14, 15, 16, 18, 20, 21, 22, 24, 26, 28, 30, 32,
+                             33, 35, 36, 39, 40, 44, 48, 52, 56, 64};
+constexpr int kNumRegSizes = sizeof(kRegSizes) / sizeof(int);
+__host__ __device__ constexpr int tw_off_of(int n) {
+    int off = 0;
+    for (int i = 0; i < kNumRegSizes; ++i) {
+        if (kRegSizes[i] == n) return off;
+        off += kRegSizes[i];
+    }
+    return -1;
+}
+__host__ __device__ constexpr int tw_total() {
+    int off = 0;
+    for (int i = 0; i < kNumRegSizes; ++i) off += kRegSizes[i];
+    return off;
+}
+
+template <int N>
+__device__ __forceinline__ double2 twid(int t, int sgn, const double2* tab) {
+    constexpr int off = tw_off_of(N);
+    static_assert(off >= 0, "register FFT size without a twiddle table");
+    double2 w = tab[off + t];
+    if (sgn > 0) w.y = -w.y;
+    return w;
+}
+
+template <int N>
+__device__ __forceinline__ void rfft(double2* v, int sgn, const double2* tab) {
+    if constexpr (is_base(N)) {
+        Dft<N>::run(v, sgn);
+    } else {
+        constexpr int P = first_radix(N), M = N / P;
+        double2 sub[P][M];
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+#pragma unroll
+            for (int j = 0; j < M; ++j) sub[r][j] = v[j * P + r];
+#pragma unroll
+        for (int r = 0; r < P; ++r) rfft<M>(sub[r], sgn, tab);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            double2 y[P];
+#pragma unroll
+            for (int r = 0; r < P; ++r) {
+                y[r] = sub[r][k];
+                if ((r * k) % N != 0) y[r] = cmul(y[r], twid<N>((r * k) % N, sgn, tab));
+            }
+            Dft<P>::run(y, sgn);
+#pragma unroll
+            for (int q = 0; q < P; ++q) v[k + M * q] = y[q];
+        }
+    }
+}
+
+// Column FFT of length D1*D2 on `ncol` columns stored at buf[pad(c*D + n)].
+// Requires ncol*D2 <= blockDim.x and ncol*D1 <= blockDim.x (one item per thread).
+// twD: W_D^t, t < D; tab: small-size twiddles (tw_off_of layout).
+template <int D1, int D2>
+__device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
+                                            const double2* twD, const double2* tab) {
+    constexpr int D = D1 * D2;
+    const int tid = threadIdx.x;
+    // pass 1: item (c, n2)
+    double2 v[D1];
+    const bool a1 = tid < ncol * D2;
+    int c1 = 0, n2 = 0;
+    if (a1) {
+        c1 = tid / D2;
+        n2 = tid - c1 * D2;
+#pragma unroll
+        for (int n1 = 0; n1 < D1; ++n1) v[n1] = buf[pad(c1 * D + n1 * D2 + n2)];
+        rfft<D1>(v, sgn, tab);
+        int t = 0;  // n2 * k1 mod D
+#pragma unroll
+        for (int k1 = 0; k1 < D1; ++k1) {
+            if (k1 > 0) {
+                double2 w = twD[t];
+                if (sgn > 0) w.y = -w.y;
+                v[k1] = cmul(v[k1], w);
+            }
+            t += n2;
+            if (t >= D) t -= D;
+        }
+    }
+    __syncthreads();
+    if (a1) {
+#pragma unroll
+        for (int k1 = 0; k1 < D1; ++k1) buf[pad(c1 * D + k1 * D2 + n2)] = v[k1];
+    }
+    __syncthreads();
+    // pass 2: item (c, k1)
+    double2 u[D2];
+    const bool a2 = tid < ncol * D1;
+    int c2 = 0, k1 = 0;
+    if (a2) {
+        c2 = tid / D1;
+        k1 = tid - c2 * D1;
+#pragma unroll
+        for (int j = 0; j < D2; ++j) u[j] = buf[pad(c2 * D + k1 * D2 + j)];
+        rfft<D2>(u, sgn, tab);
+    }
+    __syncthreads();
+    if (a2) {
+#pragma unroll
+        for (int k2 = 0; k2 < D2; ++k2) buf[pad(c2 * D + k1 + D1 * k2)] = u[k2];
+    }
+    __syncthreads();
+}
+
+}  // namespace freg
+}  // namespace fsecu

@@ -446,12 +446,16 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
     FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_START], 0));
 
     double* uR = nullptr;
-    if (want_r) {
+    // The FP64-bound real-space sum runs on stream s1.  With the Fourier part
+    // it is enqueued after the source preparation (below), so the short,
+    // latency-bound prep kernels do not queue behind its CTAs.
+    auto enqueue_real = [&]() {
         uR = want_f ? buf<double>(c, "uR", 3 * nt) : d_u;
         FSE_CU(cudaEventRecord(c->ev[EV_R0], c->s1));
         real_part(c, kind, d_pos, d_str, n, box_side, cfg->xi, cfg->rc, d_tgt, nt, tas, uR);
         FSE_CU(cudaEventRecord(c->ev[EV_R1], c->s1));
-    }
+    };
+    if (want_r && !want_f) enqueue_real();
 
     double* uF = nullptr;
     if (want_f) {
@@ -463,6 +467,11 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         launch_quad_table(L, g, qtab);
         Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, tas ? 1 : 0, qtab);
         FSE_CU(cudaEventRecord(c->ev[EV_PREP], c->s0));
+        static const bool serial = std::getenv("FSE_SERIAL") != nullptr;  // profiling aid
+        if (want_r && !serial) {
+            FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_PREP], 0));
+            enqueue_real();
+        }
         // R: a compact Mt^3 real grids (every node is written by exactly one
         // spread tile, so no memset); B, C: pruned spectra (k_fft.cu)
         const int64_t Dh = g.Dh;
@@ -487,7 +496,8 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         launch_group_counts(L, tg.tstart, g.nkeys, gcnt);
         exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
         // upper bound on groups: one partial group per non-empty key + nt/8
-        const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + 7) / 8;
+        const int gk = gather_group_size();
+        const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + gk - 1) / gk;
         uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
         const double h3 = g.h * g.h * g.h;  // prefac is folded into the x weights
         int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
@@ -495,6 +505,10 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
         launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, uF);
         FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
+        if (want_r && serial) {
+            FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_QUAD], 0));
+            enqueue_real();
+        }
     }
 
     if (want_r) {

@@ -129,6 +129,7 @@ void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    int64_t max_groups, const double* X, const uint32_t* perm, double scale,
                    double* u);
 void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount);
+int gather_group_size();
 void launch_fill_groups(const Launch& L, const int32_t* tstart, const int32_t* goff,
                         int64_t nkeys, int32_t* gkey);
 

@@ -4,9 +4,8 @@
 // Why not cuFFT: measured on B200 at D = 624 (tools/fft_probe.cu), a 3D
 // D2Z runs at ~0.5 TB/s effective and the strided 1D x-pass the pruned
 // transform needs takes 7.2 ms per component (it transposes through a
-// full-size workspace), while a contiguous batched pass streams at ~6.4 TB/s.
-// Writing the passes ourselves lets every pass touch HBM once and skip the
-// known zeros:
+// full-size workspace).  Writing the passes ourselves lets every pass touch
+// HBM once and skip the known zeros:
 //
 //   R  [i][j][n]   Mt^3 real   (spread output, compact)
 //   zfwd: rows (i,j), two real rows per complex FFT, Mt inputs    -> B [i][j][kz]  Mt x Mt x Dh
@@ -19,17 +18,24 @@
 // The planes i >= Mt of the x-pass input and j >= Mt of the y-pass input are
 // zeros that are never stored; outputs outside the window are never written.
 //
-// Engine: a CTA holds NCOL columns of length D in shared memory (column-major,
-// one 16-byte pad every 8 elements against bank conflicts) and runs a Stockham
-// autosort FFT, one __syncthreads-separated stage per radix.  Radices 2/3/4/5/
-// 7/8/11/13 are register butterflies (a thread loads all its butterflies'
-// inputs before the barrier and stores after, so a stage runs in place);
-// any other factor runs as one generic DFT stage through a second buffer.
-// Twiddles W_{Ns p}^{r k} come from host-computed tables (long double).
+// Column engines (a CTA holds NCOL columns of length D in shared memory,
+// column-major with one 16-byte pad every 8 elements against bank conflicts):
+//  ENG 0: Stockham autosort, one __syncthreads-separated stage per radix
+//         (register butterflies for 2/3/4/5/7/8/11/13, one generic DFT stage
+//         through a second buffer for any other factor, e.g. 97 in D = 194);
+//  ENG>0: two-level register engine (fft_reg.cuh) for D = D1 D2 with
+//         register-friendly D1, D2 (624 = 24 x 26, 1200 = 30 x 40,
+//         704 = 22 x 32, 242 = 11 x 22): two shared-memory round trips per
+//         element instead of one per radix stage.
+// Twiddles come from host tables computed in long double, staged in shared
+// memory per CTA.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
+#include "fft_reg.cuh"
 #include "fse_internal.cuh"
 #include "k_fft.cuh"
 
@@ -37,121 +43,12 @@ namespace fsecu {
 
 namespace {
 
-__constant__ double c_cos[4][14];  // cos(2 pi t / p) for p = 5, 7, 11, 13
-__constant__ double c_sin[4][14];
-
-__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-// i * s * a  (s = +-1)
-__device__ __forceinline__ double2 cis(double2 a, int s) {
-    return s > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
-}
-
-template <int P>
-struct Dft;
-
-template <>
-struct Dft<2> {
-    __device__ __forceinline__ static void run(double2* v, int) {
-        const double2 a = v[0], b = v[1];
-        v[0] = cadd(a, b);
-        v[1] = csub(a, b);
-    }
-};
-
-template <>
-struct Dft<3> {
-    __device__ __forceinline__ static void run(double2* v, int s) {
-        const double h = 0.86602540378443864676372317075293618;
-        const double2 t1 = cadd(v[1], v[2]);
-        const double2 t2 = make_double2(v[0].x - 0.5 * t1.x, v[0].y - 0.5 * t1.y);
-        const double2 d = csub(v[1], v[2]);
-        const double2 t3 = cis(make_double2(h * d.x, h * d.y), s);  // i s (sqrt3/2) (v1 - v2)
-        v[0] = cadd(v[0], t1);
-        v[1] = cadd(t2, t3);
-        v[2] = csub(t2, t3);
-    }
-};
-
-template <>
-struct Dft<4> {
-    __device__ __forceinline__ static void run(double2* v, int s) {
-        const double2 s0 = cadd(v[0], v[2]), d0 = csub(v[0], v[2]);
-        const double2 s1 = cadd(v[1], v[3]), d1 = cis(csub(v[1], v[3]), s);
-        v[0] = cadd(s0, s1);
-        v[2] = csub(s0, s1);
-        v[1] = cadd(d0, d1);
-        v[3] = csub(d0, d1);
-    }
-};
-
-template <>
-struct Dft<8> {
-    __device__ __forceinline__ static void run(double2* v, int s) {
-        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
-        Dft<4>::run(e, s);
-        Dft<4>::run(o, s);
-        const double r = 0.70710678118654752440084436210484904;
-        // o[q] *= w^q, w = exp(s 2 pi i / 8) = r (1 + s i)
-        const double2 o1 = o[1], o3 = o[3];
-        o[1] = make_double2(r * (o1.x - s * o1.y), r * (o1.y + s * o1.x));
-        o[2] = cis(o[2], s);
-        o[3] = make_double2(r * (-o3.x - s * o3.y), r * (-o3.y + s * o3.x));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            v[q] = cadd(e[q], o[q]);
-            v[q + 4] = csub(e[q], o[q]);
-        }
-    }
-};
-
-// odd prime p via conjugate pairs: y_q = v0 + sum_r s_r cos + i s sum_r d_r sin
-template <int P, int T>
-struct DftOdd {
-    __device__ __forceinline__ static void run(double2* v, int sgn) {
-        constexpr int H = (P - 1) / 2;
-        double2 sr[H], dr[H];
-#pragma unroll
-        for (int r = 1; r <= H; ++r) {
-            sr[r - 1] = cadd(v[r], v[P - r]);
-            dr[r - 1] = csub(v[r], v[P - r]);
-        }
-        const double2 v0 = v[0];
-        double2 y0 = v0;
-#pragma unroll
-        for (int r = 0; r < H; ++r) y0 = cadd(y0, sr[r]);
-#pragma unroll
-        for (int q = 1; q <= H; ++q) {
-            double2 A = v0, B = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int r = 1; r <= H; ++r) {
-                const int t = (r * q) % P;
-                const double c = c_cos[T][t], sn = c_sin[T][t];
-                A.x = fma(sr[r - 1].x, c, A.x);
-                A.y = fma(sr[r - 1].y, c, A.y);
-                B.x = fma(dr[r - 1].x, sn, B.x);
-                B.y = fma(dr[r - 1].y, sn, B.y);
-            }
-            const double2 iB = cis(B, sgn);
-            v[q] = cadd(A, iB);
-            v[P - q] = csub(A, iB);
-        }
-        v[0] = y0;
-    }
-};
-template <>
-struct Dft<5> : DftOdd<5, 0> {};
-template <>
-struct Dft<7> : DftOdd<7, 1> {};
-template <>
-struct Dft<11> : DftOdd<11, 2> {};
-template <>
-struct Dft<13> : DftOdd<13, 3> {};
+using freg::cadd;
+using freg::cis;
+using freg::cmul;
+using freg::csub;
+using freg::Dft;
+using freg::pad;
 
 // register staging per thread: at most ~16 complex values per stage
 template <int P>
@@ -231,10 +128,6 @@ __device__ __forceinline__ void stage_gen(const double2* in, double2* out, int D
     __syncthreads();
 }
 
-// runs the plan on `ncol` columns in a (scratch b for generic stages);
-// returns the buffer holding the result.  The stage order is fixed by the
-// planner (generic, 8s, 4, 2, 3s, 5s, 7s, 11s, 13s), so every radix has its
-// own straight-line code region and its staging array stays in registers.
 template <int P>
 __device__ __forceinline__ void run_radix(double2* cur, int& s, const FftPlan& pl, int ncol,
                                           const double2* __restrict__ tw, int sgn) {
@@ -244,11 +137,14 @@ __device__ __forceinline__ void run_radix(double2* cur, int& s, const FftPlan& p
     }
 }
 
-__device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, const FftPlan& pl,
-                                             const double2* __restrict__ tw, int sgn) {
+// Stockham engine: the planner orders stages generic, 8s, 4, 2, 3s, 5s, 7s,
+// 11s, 13s, so every radix has its own straight-line code region.
+__device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int ncol,
+                                                 const FftPlan& pl, const double2* __restrict__ tw,
+                                                 int sgn) {
     double2* cur = a;
     int s = 0;
-    if (pl.nst > 0 && pl.p[0] > 13) {  // generic stage (planner puts it first)
+    if (pl.nst > 0 && pl.p[0] > 13) {
         stage_gen(cur, b, pl.D, ncol, pl.p[0], pl.Ns[0], pl, 0, tw + pl.tw[0], sgn);
         cur = b;
         s = 1;
@@ -264,6 +160,40 @@ __device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, c
     return cur;
 }
 
+// engine table: ENG -> (D1, D2)
+template <int ENG>
+struct Eng {
+    static constexpr int D1 = 1, D2 = 1;
+};
+template <>
+struct Eng<1> {
+    static constexpr int D1 = 24, D2 = 26;
+};
+template <>
+struct Eng<2> {
+    static constexpr int D1 = 30, D2 = 40;
+};
+template <>
+struct Eng<3> {
+    static constexpr int D1 = 22, D2 = 32;
+};
+template <>
+struct Eng<4> {
+    static constexpr int D1 = 11, D2 = 22;
+};
+
+template <int ENG>
+__device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, const FftPlan& pl,
+                                             const double2* __restrict__ tw, int sgn) {
+    if constexpr (ENG == 0) {
+        return fft_stockham(a, b, ncol, pl, tw, sgn);
+    } else {
+        constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2;
+        freg::fft_cols_2l<D1, D2>(a, ncol, sgn, tw, tw + D1 * D2);
+        return a;
+    }
+}
+
 extern __shared__ __align__(16) unsigned char fse_smem[];
 
 // the plan's twiddle table lives after the column buffer(s) in shared memory
@@ -276,9 +206,10 @@ __device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPl
 }
 
 // ------------------------------------------------------------------ test kernel
+template <int ENG>
 __global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
-                                                  double2* data, int ncol_total, int ncol,
-                                                  int sgn) {
+                                                     double2* data, int ncol_total, int ncol,
+                                                     int sgn) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* b = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
@@ -287,15 +218,17 @@ __global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* 
     for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
         a[pad(e)] = data[static_cast<int64_t>(c0) * pl.D + e];  // contiguous columns
     __syncthreads();
-    double2* r = fft_cols(a, b, nc, pl, tw, sgn);
+    double2* r = fft_cols<ENG>(a, b, nc, pl, tw, sgn);
     for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
         data[static_cast<int64_t>(c0) * pl.D + e] = r[pad(e)];
 }
 
 // ------------------------------------------------------------------ z forward
 // column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
-__global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
-                                                 int ncomp, int ncol, const double* __restrict__ R,
+template <int ENG>
+__global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
+                                                 int Mt, int ncomp, int ncol,
+                                                 const double* __restrict__ R,
                                                  double2* __restrict__ B) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -305,8 +238,7 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
     const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
     const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
     const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
-    const FDiv fMt = make_fdiv(Mt), fJp = make_fdiv(Jp), fDh = make_fdiv(Dh);
-    // per-column row pointers (<= 64 columns per CTA)
+    const FDiv fDh = make_fdiv(Dh);
     __shared__ int64_t row0[64];  // first R/W row of the pair, in doubles
     __shared__ int64_t brow[64];  // first B row of the pair, in rows of Dh
     __shared__ int has1[64];
@@ -320,7 +252,6 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
         has1[threadIdx.x] = (2 * jp + 1 < Mt);
     }
     __syncthreads();
-    // load: lanes walk n (contiguous in R); zero padding n >= Mt
     for (int c = 0; c < nc; ++c) {
         const double* row = R + row0[c];
         const bool h1 = has1[c];
@@ -334,7 +265,7 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
         }
     }
     __syncthreads();
-    double2* r = fft_cols(a, sb, nc, pl, tw, -1);
+    double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, -1);
     // split: X0[k] = (Z[k] + conj Z[-k]) / 2, X1[k] = (Z[k] - conj Z[-k]) / (2i)
     for (int e = threadIdx.x; e < nc * Dh; e += blockDim.x) {
         const int c = static_cast<int>(fdiv(e, fDh)), k = e - c * Dh;
@@ -346,16 +277,15 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
         dst[0] = x0;
         if (has1[c]) dst[Dh] = x1;
     }
-    (void)fMt;
-    (void)fJp;
 }
 
 // ------------------------------------------------------------------ y passes
 // forward: columns (comp, i, kz-tile of ncol); input B[comp][i][j][kz], j < Mt
 // inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
-template <bool INV>
-__global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
-                                                  int ncomp, int ncol, double2* __restrict__ B,
+template <int ENG, bool INV>
+__global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
+                                                  int Mt, int ncomp, int ncol,
+                                                  double2* __restrict__ B,
                                                   double2* __restrict__ Cb) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -381,7 +311,7 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
             a[pad(c * D + Mt + jj)] = make_double2(0.0, 0.0);
         }
     __syncthreads();
-    double2* r = fft_cols(a, sb, nc, pl, tw, INV ? +1 : -1);
+    double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, INV ? +1 : -1);
     const int nout = INV ? Mt : D;
     double2* dst = INV ? Bp : Cp;
     for (int e = threadIdx.x; e < nc * nout; e += blockDim.x) {
@@ -391,10 +321,6 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
 }
 
 // ------------------------------------------------------------------ x pass + scale
-struct C2 {
-    double re, im;
-};
-
 template <int KIND>
 __device__ __forceinline__ void apply(const double k[3], double k2, double gval, double rem,
                                       double inv4xi2, const double2* g, double2* out) {
@@ -448,11 +374,11 @@ __device__ __forceinline__ double kax(int q, int D, double dk) {
 }
 
 // columns (ky, kz-tile); smem holds a*nc columns: column (comp*nc + c)
-template <int KIND>
+template <int ENG, int KIND>
 __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
-                                                GridParams g, int ncol,
-                                                const double* __restrict__ G,
-                                                double2* __restrict__ Cb) {
+                                                   GridParams g, int ncol,
+                                                   const double* __restrict__ G,
+                                                   double2* __restrict__ Cb) {
     constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -475,18 +401,17 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     }
     for (int comp = 0; comp < A; ++comp) {
         const double2* src = Cb + comp * compC + rowoff;
-        double2* dst = a + 0;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;  // lanes walk kz
-            dst[pad((comp * nc + c) * D + i)] = src[static_cast<int64_t>(i) * slab + c];
+            a[pad((comp * nc + c) * D + i)] = src[static_cast<int64_t>(i) * slab + c];
         }
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int ii = static_cast<int>(fdiv(e, fnc)), c = e - ii * nc;
-            dst[pad((comp * nc + c) * D + Mt + ii)] = make_double2(0.0, 0.0);
+            a[pad((comp * nc + c) * D + Mt + ii)] = make_double2(0.0, 0.0);
         }
     }
     __syncthreads();
-    double2* r = fft_cols(a, sb, A * nc, pl, tw, -1);
+    double2* r = fft_cols<ENG>(a, sb, A * nc, pl, tw, -1);
     // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
     // Hermitian average (see k_kscale.cu), 1/D^3 folded in
     const int half = D / 2;
@@ -519,7 +444,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     }
     __syncthreads();
     double2* other = (r == a) ? sb : a;
-    double2* r2 = fft_cols(r, other, 3 * nc, pl, tw, +1);
+    double2* r2 = fft_cols<ENG>(r, other, 3 * nc, pl, tw, +1);
     for (int comp = 0; comp < 3; ++comp) {
         double2* dst = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
@@ -531,8 +456,10 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
 
 // ------------------------------------------------------------------ z inverse
 // row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
-__global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g, int Mt,
-                                                 int ncomp, int ncol, const double2* __restrict__ B,
+template <int ENG>
+__global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
+                                                 int Mt, int ncomp, int ncol,
+                                                 const double2* __restrict__ B,
                                                  double* __restrict__ W) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -543,12 +470,12 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
     const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
     const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
     const FDiv fDh = make_fdiv(Dh);
-    __shared__ int64_t row0[64];  // first R/W row of the pair, in doubles
-    __shared__ int64_t brow[64];  // first B row of the pair, in rows of Dh
+    __shared__ int64_t row0[64];
+    __shared__ int64_t brow[64];
     __shared__ int has1[64];
     if (threadIdx.x < nc) {
         const int64_t q = q0 + threadIdx.x;
-        const int64_t ci = q / Jp;  // comp * Mt + i
+        const int64_t ci = q / Jp;
         const int jp = static_cast<int>(q - ci * Jp);
         const int64_t comp = ci / Mt, i = ci - comp * Mt;
         row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
@@ -570,7 +497,7 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
         if (k != 0 && k != D / 2) a[pad(c * D + D - k)] = make_double2(x0.x + x1.y, -x0.y + x1.x);
     }
     __syncthreads();
-    double2* r = fft_cols(a, sb, nc, pl, tw, +1);
+    double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, +1);
     for (int c = 0; c < nc; ++c) {
         double* row = W + row0[c];
         const bool h1 = has1[c];
@@ -587,10 +514,12 @@ bool is_reg_radix(int p) {
     return p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 11 || p == 13;
 }
 
-bool g_consts_ready = false;
+bool g_consts_ready[64] = {};
 
 void upload_consts() {
-    if (g_consts_ready) return;
+    int dev = 0;
+    FSE_CU(cudaGetDevice(&dev));
+    if (dev < 64 && g_consts_ready[dev]) return;
     double cs[4][14] = {}, sn[4][14] = {};
     const int ps[4] = {5, 7, 11, 13};
     for (int k = 0; k < 4; ++k)
@@ -599,10 +528,35 @@ void upload_consts() {
             cs[k][t] = static_cast<double>(cosl(ang));
             sn[k][t] = static_cast<double>(sinl(ang));
         }
-    FSE_CU(cudaMemcpyToSymbol(c_cos, cs, sizeof cs));
-    FSE_CU(cudaMemcpyToSymbol(c_sin, sn, sizeof sn));
-    g_consts_ready = true;
+    FSE_CU(cudaMemcpyToSymbol(freg::c_rcos, cs, sizeof cs));
+    FSE_CU(cudaMemcpyToSymbol(freg::c_rsin, sn, sizeof sn));
+    if (dev < 64) g_consts_ready[dev] = true;
 }
+
+// D -> two-level engine id and factors
+int engine_for(int D, int* D1, int* D2) {
+    struct E {
+        int D, e, d1, d2;
+    };
+    const E table[] = {{624, 1, 24, 26}, {1200, 2, 30, 40}, {704, 3, 22, 32}, {242, 4, 11, 22}};
+    if (!std::getenv("FSE_FFT_STOCKHAM"))
+        for (const E& t : table)
+            if (t.D == D) {
+                *D1 = t.d1;
+                *D2 = t.d2;
+                return t.e;
+            }
+    return 0;
+}
+
+double2 cexp_neg(long double num, long double den) {
+    const long double two_pi = 2.0L * 3.141592653589793238462643383279502884L;
+    const long double ang = -two_pi * num / den;
+    return make_double2(static_cast<double>(cosl(ang)), static_cast<double>(sinl(ang)));
+}
+
+constexpr int kThreads = 256;
+constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
 
 }  // namespace
 
@@ -611,6 +565,18 @@ HostFftPlan make_fft_plan(int D) {
     HostFftPlan h;
     std::memset(&h.dev, 0, sizeof h.dev);
     h.dev.D = D;
+    h.eng = engine_for(D, &h.D1, &h.D2);
+    if (h.eng > 0) {
+        // table: W_D^t (t < D), then the small register-FFT tables
+        for (int t = 0; t < D; ++t) h.tw.push_back(cexp_neg(t, D));
+        for (int i = 0; i < freg::kNumRegSizes; ++i) {
+            const int n = freg::kRegSizes[i];
+            for (int t = 0; t < n; ++t) h.tw.push_back(cexp_neg(t, n));
+        }
+        h.dev.nst = 0;
+        h.dev.dD = make_fdiv(D);
+        return h;
+    }
     std::vector<int> rad;
     int rem = D;
     while (rem % 8 == 0) { rad.push_back(8); rem /= 8; }
@@ -627,22 +593,15 @@ HostFftPlan make_fft_plan(int D) {
         h.dev.p[s] = p;
         h.dev.Ns[s] = Ns;
         h.dev.tw[s] = static_cast<int>(h.tw.size());
-        const long double two_pi = 2.0L * 3.141592653589793238462643383279502884L;
         if (is_reg_radix(p)) {
             for (int k = 0; k < Ns; ++k)
-                for (int r = 1; r < p; ++r) {
-                    const long long num = (static_cast<long long>(r) * k) % (static_cast<long long>(Ns) * p);
-                    const long double ang = -two_pi * num / (static_cast<long double>(Ns) * p);
-                    h.tw.push_back(make_double2(static_cast<double>(cosl(ang)),
-                                                static_cast<double>(sinl(ang))));
-                }
+                for (int r = 1; r < p; ++r)
+                    h.tw.push_back(cexp_neg((static_cast<long long>(r) * k) %
+                                                (static_cast<long long>(Ns) * p),
+                                            static_cast<long double>(Ns) * p));
         } else {
             h.generic = true;
-            for (int t = 0; t < Ns * p; ++t) {
-                const long double ang = -two_pi * t / (static_cast<long double>(Ns) * p);
-                h.tw.push_back(make_double2(static_cast<double>(cosl(ang)),
-                                            static_cast<double>(sinl(ang))));
-            }
+            for (int t = 0; t < Ns * p; ++t) h.tw.push_back(cexp_neg(t, static_cast<long double>(Ns) * p));
         }
         if (h.tw.empty()) h.tw.push_back(make_double2(1.0, 0.0));
         Ns *= p;
@@ -659,21 +618,33 @@ HostFftPlan make_fft_plan(int D) {
     return h;
 }
 
-// largest column count for `cols_per_unit` columns per unit that fits smem and
-// the register-staged stages (items per thread <= maxit)
-int fft_units_per_cta(const HostFftPlan& h, int cols_per_unit, int threads, size_t smem_cap) {
+namespace {
+
+size_t col_elems(const HostFftPlan& h, int cols) {
+    return static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
+}
+
+size_t smem_bytes(const HostFftPlan& h, int cols) {
+    return (col_elems(h, cols) * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
+}
+
+// largest number of units (each `cols_per_unit` columns) that fits the
+// shared-memory cap and the engine's per-thread work limits
+int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
     const int D = h.dev.D;
     int best = 0;
     for (int u = 1; u <= 64; ++u) {
         const int cols = u * cols_per_unit;
-        const size_t elems = static_cast<size_t>(cols) * D + (static_cast<size_t>(cols) * D) / 8 + 8;
-        const size_t bytes = (elems * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
-        if (bytes > smem_cap) break;
+        if (smem_bytes(h, cols) > cap) break;
         bool ok = true;
-        for (int p : h.radices)
-            if (is_reg_radix(p) && static_cast<long long>(cols) * (D / p) >
-                                       static_cast<long long>(threads) * maxit_host(p))
-                ok = false;
+        if (h.eng > 0) {
+            ok = cols * h.D1 <= kThreads && cols * h.D2 <= kThreads;
+        } else {
+            for (int p : h.radices)
+                if (is_reg_radix(p) &&
+                    static_cast<long long>(cols) * (D / p) > static_cast<long long>(kThreads) * maxit_host(p))
+                    ok = false;
+        }
         if (!ok) break;
         best = u;
     }
@@ -681,37 +652,45 @@ int fft_units_per_cta(const HostFftPlan& h, int cols_per_unit, int threads, size
     return best;
 }
 
-static size_t smem_bytes(const HostFftPlan& h, int cols) {
-    const size_t elems = static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
-    return (elems * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
-}
-
-static void set_buf(FftPlan& p, const HostFftPlan& h, int cols) {
-    p.buf_elems = static_cast<int>(static_cast<size_t>(cols) * h.dev.D +
-                                   (static_cast<size_t>(cols) * h.dev.D) / 8 + 8);
+void set_buf(FftPlan& p, const HostFftPlan& h, int cols) {
+    p.buf_elems = static_cast<int>(col_elems(h, cols));
     p.two_bufs = h.generic ? 1 : 0;
     p.tw_elems = static_cast<int>(h.tw.size());
 }
 
 template <class K>
-static void allow_smem(K kern, size_t bytes) {
+void allow_smem(K kern, size_t bytes) {
     FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes)));
 }
 
-constexpr int kThreads = 256;
-constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
+// dispatch a callable on the engine id as a compile-time constant
+template <class F>
+void with_engine(int eng, F&& f) {
+    switch (eng) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        default: f(std::integral_constant<int, 0>{}); break;
+    }
+}
+
+}  // namespace
 
 void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw, double2* data,
                       int ncols, int inverse) {
     upload_consts();
-    const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
+    const int u = units_per_cta(h, 1, kSmemCap);
     FftPlan p = h.dev;
     set_buf(p, h, u);
     const size_t sm = smem_bytes(h, u);
-    allow_smem(k_fft_test, sm);
-    k_fft_test<<<(ncols + u - 1) / u, kThreads, sm, L.s>>>(p, d_tw, data, ncols, u,
-                                                            inverse ? +1 : -1);
+    with_engine(h.eng, [&](auto E) {
+        constexpr int EV = decltype(E)::value;
+        allow_smem(k_fft_test<EV>, sm);
+        k_fft_test<EV><<<(ncols + u - 1) / u, kThreads, sm, L.s>>>(p, d_tw, data, ncols, u,
+                                                                   inverse ? +1 : -1);
+    });
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
@@ -720,30 +699,33 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
                            int ncomp, const double* R, double2* B, double2* C) {
     upload_consts();
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
-    {
-        const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
-        FftPlan p = h.dev;
-        set_buf(p, h, u);
-        const size_t sm = smem_bytes(h, u);
-        allow_smem(k_zfwd, sm);
-        const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
-        k_zfwd<<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(p, d_tw, Mt,
-                                                                                   ncomp, u, R, B);
-        FSE_LAUNCH_CHECK();
-        ++*L.launches;
-    }
-    {
-        const int u = std::min(fft_units_per_cta(h, 1, kThreads, kSmemCap), Dh);
-        FftPlan p = h.dev;
-        set_buf(p, h, u);
-        const size_t sm = smem_bytes(h, u);
-        allow_smem(k_ypass<false>, sm);
-        const int ntz = (Dh + u - 1) / u;
-        k_ypass<false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz), kThreads,
-                         sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
-        FSE_LAUNCH_CHECK();
-        ++*L.launches;
-    }
+    with_engine(h.eng, [&](auto E) {
+        constexpr int EV = decltype(E)::value;
+        {
+            const int u = units_per_cta(h, 1, kSmemCap);
+            FftPlan p = h.dev;
+            set_buf(p, h, u);
+            const size_t sm = smem_bytes(h, u);
+            allow_smem(k_zfwd<EV>, sm);
+            const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+            k_zfwd<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
+                p, d_tw, Mt, ncomp, u, R, B);
+            FSE_LAUNCH_CHECK();
+            ++*L.launches;
+        }
+        {
+            const int u = std::min(units_per_cta(h, 1, kSmemCap), Dh);
+            FftPlan p = h.dev;
+            set_buf(p, h, u);
+            const size_t sm = smem_bytes(h, u);
+            allow_smem(k_ypass<EV, false>, sm);
+            const int ntz = (Dh + u - 1) / u;
+            k_ypass<EV, false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz),
+                                 kThreads, sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+            FSE_LAUNCH_CHECK();
+            ++*L.launches;
+        }
+    });
 }
 
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
@@ -751,22 +733,25 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     upload_consts();
     const int A = arity_of(kind);
     const int D = h.dev.D, Dh = D / 2 + 1;
-    const int u = std::min(fft_units_per_cta(h, A, kThreads, kSmemCap - 16 * D), Dh);
+    const int u = std::min(units_per_cta(h, A, kSmemCap - 16 * static_cast<size_t>(D)), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
     const size_t sm = smem_bytes(h, A * u) + sizeof(double) * u * D;
     const int ntz = (Dh + u - 1) / u;
     const unsigned blocks = static_cast<unsigned>(D) * ntz;
-    if (kind == FSE_STOKESLET) {
-        allow_smem(k_xscale<FSE_STOKESLET>, sm);
-        k_xscale<FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
-    } else if (kind == FSE_STRESSLET) {
-        allow_smem(k_xscale<FSE_STRESSLET>, sm);
-        k_xscale<FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
-    } else {
-        allow_smem(k_xscale<FSE_ROTLET>, sm);
-        k_xscale<FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
-    }
+    with_engine(h.eng, [&](auto E) {
+        constexpr int EV = decltype(E)::value;
+        if (kind == FSE_STOKESLET) {
+            allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
+            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+        } else if (kind == FSE_STRESSLET) {
+            allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
+            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+        } else {
+            allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
+            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+        }
+    });
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
@@ -775,30 +760,33 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
                            int ncomp, double2* C, double2* B, double* W) {
     upload_consts();
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
-    {
-        const int u = std::min(fft_units_per_cta(h, 1, kThreads, kSmemCap), Dh);
-        FftPlan p = h.dev;
-        set_buf(p, h, u);
-        const size_t sm = smem_bytes(h, u);
-        allow_smem(k_ypass<true>, sm);
-        const int ntz = (Dh + u - 1) / u;
-        k_ypass<true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz), kThreads,
-                        sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
-        FSE_LAUNCH_CHECK();
-        ++*L.launches;
-    }
-    {
-        const int u = fft_units_per_cta(h, 1, kThreads, kSmemCap);
-        FftPlan p = h.dev;
-        set_buf(p, h, u);
-        const size_t sm = smem_bytes(h, u);
-        allow_smem(k_zinv, sm);
-        const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
-        k_zinv<<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(p, d_tw, Mt,
-                                                                                   ncomp, u, B, W);
-        FSE_LAUNCH_CHECK();
-        ++*L.launches;
-    }
+    with_engine(h.eng, [&](auto E) {
+        constexpr int EV = decltype(E)::value;
+        {
+            const int u = std::min(units_per_cta(h, 1, kSmemCap), Dh);
+            FftPlan p = h.dev;
+            set_buf(p, h, u);
+            const size_t sm = smem_bytes(h, u);
+            allow_smem(k_ypass<EV, true>, sm);
+            const int ntz = (Dh + u - 1) / u;
+            k_ypass<EV, true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz),
+                                kThreads, sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+            FSE_LAUNCH_CHECK();
+            ++*L.launches;
+        }
+        {
+            const int u = units_per_cta(h, 1, kSmemCap);
+            FftPlan p = h.dev;
+            set_buf(p, h, u);
+            const size_t sm = smem_bytes(h, u);
+            allow_smem(k_zinv<EV>, sm);
+            const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+            k_zinv<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
+                p, d_tw, Mt, ncomp, u, B, W);
+            FSE_LAUNCH_CHECK();
+            ++*L.launches;
+        }
+    });
 }
 
 }  // namespace fsecu

@@ -48,9 +48,11 @@ struct FftPlan {
 
 struct HostFftPlan {
     FftPlan dev;
-    std::vector<double2> tw;  // concatenated twiddle tables
+    std::vector<double2> tw;  // concatenated twiddle tables (copied to shared memory)
     std::vector<int> radices;
     bool generic = false;     // a non-register (generic DFT) stage is present
+    int eng = 0;              // 0: shared-memory Stockham; >0: two-level register engine
+    int D1 = 0, D2 = 0;       // D = D1 * D2 for eng > 0
 };
 
 HostFftPlan make_fft_plan(int D);

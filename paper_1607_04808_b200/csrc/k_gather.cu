@@ -14,16 +14,18 @@
 // caller's target order.
 //
 // Roofline: FP64 FMA (2 a P^3 flops per target).
+#include <cstdlib>
+
 #include "fse_internal.cuh"
 
 namespace fsecu {
 
 namespace {
 
-constexpr int K = 8;        // targets per warp group
 constexpr int WPB = 4;      // warps per CTA
 constexpr int MAXU = 72;    // union window (P + 7 <= 72 => P <= 64)
 
+template <int K>
 struct GatherWarp {
     double wxu[K][MAXU];
     double wyu[K][MAXU];
@@ -31,17 +33,18 @@ struct GatherWarp {
     int ix[K], iy[K], iz[K];
 };
 
+template <int K>
 __global__ void __launch_bounds__(WPB * 32) k_gather(
     GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ gkey,
     const int32_t* __restrict__ goff, const int32_t* __restrict__ ngroups_dev,
     const double* __restrict__ X,
     const uint32_t* __restrict__ perm, double scale, double* __restrict__ u) {
-    __shared__ GatherWarp smw[WPB];
+    __shared__ GatherWarp<K> smw[WPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t grp = static_cast<int64_t>(blockIdx.x) * WPB + warp;
     if (grp >= *ngroups_dev) return;  // grid is an upper bound (no host sync)
-    GatherWarp& s = smw[warp];
+    GatherWarp<K>& s = smw[warp];
     const int P = g.P;
     const int key = gkey[grp];
     const int first = tstart[key] + K * static_cast<int>(grp - goff[key]);
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(WPB * 32) k_gather(
     }
 }
 
-__global__ void k_group_counts(const int32_t* __restrict__ tstart, int64_t nkeys,
+__global__ void k_group_counts(const int32_t* __restrict__ tstart, int64_t nkeys, int K,
                                int32_t* __restrict__ gcount) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (k < nkeys) gcount[k] = (tstart[k + 1] - tstart[k] + K - 1) / K;
@@ -189,9 +192,18 @@ __global__ void k_fill_groups(const int32_t* __restrict__ goff, int64_t nkeys,
 
 }  // namespace
 
+// targets per warp group (FSE_GATHER_K=4 trades L2 traffic for occupancy)
+int gather_group_size() {
+    static const int k = [] {
+        const char* e = std::getenv("FSE_GATHER_K");
+        return (e && std::atoi(e) == 4) ? 4 : 8;
+    }();
+    return k;
+}
+
 void launch_group_counts(const Launch& L, const int32_t* tstart, int64_t nkeys, int32_t* gcount) {
-    k_group_counts<<<static_cast<unsigned>((nkeys + 256) / 256), 256, 0, L.s>>>(tstart, nkeys,
-                                                                              gcount);
+    k_group_counts<<<static_cast<unsigned>((nkeys + 256) / 256), 256, 0, L.s>>>(
+        tstart, nkeys, gather_group_size(), gcount);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
@@ -210,8 +222,12 @@ void launch_gather(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    double* u) {
     if (max_groups <= 0) return;
     const unsigned blocks = static_cast<unsigned>((max_groups + WPB - 1) / WPB);
-    k_gather<<<blocks, WPB * 32, 0, L.s>>>(g, i0s, w, tstart, gkey, goff, goff + g.nkeys, X, perm,
-                                           scale, u);
+    if (gather_group_size() == 4)
+        k_gather<4><<<blocks, WPB * 32, 0, L.s>>>(g, i0s, w, tstart, gkey, goff, goff + g.nkeys, X,
+                                                  perm, scale, u);
+    else
+        k_gather<8><<<blocks, WPB * 32, 0, L.s>>>(g, i0s, w, tstart, gkey, goff, goff + g.nkeys, X,
+                                                  perm, scale, u);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
