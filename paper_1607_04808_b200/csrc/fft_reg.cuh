@@ -139,8 +139,8 @@ __host__ __device__ constexpr int first_radix(int n) {
          : (n % 5 == 0) ? 5 : (n % 7 == 0) ? 7 : (n % 11 == 0) ? 11 : 13;
 }
 // composite register sizes that own a twiddle table, in table order
-constexpr int kRegSizes[] = {6, 9, 10, 12, 14, 15, 16, 18, 20, 21, 22, 24, 26, 28, 30, 32,
-                             33, 35, 36, 39, 40, 44, 48, 52, 56, 64};
+// (only the composite sizes the engines in k_fft.cu use; twid<> static_asserts)
+constexpr int kRegSizes[] = {15, 22, 24, 26, 30, 32, 40};
 constexpr int kNumRegSizes = sizeof(kRegSizes) / sizeof(int);
 __host__ __device__ constexpr int tw_off_of(int n) {
     int off = 0;

@@ -648,8 +648,17 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
         if (!ok) break;
         best = u;
     }
-    if (best == 0) throw Error(FSE_EINVAL, "FFT: grid size does not fit the shared-memory engine");
     return best;
+}
+
+// two CTAs per SM when possible, otherwise one CTA with up to ~220 KB
+int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit) {
+    for (size_t cap : {kSmemCap, static_cast<size_t>(220 * 1024)}) {
+        int u = units_per_cta(h, cols_per_unit, cap);
+        while (u > 0 && smem_bytes(h, u * cols_per_unit) + extra_per_unit * u > cap) --u;
+        if (u > 0) return u;
+    }
+    throw Error(FSE_EINVAL, "FFT: grid size does not fit the shared-memory engine");
 }
 
 void set_buf(FftPlan& p, const HostFftPlan& h, int cols) {
@@ -681,7 +690,7 @@ void with_engine(int eng, F&& f) {
 void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw, double2* data,
                       int ncols, int inverse) {
     upload_consts();
-    const int u = units_per_cta(h, 1, kSmemCap);
+    const int u = units_fit(h, 1, 0);
     FftPlan p = h.dev;
     set_buf(p, h, u);
     const size_t sm = smem_bytes(h, u);
@@ -702,7 +711,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
-            const int u = units_per_cta(h, 1, kSmemCap);
+            const int u = units_fit(h, 1, 0);
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
@@ -714,7 +723,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             ++*L.launches;
         }
         {
-            const int u = std::min(units_per_cta(h, 1, kSmemCap), Dh);
+            const int u = std::min(units_fit(h, 1, 0), Dh);
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
@@ -733,7 +742,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     upload_consts();
     const int A = arity_of(kind);
     const int D = h.dev.D, Dh = D / 2 + 1;
-    const int u = std::min(units_per_cta(h, A, kSmemCap - 16 * static_cast<size_t>(D)), Dh);
+    const int u = std::min(units_fit(h, A, sizeof(double) * static_cast<size_t>(D)), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
     const size_t sm = smem_bytes(h, A * u) + sizeof(double) * u * D;
@@ -763,7 +772,7 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
-            const int u = std::min(units_per_cta(h, 1, kSmemCap), Dh);
+            const int u = std::min(units_fit(h, 1, 0), Dh);
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
@@ -775,7 +784,7 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             ++*L.launches;
         }
         {
-            const int u = units_per_cta(h, 1, kSmemCap);
+            const int u = units_fit(h, 1, 0);
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
