@@ -196,6 +196,23 @@ __device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, c
 
 extern __shared__ __align__(16) unsigned char fse_smem[];
 
+// Asynchronous global -> shared copies (LDGSTS): every load of a pass is in
+// flight at once instead of one register round trip per element, which is
+// what bounds these strided column gathers.  src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src, int src_bytes = 8) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // the plan's twiddle table lives after the column buffer(s) in shared memory
 __device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPlan& pl,
                                                          const double2* __restrict__ tw_g) {
@@ -256,14 +273,16 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
         const double* row = R + row0[c];
         const bool h1 = has1[c];
         for (int n = threadIdx.x; n < D; n += blockDim.x) {
-            double2 z = make_double2(0.0, 0.0);
+            double* z = reinterpret_cast<double*>(a + pad(c * D + n));
             if (n < Mt) {
-                z.x = row[n];
-                if (h1) z.y = row[Mt + n];
+                cp8(z, row + n);
+                cp8(z + 1, row + (h1 ? Mt + n : n), h1 ? 8 : 0);
+            } else {
+                *reinterpret_cast<double2*>(z) = make_double2(0.0, 0.0);
             }
-            a[pad(c * D + n)] = z;
         }
     }
+    cp_wait_all();
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, -1);
     // split: X0[k] = (Z[k] + conj Z[-k]) / 2, X1[k] = (Z[k] - conj Z[-k]) / (2i)
@@ -303,13 +322,14 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
     const double2* src = INV ? Cp : Bp;
     for (int e = threadIdx.x; e < nc * nin; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;  // lanes walk kz
-        a[pad(c * D + j)] = src[static_cast<int64_t>(j) * Dh + c];
+        cp16(a + pad(c * D + j), src + static_cast<int64_t>(j) * Dh + c);
     }
     if (!INV)
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int jj = static_cast<int>(fdiv(e, fnc)), c = e - jj * nc;
             a[pad(c * D + Mt + jj)] = make_double2(0.0, 0.0);
         }
+    cp_wait_all();
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, INV ? +1 : -1);
     const int nout = INV ? Mt : D;
@@ -397,19 +417,20 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     double* Gs = reinterpret_cast<double*>(const_cast<double2*>(tw) + pl.tw_elems);
     for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
         const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
-        Gs[e] = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0 + c);
+        cp8(Gs + e, G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0 + c);
     }
     for (int comp = 0; comp < A; ++comp) {
         const double2* src = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;  // lanes walk kz
-            a[pad((comp * nc + c) * D + i)] = src[static_cast<int64_t>(i) * slab + c];
+            cp16(a + pad((comp * nc + c) * D + i), src + static_cast<int64_t>(i) * slab + c);
         }
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int ii = static_cast<int>(fdiv(e, fnc)), c = e - ii * nc;
             a[pad((comp * nc + c) * D + Mt + ii)] = make_double2(0.0, 0.0);
         }
     }
+    cp_wait_all();
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, A * nc, pl, tw, -1);
     // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
