@@ -381,11 +381,12 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     Launch L = L1(c);
     int32_t* icnt = buf<int32_t>(c, "rs_icnt", cg.ncell + 1);
     int32_t* ioff = buf<int32_t>(c, "rs_ioff", cg.ncell + 1);
-    launch_item_counts(L, tgt.start, cg.ncell, 128, icnt);
+    const int per = realspace_item_size();
+    launch_item_counts(L, tgt.start, cg.ncell, per, icnt);
     exclusive_scan(c, c->s1, "s1", icnt, ioff, cg.ncell + 1);
-    const int64_t max_items = std::min<int64_t>(cg.ncell, nt) + (nt + 127) / 128;
+    const int64_t max_items = std::min<int64_t>(cg.ncell, nt) + (nt + per - 1) / per;
     int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(max_items));
-    launch_fill_items(L, tgt.start, ioff, cg.ncell, 128, items);
+    launch_fill_items(L, tgt.start, ioff, cg.ncell, per, items);
     FSE_CU(cudaEventRecord(c->ev[EV_RPAIR], c->s1));
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,

@@ -1,14 +1,15 @@
 // k_realspace.cu -- screened real-space pair sum (realspace.cpp:86-149) with
 // the screened kernels of realspace.cpp:13-58.
 //
-// Work item = (target cell, up to 128 of its targets); one thread per target.
+// Work item = (target cell, up to 32 of its targets) = one warp, one lane
+// per target; a CTA runs 4 independent items (no CTA barrier in the loop).
 // The 27 neighbour buckets (lexicographic (di,dj,dk), sources in bucket order
 // -- the reference's summation order) are concatenated virtually and
-// streamed through shared memory in chunks of 128 sources shared by all
-// targets of the item.  Each thread first tests its target against the whole
-// chunk (exact closed-ball test 0 < d2 <= rc2 with d2 = (x*x + y*y) + z*z
-// rounded like the reference) into a 128-bit mask, then evaluates only the
-// accepted pairs in ascending order.  This keeps the pair evaluation off the
+// streamed through the warp's shared memory in chunks of 128 sources.  Each
+// lane first tests its target against the whole chunk (exact closed-ball
+// test 0 < d2 <= rc2 with d2 = (x*x + y*y) + z*z rounded like the
+// reference) into a 128-bit mask, then evaluates only the accepted pairs in
+// ascending order.  This keeps the pair evaluation off the
 // ~85% of candidates that fail the test, instead of predicating the whole
 // warp on every candidate.
 //
@@ -19,11 +20,22 @@
 //   rotlet:    c = inv^2 Chat(x)
 //   stresslet: c1 = -2 inv^2 Dhat(x), c2 = xi^2 Ehat(x),
 //              Dhat = 3 erfc x + s x (3 + 2x^2) e^{-x^2},  Ehat = 2 s x e^{-x^2}
-// Those are tabulated on [0, 6.5) as piecewise degree-12 Chebyshev fits
+// Those are tabulated on [0, 6.5) as 128 piecewise degree-7 Chebyshev fits
 // (monomial in the local t), computed on the host in long double from
-// erfcl/expl, so a pair costs one rsqrt and two 12-term Horner evaluations
-// instead of erfc + exp + divisions.  Absolute fit error < 1e-17 of the
-// functions' O(1) scale.  x >= 6.5 (only for xi rc > 6.5) uses erfc/exp.
+// erfcl/expl, so a pair costs one rsqrt and two 8-term Horner evaluations
+// instead of erfc + exp + divisions.  Max abs fit error 2.6e-16 (Ahat, Chat),
+// 1.0e-15 (Dhat ~ 3), 4e-16 (Ehat).  x >= 6.5 (only for xi rc > 6.5) uses
+// erfc/exp.
+//
+// Candidate test: the closed-ball test is decided in fp32 on coordinates
+// relative to the item's cell centre (FP32 pipe, off the FP64 pipe that
+// the pair math saturates).  With |relative coordinate| <= Rm the fp32
+// squared distance is within B of the exact one (bound derived in
+// fp32_bounds()), so d2f <= rc2 - B is certainly inside, d2f > rc2 + B
+// certainly outside, and only the rare band in between, near-coincident
+// pairs and points farther than Rm from the centre (NaN sentinels: points
+// outside the box clamped into edge cells) take the exact fp64 test of
+// realspace.cpp:140.  The accepted set is therefore exactly the reference's.
 //
 // Roofline: FP64 (pair work).
 #include <cmath>
@@ -37,19 +49,51 @@ namespace {
 constexpr int TPB = 128, CH = 128;
 constexpr double kInvSqrtPi = 0.5641895835477562869;
 
-constexpr int kNI = 32, kDeg = 12;
+constexpr int kNI = 128, kDeg = 7;
 constexpr double kXMax = 6.5;
 constexpr int kNumFn = 4;  // Ahat, Chat, Dhat, Ehat
 __constant__ double c_fn[kNumFn][kDeg + 1][kNI];
 
+// both tabulated functions of a kind, interleaved: one LDS.128 per coefficient
 struct Tab {
-    double c[kDeg + 1][kNI];
+    double2 c[kDeg + 1][kNI];
 };
 
-__device__ __forceinline__ double horner(const Tab& tb, int iv, double t) {
-    double acc = tb.c[kDeg][iv];
+struct FastTest {
+    double rm;        // max |relative coordinate| of the fast path
+    float lo, hi, z0; // certainly inside: z0 < d2f <= lo; certainly outside: d2f > hi
+};
+
+// Error bound of the fp32 squared distance.  Relative coordinates are
+// computed in fp64 (error <= 2^-53 Rm) and rounded to fp32 (<= 2^-24 Rm);
+// the fp32 difference adds <= 2^-24 |dx| <= 2^-23 Rm, so per component
+// |dxf - dx| <= delta = 2^-21 Rm (generous).  Then
+//   |d2f - d2| <= 2 sqrt(3) d delta + 3 delta^2 + 2^-22 d2f,
+// evaluated at d <= 1.01 rc and doubled for the band; near zero
+// d2f <= 3 delta^2 (1 + 2^-22) when d2 = 0, doubled for z0.
+FastTest fp32_bounds(double rc, double side) {
+    FastTest f;
+    f.rm = 1.6 * side;
+    const double delta = std::ldexp(f.rm, -21);
+    const double d = 1.01 * rc;
+    const double B = 2.0 * (2.0 * std::sqrt(3.0) * d * delta + 3.0 * delta * delta +
+                            std::ldexp(d * d, -22));
+    const double rc2 = rc * rc;
+    f.lo = std::nextafter(static_cast<float>(rc2 - B), 0.0f);
+    f.hi = std::nextafter(static_cast<float>(rc2 + B), 1e30f);
+    f.z0 = std::nextafter(static_cast<float>(6.0 * delta * delta), 1e30f);
+    if (!(rc2 - B > 0.0)) f.lo = -1.0f;  // degenerate: everything takes the exact test
+    return f;
+}
+
+__device__ __forceinline__ double2 horner2(const Tab& tb, int iv, double t) {
+    double2 acc = tb.c[kDeg][iv];
 #pragma unroll
-    for (int j = kDeg - 1; j >= 0; --j) acc = fma(acc, t, tb.c[j][iv]);
+    for (int j = kDeg - 1; j >= 0; --j) {
+        const double2 c = tb.c[j][iv];
+        acc.x = fma(acc.x, t, c.x);
+        acc.y = fma(acc.y, t, c.y);
+    }
     return acc;
 }
 
@@ -68,34 +112,36 @@ __device__ __forceinline__ double exact_d2(double rx, double ry, double rz) {
     return __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
 }
 
-// tab0/tab1: the two functions this kernel needs (stokeslet: Ahat, Chat;
-// rotlet: Chat; stresslet: Dhat, Ehat)
-template <int KIND>
+// tab: the two functions this kernel needs (stokeslet: Ahat, Chat;
+// rotlet: Chat, -; stresslet: Dhat, Ehat).  TAIL: x = xi r can reach the
+// end of the table (xi rc >= 6.5), so the exact formulas take over there.
+template <int KIND, bool TAIL>
 __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2, double xi,
-                                     const double* f, const Tab& tab0, const Tab& tab1,
-                                     double acc[3]) {
+                                     const double* f, const Tab& tab, double acc[3]) {
     const double inv = rsqrt(r2);
     const double rn = r2 * inv;
     const double xr = xi * rn;
     double F0, F1 = 0.0;
-    if (xr < kXMax) {
+    if (!TAIL || xr < kXMax) {
         const double uu = xr * (kNI / kXMax);
         const int iv = min(static_cast<int>(uu), kNI - 1);
         const double t = 2.0 * (uu - iv) - 1.0;
-        F0 = horner(tab0, iv, t);
-        if (KIND != FSE_ROTLET) F1 = horner(tab1, iv, t);
+        const double2 F = horner2(tab, iv, t);
+        F0 = F.x;
+        F1 = F.y;
     } else {
         fn_exact(KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2), xr, &F0);
         if (KIND != FSE_ROTLET) fn_exact(KIND == FSE_STOKESLET ? 1 : 3, xr, &F1);
     }
-    const double rh[3] = {inv * rx, inv * ry, inv * rz};
     if (KIND == FSE_STOKESLET) {
-        const double amb = inv * F0;  // a - b
-        const double a = inv * F1;
-        const double s = a * (rh[0] * f[0] + rh[1] * f[1] + rh[2] * f[2]);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) acc[j] += amb * f[j] + s * rh[j];
+        // (a - b) f + a (rhat . f) rhat = inv F0 f + inv^3 F1 (r . f) r
+        const double amb = inv * F0;
+        const double s = inv * inv * inv * F1 * (rx * f[0] + ry * f[1] + rz * f[2]);
+        acc[0] += amb * f[0] + s * rx;
+        acc[1] += amb * f[1] + s * ry;
+        acc[2] += amb * f[2] + s * rz;
     } else if (KIND == FSE_STRESSLET) {
+        const double rh[3] = {inv * rx, inv * ry, inv * rz};
         const double c1 = -2.0 * inv * inv * F0;
         const double c2 = xi * xi * F1;
         double rfr = 0, f_r[3] = {0, 0, 0}, r_f[3] = {0, 0, 0};
@@ -112,14 +158,37 @@ __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2,
 #pragma unroll
         for (int j = 0; j < 3; ++j) acc[j] += s * rh[j] + c2 * (f_r[j] + r_f[j]);
     } else {
-        const double c = inv * inv * F0;
-        acc[0] += c * (f[1] * rh[2] - f[2] * rh[1]);
-        acc[1] += c * (f[2] * rh[0] - f[0] * rh[2]);
-        acc[2] += c * (f[0] * rh[1] - f[1] * rh[0]);
+        // inv^2 Chat (f x rhat) = inv^3 Chat (f x r)
+        const double c = inv * inv * inv * F0;
+        acc[0] += c * (f[1] * rz - f[2] * ry);
+        acc[1] += c * (f[2] * rx - f[0] * rz);
+        acc[2] += c * (f[0] * ry - f[1] * rx);
     }
 }
 
-template <int KIND>
+__device__ __forceinline__ int gcd_int(int a, int b) {
+    while (b) {
+        const int t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// fp32 relative coordinate, NaN beyond Rm (forces the exact test)
+__device__ __forceinline__ float rel32(double v, double rm) {
+    return fabs(v) <= rm ? static_cast<float>(v) : __int_as_float(0x7fffffff);
+}
+
+template <int A>
+struct WarpChunk {
+    float4 sr[CH];
+    double sx[CH], sy[CH], sz[CH];
+    double sf[CH][A];
+    int nb_start[27], nb_pref[28];
+};
+
+template <int KIND, bool TAIL>
 __global__ void __launch_bounds__(TPB) k_realspace(
     int dim, const double* __restrict__ spx, const double* __restrict__ spy,
     const double* __restrict__ spz, const double* __restrict__ sfs,
@@ -127,44 +196,59 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     const double* __restrict__ tpy, const double* __restrict__ tpz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
     const uint32_t* __restrict__ tperm, const int32_t* __restrict__ nitems_dev, double xi,
-    double rc2, double* __restrict__ u) {
+    double rc2, double origin, double side, FastTest ft, double* __restrict__ u) {
     constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
     constexpr int F0 = KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2);
     constexpr int F1 = KIND == FSE_STOKESLET ? 1 : 3;
-    __shared__ double sx[CH], sy[CH], sz[CH];
-    __shared__ double sf[CH][A];
-    __shared__ int nb_start[27], nb_pref[28];
-    __shared__ Tab tab0, tab1;
+    constexpr int W = TPB / 32;
+    // per-warp source chunk (each warp is an independent work item), in
+    // dynamic shared memory: WarpChunk<A>[W]
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    WarpChunk<A>& wc = reinterpret_cast<WarpChunk<A>*>(rs_smem)[threadIdx.x >> 5];
+    auto& sx = wc.sx;
+    auto& sy = wc.sy;
+    auto& sz = wc.sz;
+    auto& sr = wc.sr;  // fp32 coordinates relative to the cell centre
+    auto& sf = wc.sf;
+    auto& nb_start = wc.nb_start;
+    auto& nb_pref = wc.nb_pref;
+    __shared__ Tab tab;
     for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += blockDim.x) {
-        tab0.c[e / kNI][e % kNI] = c_fn[F0][e / kNI][e % kNI];
-        if (KIND != FSE_ROTLET) tab1.c[e / kNI][e % kNI] = c_fn[F1][e / kNI][e % kNI];
+        const int j = e / kNI, iv = e % kNI;
+        tab.c[j][iv] = make_double2(c_fn[F0][j][iv], KIND != FSE_ROTLET ? c_fn[F1][j][iv] : 0.0);
     }
+    __syncthreads();  // the only CTA-wide barrier
 
-    if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // grid is an upper bound
-    const int cell = items[2 * blockIdx.x];
-    const int sub = items[2 * blockIdx.x + 1];
-    const int tid = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int item = blockIdx.x * W + warp;
+    if (item >= *nitems_dev) return;  // grid is an upper bound
+    const int cell = items[2 * item];
+    const int sub = items[2 * item + 1];
     const int ck = cell % dim, cj = (cell / dim) % dim, ci = cell / (dim * dim);
-    if (tid == 0) {
-        int acc = 0, r = 0;
-        for (int di = -1; di <= 1; ++di)
-            for (int dj = -1; dj <= 1; ++dj)
-                for (int dk = -1; dk <= 1; ++dk) {
-                    const int i = ci + di, j = cj + dj, k = ck + dk;
-                    int len = 0, st = 0;
-                    if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
-                        const int b = (i * dim + j) * dim + k;
-                        st = bstart[b];
-                        len = bstart[b + 1] - st;
-                    }
-                    nb_start[r] = st;
-                    nb_pref[r] = acc;
-                    acc += len;
-                    ++r;
-                }
-        nb_pref[27] = acc;
+    // the 27 neighbour buckets in lexicographic (di, dj, dk) order, prefix-summed
+    {
+        int len = 0, st = 0;
+        if (lane < 27) {
+            const int i = ci + lane / 9 - 1, j = cj + (lane / 3) % 3 - 1, k = ck + lane % 3 - 1;
+            if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
+                const int b = (i * dim + j) * dim + k;
+                st = bstart[b];
+                len = bstart[b + 1] - st;
+            }
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane < 27) {
+            nb_start[lane] = st;
+            nb_pref[lane] = incl - len;
+        }
+        if (lane == 26) nb_pref[27] = incl;
     }
-    const int q = tstart[cell] + sub * TPB + tid;
+    const int q = tstart[cell] + sub * 32 + lane;
     const bool valid = q < tstart[cell + 1];
     double x = 0, y = 0, z = 0;
     if (valid) {
@@ -172,22 +256,50 @@ __global__ void __launch_bounds__(TPB) k_realspace(
         y = tpy[q];
         z = tpz[q];
     }
+    const double cxc = origin + (ci + 0.5) * side, cyc = origin + (cj + 0.5) * side,
+                 czc = origin + (ck + 0.5) * side;
+    // idle lanes sit at infinity: every candidate is certainly outside
+    const float xf = valid ? rel32(x - cxc, ft.rm) : 3e38f;
+    const float yf = valid ? rel32(y - cyc, ft.rm) : 3e38f;
+    const float zf = valid ? rel32(z - czc, ft.rm) : 3e38f;
     double acc[3] = {0.0, 0.0, 0.0};
-    __syncthreads();
+    __syncwarp();
     const int total = nb_pref[27];
-    int r = 0;  // neighbour cursor for the cooperative load (monotone in v)
+    // Chunks sample the neighbourhood with a coprime stride S ~ 0.618 total,
+    // so every chunk mixes sources from all 27 buckets and each lane accepts
+    // about the same number of pairs per chunk (bucket-ordered chunks left
+    // ~10 of 32 lanes busy in the pair loop: a chunk from one corner bucket
+    // is accepted only by the targets near that corner).
+    int S = 1;
+    if (total > 2) {
+        S = static_cast<int>(0.6180339887 * total) | 1;
+        while (gcd_int(S, total) != 1) S += 2;
+    }
     for (int base = 0; base < total; base += CH) {
-        const int v = base + tid;
-        if (v < total) {
-            while (nb_pref[r + 1] <= v) ++r;
-            const int sidx = nb_start[r] + (v - nb_pref[r]);
-            sx[tid] = spx[sidx];
-            sy[tid] = spy[sidx];
-            sz[tid] = spz[sidx];
 #pragma unroll
-            for (int c = 0; c < A; ++c) sf[tid][c] = sfs[static_cast<int64_t>(sidx) * A + c];
+        for (int k = 0; k < CH / 32; ++k) {
+            const int slot = k * 32 + lane;
+            const int v = base + slot;
+            if (v < total) {
+                const int pos = static_cast<int>((static_cast<int64_t>(v) * S) % total);
+                int r = 0;  // bucket of pos: largest r with nb_pref[r] <= pos
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1)
+                    if (r + stp < 28 && nb_pref[r + stp] <= pos) r += stp;
+                while (nb_pref[r + 1] <= pos) ++r;  // skip empty buckets
+                const int sidx = nb_start[r] + (pos - nb_pref[r]);
+                const double vx = spx[sidx], vy = spy[sidx], vz = spz[sidx];
+                sx[slot] = vx;
+                sy[slot] = vy;
+                sz[slot] = vz;
+                sr[slot] = make_float4(rel32(vx - cxc, ft.rm), rel32(vy - cyc, ft.rm),
+                                             rel32(vz - czc, ft.rm), 0.0f);
+#pragma unroll
+                for (int c = 0; c < A; ++c)
+                    sf[slot][c] = sfs[static_cast<int64_t>(sidx) * A + c];
+            }
         }
-        __syncthreads();
+        __syncwarp();
         const int cnt = min(CH, total - base);
         uint32_t mask[CH / 32];
 #pragma unroll
@@ -196,24 +308,36 @@ __global__ void __launch_bounds__(TPB) k_realspace(
             const int lim = min(32, cnt - wd * 32);
             for (int b = 0; b < lim; ++b) {
                 const int j = wd * 32 + b;
-                const double d2 = exact_d2(x - sx[j], y - sy[j], z - sz[j]);
-                const bool pass = (d2 != 0.0) && !(d2 > rc2);  // realspace.cpp:140
+                const float4 rr = sr[j];
+                const float dx = xf - rr.x, dy = yf - rr.y, dz = zf - rr.z;
+                const float d2f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                bool pass = d2f <= ft.lo && d2f > ft.z0;
+                if (!pass && !(d2f > ft.hi)) {  // band, near-coincident or NaN: exact test
+                    const double d2 = exact_d2(x - sx[j], y - sy[j], z - sz[j]);
+                    pass = (d2 != 0.0) && !(d2 > rc2);  // realspace.cpp:140
+                }
                 m |= static_cast<uint32_t>(pass) << b;
             }
-            mask[wd] = valid ? m : 0u;
+            mask[wd] = m;
         }
-#pragma unroll
-        for (int wd = 0; wd < CH / 32; ++wd) {
-            uint32_t m = mask[wd];
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                const int j = wd * 32 + b;
-                const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
-                pair<KIND>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab0, tab1, acc);
+        // accepted pairs in ascending source order, one 128-bit mask per lane
+        // (a single loop over all four words balances the lanes better than
+        // a loop per word)
+        uint64_t lo = mask[0] | (static_cast<uint64_t>(mask[1]) << 32);
+        uint64_t hi = mask[2] | (static_cast<uint64_t>(mask[3]) << 32);
+        while (lo | hi) {
+            int j;
+            if (lo) {
+                j = __ffsll(static_cast<long long>(lo)) - 1;
+                lo &= lo - 1;
+            } else {
+                j = 63 + __ffsll(static_cast<long long>(hi));
+                hi &= hi - 1;
             }
+            const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
+            pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
         }
-        __syncthreads();
+        __syncwarp();
     }
     if (valid) {
         const int64_t m = tperm[q];
@@ -304,6 +428,8 @@ void ensure_tables() {
 
 }  // namespace
 
+int realspace_item_size() { return 32; }
+
 void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
                         int32_t* cnt) {
     k_item_counts<<<static_cast<unsigned>((ncell + 256) / 256), 256, 0, L.s>>>(start, ncell, per,
@@ -331,19 +457,23 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
     if (max_items <= 0) return;
     ensure_tables();
     const double rc2 = rc * rc;
-    const unsigned b = static_cast<unsigned>(max_items);
+    const FastTest ft = fp32_bounds(rc, cg.side);
+    const unsigned b = static_cast<unsigned>((max_items + TPB / 32 - 1) / (TPB / 32));
+    const size_t sm3 = sizeof(WarpChunk<3>) * (TPB / 32), sm9 = sizeof(WarpChunk<9>) * (TPB / 32);
+    // the table covers x = xi r < 6.5; past it (xi rc >= 6.5) the exact tail
+    const bool tail = xi * rc >= kXMax * (1.0 - 1e-9);
+    auto go = [&](auto kern, size_t sm) {
+        FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+        kern<<<b, TPB, sm, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy, tpz, tcell_start,
+                                  items, tperm, nitems_dev, xi, rc2, cg.origin, cg.side, ft, uR);
+    };
     if (kind == FSE_STOKESLET)
-        k_realspace<FSE_STOKESLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx,
-                                                       tpy, tpz, tcell_start, items, tperm,
-                                                       nitems_dev, xi, rc2, uR);
+        tail ? go(k_realspace<FSE_STOKESLET, true>, sm3) : go(k_realspace<FSE_STOKESLET, false>, sm3);
     else if (kind == FSE_STRESSLET)
-        k_realspace<FSE_STRESSLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx,
-                                                       tpy, tpz, tcell_start, items, tperm,
-                                                       nitems_dev, xi, rc2, uR);
+        tail ? go(k_realspace<FSE_STRESSLET, true>, sm9) : go(k_realspace<FSE_STRESSLET, false>, sm9);
     else
-        k_realspace<FSE_ROTLET><<<b, TPB, 0, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy,
-                                                    tpz, tcell_start, items, tperm, nitems_dev,
-                                                    xi, rc2, uR);
+        tail ? go(k_realspace<FSE_ROTLET, true>, sm3) : go(k_realspace<FSE_ROTLET, false>, sm3);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
