@@ -1,0 +1,357 @@
+// k_gather_slab.cu -- trapezoidal quadrature back to the targets
+// (ewald.cpp:349-391) on the FP64 tensor cores (DMMA m8n8k4).
+//
+// Work item = one z-half of a coarse tile: the <= 32 targets (more => more
+// items) whose support start lies in an 8 x 8 x 8 block of starts
+// (x0, y0, z0) -- a contiguous key range, since the fine key puts the z-half
+// first.  Every support lies in the union box
+// [x0, x0+P+7) x [y0, y0+P+7) x [z0, z0+P+7).  The CTA streams the box
+// through shared memory one x-plane ("slab") at a time with cp.async double
+// buffering.  A slab is the matrix
+//     A[(c, y)][z] = g_c[x][y0 + y][z0 + z]        (3 (P+7) rows, 4 KS cols)
+// and the z contraction of every row against every target is the GEMM
+//     S = A B,   B[z][t] = wz_t[z0 + z]            (zero outside the support)
+// done with mma.sync.m8n8k4.f64 (B lives in registers for the whole item,
+// each A fragment is one LDS and feeds NT MMAs).  The epilogue folds each
+// slab's S into per-lane accumulators with the separable weights,
+//     acc[(c, y)][t] += wx_t[x] wy_t[y] S[(c, y)][t],
+// and the item ends with a reduction of acc over y through shared memory:
+// u_t[c] = h^3 sum_y acc[(c, y)][t].  No atomics; fixed order.
+//
+// The union box costs (P+7)^2 (4 KS) / P^3 ~ 2.2x the exact FMA count at
+// P = 24 and target padding to 8 another ~1.2x, but at 256 FMAs per MMA
+// instruction the tensor pipe runs near its (FP64) peak instead of the
+// issue- and latency-bound per-lane DFMA loops.  P + 7 <= 32 (P <= 25);
+// larger supports use k_gather.cu.
+//
+// Roofline: FP64 tensor (DMMA) -- same ~37 TFLOP/s peak as DFMA on B200.
+#include <cstdlib>
+
+#include "fse_internal.cuh"
+
+namespace fsecu {
+
+namespace {
+
+constexpr int SW = 4;      // warps per CTA
+constexpr int MAXT = 32;   // targets per item
+constexpr int RS = 36;     // slab row stride (doubles): 32 + 4 keeps A-fragment loads conflict-free
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp16z(void* dst, const void* src, int bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp8z(void* dst, const void* src, int bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// stage x-plane x of the union box: rows r = c NY + yy, columns z < NZ
+// (zero-filled up to 4 KS); pad rows >= 3 NY stay zero from the prologue
+template <int KS>
+__device__ __forceinline__ void stage_slab(const GridParams& g, const double* __restrict__ X,
+                                           int x, int y0, int z0, int NY, int NZ, bool vec16,
+                                           double* dst) {
+    const double* src0 =
+        X + static_cast<int64_t>(x) * g.plane + static_cast<int64_t>(y0) * g.rowp + z0;
+    if (vec16) {
+        constexpr int NCH = 2 * KS;  // 16-byte chunks per row
+        const int total = 3 * NY * NCH;
+        for (int idx = threadIdx.x; idx < total; idx += SW * 32) {
+            const int r = idx / NCH, k = idx - r * NCH;
+            const int c = (r >= NY) + (r >= 2 * NY);
+            const int yy = r - c * NY;
+            const double* src = src0 + c * g.comp + static_cast<int64_t>(yy) * g.rowp;
+            const int zz = 2 * k;
+            const int bytes = zz + 1 < NZ ? 16 : (zz < NZ ? 8 : 0);
+            cp16z(dst + r * RS + zz, bytes ? src + zz : src0, bytes);
+        }
+    } else {
+        constexpr int NCH = 4 * KS;
+        const int total = 3 * NY * NCH;
+        for (int idx = threadIdx.x; idx < total; idx += SW * 32) {
+            const int r = idx / NCH, k = idx - r * NCH;
+            const int c = (r >= NY) + (r >= 2 * NY);
+            const int yy = r - c * NY;
+            const double* src = src0 + c * g.comp + static_cast<int64_t>(yy) * g.rowp;
+            cp8z(dst + r * RS + k, k < NZ ? src + k : src0, k < NZ ? 8 : 0);
+        }
+    }
+}
+
+// MT: m-tiles (8 rows) per warp; NT: n-tiles (8 targets); KS: k-steps (4 z)
+template <int MT, int NT, int KS>
+__device__ void gather_item(const GridParams& g, const double* __restrict__ X,
+                            const double* __restrict__ w, double* slab, const double* wys,
+                            const double* wxs, const int4* tinfo, int n, int x0, int y0, int z0,
+                            int NX, int NY, int NZ, bool vec16, double* red) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = g.P;
+    const int rows_pad = 8 * MT * SW;
+    const int buf_elems = rows_pad * RS;
+    // B fragments: b[ks][nt] = wz_t[z0 + 4 ks + lane % 4 - iz_t], t = 8 nt + lane / 4
+    double b[KS][NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int t = 8 * nt + (lane >> 2);
+        const int4 ti = tinfo[t];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int z = 4 * ks + (lane & 3);
+            const int pz = z0 + z - ti.w;
+            b[ks][nt] = (t < n && z < NZ && pz >= 0 && pz < P)
+                            ? __ldg(w + static_cast<int64_t>(ti.x) * 3 * P + 2 * P + pz)
+                            : 0.0;
+        }
+    }
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    // this lane's A rows (one per m-tile) and its C rows' y index
+    const int rbase = 8 * MT * warp + (lane >> 2);
+    int yrow[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int r = rbase + 8 * mt;
+        const int c = (r >= NY) + (r >= 2 * NY);
+        yrow[mt] = r < 3 * NY ? r - c * NY : -1;
+    }
+    const int tc = 2 * (lane & 3);  // first C column of this lane within an n-tile
+
+    stage_slab<KS>(g, X, x0, y0, z0, NY, NZ, vec16, slab);
+    cp_commit();
+    for (int xs = 0; xs < NX; ++xs) {
+        if (xs + 1 < NX) {
+            stage_slab<KS>(g, X, x0 + xs + 1, y0, z0, NY, NZ, vec16,
+                           slab + ((xs + 1) & 1) * buf_elems);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const double* A = slab + (xs & 1) * buf_elems + rbase * RS + (lane & 3);
+        double wxv[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const double2 v = *reinterpret_cast<const double2*>(wxs + xs * MAXT + 8 * nt + tc);
+            wxv[nt][0] = v.x;
+            wxv[nt][1] = v.y;
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            double cfr[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) cfr[nt][0] = cfr[nt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const double a = A[8 * mt * RS + 4 * ks];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(cfr[nt][0], cfr[nt][1], a, b[ks][nt]);
+            }
+            if (yrow[mt] >= 0) {
+                const double* wyr = wys + yrow[mt] * MAXT + tc;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const double2 wy = *reinterpret_cast<const double2*>(wyr + 8 * nt);
+                    acc[mt][nt][0] = fma(wxv[nt][0] * wy.x, cfr[nt][0], acc[mt][nt][0]);
+                    acc[mt][nt][1] = fma(wxv[nt][1] * wy.y, cfr[nt][1], acc[mt][nt][1]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // red[r][t] = acc for this lane's rows, then u_t[c] = sum_y red[c NY + y][t]
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int r = rbase + 8 * mt;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            red[r * MAXT + 8 * nt + tc] = acc[mt][nt][0];
+            red[r * MAXT + 8 * nt + tc + 1] = acc[mt][nt][1];
+        }
+    }
+}
+
+template <int MT, int NT, int KS>
+__device__ __forceinline__ void run_item(const GridParams& g, const double* __restrict__ X,
+                                         const double* __restrict__ w, double* slab,
+                                         const double* wys, const double* wxs, const int4* tinfo,
+                                         int n, int x0, int y0, int z0, int NX, int NY, int NZ,
+                                         bool vec16, double* red) {
+    gather_item<MT, NT, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+}
+
+template <int MT, int KS>
+__global__ void __launch_bounds__(SW * 32) k_gather_mma(
+    GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
+    const int32_t* __restrict__ nitems_dev, const double* __restrict__ X,
+    const uint32_t* __restrict__ perm, double scale, double* __restrict__ u) {
+    extern __shared__ __align__(16) double gsm[];
+    __shared__ int4 tinfo[MAXT];
+    if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // CTA-uniform
+    constexpr int ROWS = 8 * MT * SW;
+    double* slab = gsm;                    // [2][ROWS][RS]
+    double* wys = slab + 2 * ROWS * RS;    // [ny][MAXT]
+    double* wxs = wys + 32 * MAXT;         // [nx][MAXT]
+    const int e = items[2 * blockIdx.x], bi = items[2 * blockIdx.x + 1];
+    const int c = e >> 1, h = e & 1;
+    const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+    const int P = g.P, Mt = g.Mt;
+    const int x0 = cx * 8, y0 = cy * 8, z0 = cz * 16 + 8 * h;
+    const int first = tstart[8 * c + 4 * h] + MAXT * bi;
+    const int n = min(MAXT, tstart[8 * c + 4 * h + 4] - first);
+    const int NX = min(P + 7, Mt - x0), NY = min(P + 7, Mt - y0), NZ = min(P + 7, Mt - z0);
+    const int tid = threadIdx.x;
+    if (tid < MAXT) {
+        int4 ti = make_int4(0, 0, 0, 0);
+        if (tid < n) {
+            const int q = first + tid;
+            ti = make_int4(q, i0s[3 * q], i0s[3 * q + 1], i0s[3 * q + 2]);
+        }
+        tinfo[tid] = ti;
+    }
+    // pad rows of both slab buffers stay zero
+    for (int idx = tid; idx < 2 * ROWS * RS; idx += SW * 32) {
+        const int r = (idx / RS) % ROWS;
+        if (r >= 3 * NY) slab[idx] = 0.0;
+    }
+    __syncthreads();
+    // separable weights on the union box: wys[y][t], wxs[x][t] (zero outside)
+    for (int idx = tid; idx < 32 * MAXT; idx += SW * 32) {
+        const int yy = idx / MAXT, t = idx % MAXT;
+        const int4 ti = tinfo[t];
+        const int py = y0 + yy - ti.z, px = x0 + yy - ti.y;
+        const double* wq = w + static_cast<int64_t>(ti.x) * 3 * P;
+        wys[idx] = (t < n && yy < NY && py >= 0 && py < P) ? wq[P + py] : 0.0;
+        wxs[idx] = (t < n && yy < NX && px >= 0 && px < P) ? wq[px] : 0.0;
+    }
+    __syncthreads();
+    const bool vec16 = (Mt % 2) == 0;
+    double* red = slab;  // reused after the last slab (ROWS x MAXT <= 2 ROWS RS)
+    const int nt = (n + 7) / 8;
+    if (nt <= 1)
+        run_item<MT, 1, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+    else if (nt == 2)
+        run_item<MT, 2, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+    else if (nt == 3)
+        run_item<MT, 3, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+    else
+        run_item<MT, 4, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+    __syncthreads();
+    if (tid < 3 * MAXT) {
+        const int t = tid % MAXT, cc = tid / MAXT;
+        if (t < n) {
+            double s = 0.0;
+            for (int yy = 0; yy < NY; ++yy) s += red[(cc * NY + yy) * MAXT + t];
+            u[3 * static_cast<int64_t>(perm[first + t]) + cc] = scale * s;
+        }
+    }
+}
+
+// items per (coarse tile, z-half): ceil(n / 32)
+__global__ void k_slab_counts(const int32_t* __restrict__ tstart, int64_t nhalf,
+                              int32_t* __restrict__ cnt) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e < nhalf) {
+        const int n = tstart[4 * e + 4] - tstart[4 * e];
+        cnt[e] = (n + MAXT - 1) / MAXT;
+    }
+    if (e == nhalf) cnt[e] = 0;
+}
+
+__global__ void k_slab_fill(const int32_t* __restrict__ off, int64_t nhalf,
+                            int32_t* __restrict__ items) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= nhalf) return;
+    for (int32_t j = off[e]; j < off[e + 1]; ++j) {
+        items[2 * j] = static_cast<int32_t>(e);
+        items[2 * j + 1] = j - off[e];
+    }
+}
+
+int ks_for(int P) { return (P + 7 + 3) / 4; }
+int mt_for(int P) { return (3 * (P + 7) + 8 * SW - 1) / (8 * SW); }
+
+}  // namespace
+
+size_t slab_smem_bytes(const GridParams& g) {
+    const int rows = 8 * mt_for(g.P) * SW;
+    return sizeof(double) * (2 * static_cast<size_t>(rows) * RS + 2 * 32 * MAXT);
+}
+
+bool gather_slab_enabled(const GridParams& g) {
+    static const bool off = [] {
+        const char* e = std::getenv("FSE_GATHER_SLAB");
+        return e && std::atoi(e) == 0;
+    }();
+    const int ks = ks_for(g.P), mt = mt_for(g.P);
+    return !off && g.P + 7 <= 32 && ks >= 4 && ks <= 8 && mt >= 1 && mt <= 3;
+}
+
+void launch_slab_counts(const Launch& L, const int32_t* tstart, int64_t nhalf, int32_t* cnt) {
+    k_slab_counts<<<static_cast<unsigned>((nhalf + 256) / 256), 256, 0, L.s>>>(tstart, nhalf, cnt);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_slab_fill(const Launch& L, const int32_t* off, int64_t nhalf, int32_t* items) {
+    k_slab_fill<<<static_cast<unsigned>((nhalf + 255) / 256), 256, 0, L.s>>>(off, nhalf, items);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+template <int MT, int KS>
+static void launch_mma(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
+                       const int32_t* tstart, const int32_t* items, int64_t max_items,
+                       const int32_t* nitems_dev, const double* X, const uint32_t* perm,
+                       double scale, double* u) {
+    const size_t sm = slab_smem_bytes(g);
+    FSE_CU(cudaFuncSetAttribute(k_gather_mma<MT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+    k_gather_mma<MT, KS><<<static_cast<unsigned>(max_items), SW * 32, sm, L.s>>>(
+        g, i0s, w, tstart, items, nitems_dev, X, perm, scale, u);
+}
+
+void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
+                        const int32_t* tstart, const int32_t* items, int64_t max_items,
+                        const int32_t* nitems_dev, const double* X, const uint32_t* perm,
+                        double scale, double* u) {
+    if (max_items <= 0) return;
+    const int ks = ks_for(g.P), mt = mt_for(g.P);
+#define FSE_MMA_CASE(M_, K_)                                                                   \
+    if (mt == M_ && ks == K_) {                                                                \
+        launch_mma<M_, K_>(L, g, i0s, w, tstart, items, max_items, nitems_dev, X, perm, scale, \
+                           u);                                                                 \
+    } else
+    FSE_MMA_CASE(3, 8)
+    FSE_MMA_CASE(3, 7)
+    FSE_MMA_CASE(3, 6)
+    FSE_MMA_CASE(2, 7)
+    FSE_MMA_CASE(2, 6)
+    FSE_MMA_CASE(2, 5)
+    FSE_MMA_CASE(2, 4)
+    FSE_MMA_CASE(1, 4)
+    throw Error(FSE_EINVAL, "gather: no tensor-core variant for this support");
+#undef FSE_MMA_CASE
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+}  // namespace fsecu

@@ -51,8 +51,10 @@ __global__ void k_support_keys(GridParams g, const double* __restrict__ pos, int
     if (key) {
         const uint32_t cx = ii[0] >> 3, cy = ii[1] >> 3, cz = ii[2] >> 4;
         const uint32_t coarse = (cx * g.ncy + cy) * g.ncz + cz;
-        const uint32_t fine = (((ii[0] >> 2) & 1) << 2) | (((ii[1] >> 2) & 1) << 1) |
-                              ((ii[2] >> 3) & 1);
+        // z-half first, so each 8 x 8 x 8 half of a coarse tile is a
+        // contiguous key range (the slab gather's work item)
+        const uint32_t fine = (((ii[2] >> 3) & 1) << 2) | (((ii[0] >> 2) & 1) << 1) |
+                              ((ii[1] >> 2) & 1);
         key[q] = coarse * 8u + fine;
     }
 }
