@@ -11,12 +11,12 @@
 //     A[(c, y)][z] = g_c[x][y0 + y][z0 + z]        (3 (P+7) rows, 4 KS cols)
 // and the z contraction of every row against every target is the GEMM
 //     S = A B,   B[z][t] = wz_t[z0 + z]            (zero outside the support)
-// done with mma.sync.m8n8k4.f64 (B lives in registers for the whole item,
-// each A fragment is one LDS and feeds NT MMAs).  The epilogue folds each
-// slab's S into per-lane accumulators with the separable weights,
-//     acc[(c, y)][t] += wx_t[x] wy_t[y] S[(c, y)][t],
-// and the item ends with a reduction of acc over y through shared memory:
-// u_t[c] = h^3 sum_y acc[(c, y)][t].  No atomics; fixed order.
+// done with mma.sync.m8n8k4.f64; each A fragment is one LDS and feeds NT
+// MMAs.  wx_t[x] is folded into the B fragments of slab x, so the MMA
+// accumulators carry
+//     C[(c, y)][t] = sum_x wx_t[x] sum_z g_c[x][y][z] wz_t[z]
+// across all slabs, and the item ends with the y contraction through shared
+// memory: u_t[c] = h^3 sum_y wy_t[y] C[(c, y)][t].  No atomics; fixed order.
 //
 // The union box costs (P+7)^2 (4 KS) / P^3 ~ 2.2x the exact FMA count at
 // P = 24 and target padding to 8 another ~1.2x, but at 256 FMAs per MMA
@@ -35,7 +35,7 @@ namespace {
 
 constexpr int SW = 4;      // warps per CTA
 constexpr int MAXT = 32;   // targets per item
-constexpr int RS = 36;     // slab row stride (doubles): 32 + 4 keeps A-fragment loads conflict-free
+constexpr int RS = 34;     // slab row stride (doubles): 32 + 2 keeps A-fragment loads at 2 wavefronts
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -92,46 +92,24 @@ __device__ __forceinline__ void stage_slab(const GridParams& g, const double* __
     }
 }
 
-// MT: m-tiles (8 rows) per warp; NT: n-tiles (8 targets); KS: k-steps (4 z)
+// MT: m-tiles (8 rows) per warp; NT: n-tiles (8 targets); KS: k-steps (4 z).
+// wx is folded into the B fragments per slab (bs = b0 wx_t[x]), so C
+// accumulates sum_x sum_z directly across slabs: no per-slab epilogue and
+// MT x NT independent accumulation chains per warp.
 template <int MT, int NT, int KS>
-__device__ void gather_item(const GridParams& g, const double* __restrict__ X,
-                            const double* __restrict__ w, double* slab, const double* wys,
-                            const double* wxs, const int4* tinfo, int n, int x0, int y0, int z0,
-                            int NX, int NY, int NZ, bool vec16, double* red) {
+__device__ void gather_item(const GridParams& g, const double* __restrict__ X, double* slab,
+                            const double* b0s, const double* wxs, int x0, int y0, int z0, int NX,
+                            int NY, int NZ, bool vec16, double* red) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P = g.P;
     const int rows_pad = 8 * MT * SW;
     const int buf_elems = rows_pad * RS;
-    // B fragments: b[ks][nt] = wz_t[z0 + 4 ks + lane % 4 - iz_t], t = 8 nt + lane / 4
-    double b[KS][NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        const int t = 8 * nt + (lane >> 2);
-        const int4 ti = tinfo[t];
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-            const int z = 4 * ks + (lane & 3);
-            const int pz = z0 + z - ti.w;
-            b[ks][nt] = (t < n && z < NZ && pz >= 0 && pz < P)
-                            ? __ldg(w + static_cast<int64_t>(ti.x) * 3 * P + 2 * P + pz)
-                            : 0.0;
-        }
-    }
-    double acc[MT][NT][2];
+    double C[MT][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    // this lane's A rows (one per m-tile) and its C rows' y index
+        for (int nt = 0; nt < NT; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
     const int rbase = 8 * MT * warp + (lane >> 2);
-    int yrow[MT];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-        const int r = rbase + 8 * mt;
-        const int c = (r >= NY) + (r >= 2 * NY);
-        yrow[mt] = r < 3 * NY ? r - c * NY : -1;
-    }
-    const int tc = 2 * (lane & 3);  // first C column of this lane within an n-tile
+    const int tb = lane >> 2;  // B column (target within an n-tile) of this lane
 
     stage_slab<KS>(g, X, x0, y0, z0, NY, NZ, vec16, slab);
     cp_commit();
@@ -146,59 +124,38 @@ __device__ void gather_item(const GridParams& g, const double* __restrict__ X,
         }
         __syncthreads();
         const double* A = slab + (xs & 1) * buf_elems + rbase * RS + (lane & 3);
-        double wxv[NT][2];
+        double wxt[NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const double2 v = *reinterpret_cast<const double2*>(wxs + xs * MAXT + 8 * nt + tc);
-            wxv[nt][0] = v.x;
-            wxv[nt][1] = v.y;
-        }
+        for (int nt = 0; nt < NT; ++nt) wxt[nt] = wxs[xs * MAXT + 8 * nt + tb];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            double cfr[NT][2];
+        for (int ks = 0; ks < KS; ++ks) {
+            double bs[NT];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) cfr[nt][0] = cfr[nt][1] = 0.0;
+            for (int nt = 0; nt < NT; ++nt) bs[nt] = b0s[(ks * 4 + nt) * 32 + lane] * wxt[nt];
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
+            for (int mt = 0; mt < MT; ++mt) {
                 const double a = A[8 * mt * RS + 4 * ks];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) dmma(cfr[nt][0], cfr[nt][1], a, b[ks][nt]);
-            }
-            if (yrow[mt] >= 0) {
-                const double* wyr = wys + yrow[mt] * MAXT + tc;
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const double2 wy = *reinterpret_cast<const double2*>(wyr + 8 * nt);
-                    acc[mt][nt][0] = fma(wxv[nt][0] * wy.x, cfr[nt][0], acc[mt][nt][0]);
-                    acc[mt][nt][1] = fma(wxv[nt][1] * wy.y, cfr[nt][1], acc[mt][nt][1]);
-                }
+                for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], a, bs[nt]);
             }
         }
         __syncthreads();
     }
-    // red[r][t] = acc for this lane's rows, then u_t[c] = sum_y red[c NY + y][t]
+    // red[r][t] = C (rows r = (c, y), columns t)
+    const int tc = 2 * (lane & 3);
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
         const int r = rbase + 8 * mt;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            red[r * MAXT + 8 * nt + tc] = acc[mt][nt][0];
-            red[r * MAXT + 8 * nt + tc + 1] = acc[mt][nt][1];
+            red[r * MAXT + 8 * nt + tc] = C[mt][nt][0];
+            red[r * MAXT + 8 * nt + tc + 1] = C[mt][nt][1];
         }
     }
 }
 
-template <int MT, int NT, int KS>
-__device__ __forceinline__ void run_item(const GridParams& g, const double* __restrict__ X,
-                                         const double* __restrict__ w, double* slab,
-                                         const double* wys, const double* wxs, const int4* tinfo,
-                                         int n, int x0, int y0, int z0, int NX, int NY, int NZ,
-                                         bool vec16, double* red) {
-    gather_item<MT, NT, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
-}
-
 template <int MT, int KS>
-__global__ void __launch_bounds__(SW * 32) k_gather_mma(
+__global__ void __launch_bounds__(SW * 32, 3) k_gather_mma(
     GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
     const int32_t* __restrict__ nitems_dev, const double* __restrict__ X,
@@ -208,8 +165,8 @@ __global__ void __launch_bounds__(SW * 32) k_gather_mma(
     if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // CTA-uniform
     constexpr int ROWS = 8 * MT * SW;
     double* slab = gsm;                    // [2][ROWS][RS]
-    double* wys = slab + 2 * ROWS * RS;    // [ny][MAXT]
-    double* wxs = wys + 32 * MAXT;         // [nx][MAXT]
+    double* wxs = slab + 2 * ROWS * RS;    // [nx][MAXT]
+    double* b0s = wxs + 32 * MAXT;         // [KS][4][32] B fragments (wz)
     const int e = items[2 * blockIdx.x], bi = items[2 * blockIdx.x + 1];
     const int c = e >> 1, h = e & 1;
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
@@ -233,33 +190,47 @@ __global__ void __launch_bounds__(SW * 32) k_gather_mma(
         if (r >= 3 * NY) slab[idx] = 0.0;
     }
     __syncthreads();
-    // separable weights on the union box: wys[y][t], wxs[x][t] (zero outside)
+    // x weights on the union box: wxs[x][t] (zero outside the support)
     for (int idx = tid; idx < 32 * MAXT; idx += SW * 32) {
-        const int yy = idx / MAXT, t = idx % MAXT;
+        const int xx = idx / MAXT, t = idx % MAXT;
         const int4 ti = tinfo[t];
-        const int py = y0 + yy - ti.z, px = x0 + yy - ti.y;
-        const double* wq = w + static_cast<int64_t>(ti.x) * 3 * P;
-        wys[idx] = (t < n && yy < NY && py >= 0 && py < P) ? wq[P + py] : 0.0;
-        wxs[idx] = (t < n && yy < NX && px >= 0 && px < P) ? wq[px] : 0.0;
+        const int px = x0 + xx - ti.y;
+        wxs[idx] = (t < n && xx < NX && px >= 0 && px < P)
+                       ? w[static_cast<int64_t>(ti.x) * 3 * P + px]
+                       : 0.0;
+    }
+    // B fragments b0[ks][nt][lane] = wz_t[z0 + 4 ks + lane % 4 - iz_t], t = 8 nt + lane / 4
+    for (int idx = tid; idx < KS * 4 * 32; idx += SW * 32) {
+        const int l = idx & 31, nt = (idx >> 5) & 3, ks = idx >> 7;
+        const int t = 8 * nt + (l >> 2), z = 4 * ks + (l & 3);
+        const int4 ti = tinfo[t];
+        const int pz = z0 + z - ti.w;
+        b0s[idx] = (t < n && z < NZ && pz >= 0 && pz < P)
+                       ? w[static_cast<int64_t>(ti.x) * 3 * P + 2 * P + pz]
+                       : 0.0;
     }
     __syncthreads();
     const bool vec16 = (Mt % 2) == 0;
     double* red = slab;  // reused after the last slab (ROWS x MAXT <= 2 ROWS RS)
     const int nt = (n + 7) / 8;
     if (nt <= 1)
-        run_item<MT, 1, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+        gather_item<MT, 1, KS>(g, X, slab, b0s, wxs, x0, y0, z0, NX, NY, NZ, vec16, red);
     else if (nt == 2)
-        run_item<MT, 2, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+        gather_item<MT, 2, KS>(g, X, slab, b0s, wxs, x0, y0, z0, NX, NY, NZ, vec16, red);
     else if (nt == 3)
-        run_item<MT, 3, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+        gather_item<MT, 3, KS>(g, X, slab, b0s, wxs, x0, y0, z0, NX, NY, NZ, vec16, red);
     else
-        run_item<MT, 4, KS>(g, X, w, slab, wys, wxs, tinfo, n, x0, y0, z0, NX, NY, NZ, vec16, red);
+        gather_item<MT, 4, KS>(g, X, slab, b0s, wxs, x0, y0, z0, NX, NY, NZ, vec16, red);
     __syncthreads();
+    // u_t[c] = h^3 sum_y wy_t[y] red[(c, y)][t]
     if (tid < 3 * MAXT) {
         const int t = tid % MAXT, cc = tid / MAXT;
         if (t < n) {
+            const int4 ti = tinfo[t];
+            const double* wy = w + static_cast<int64_t>(ti.x) * 3 * P + P;
+            const int yo = ti.z - y0;  // support rows yy = yo .. yo + P - 1
             double s = 0.0;
-            for (int yy = 0; yy < NY; ++yy) s += red[(cc * NY + yy) * MAXT + t];
+            for (int p = 0; p < P; ++p) s = fma(wy[p], red[(cc * NY + yo + p) * MAXT + t], s);
             u[3 * static_cast<int64_t>(perm[first + t]) + cc] = scale * s;
         }
     }
@@ -293,7 +264,7 @@ int mt_for(int P) { return (3 * (P + 7) + 8 * SW - 1) / (8 * SW); }
 
 size_t slab_smem_bytes(const GridParams& g) {
     const int rows = 8 * mt_for(g.P) * SW;
-    return sizeof(double) * (2 * static_cast<size_t>(rows) * RS + 2 * 32 * MAXT);
+    return sizeof(double) * (2 * static_cast<size_t>(rows) * RS + 32 * MAXT + 8 * 4 * 32);
 }
 
 bool gather_slab_enabled(const GridParams& g) {
