@@ -1,15 +1,17 @@
 // k_spread.cu -- Gaussian spreading (ewald.cpp:136-214), atomics-free.
 //
 // Ownership instead of atomics: one CTA owns an 8 x 8 x 16 tile of grid
-// nodes and is the only writer of it.  Each of its 4 warps owns a 4 (y) x 8 (z)
-// patch of lanes and all 8 x-rows of the tile, so every lane keeps 8 x 3
-// fp64 accumulators in registers.  The CTA streams, in tile-key order, every
+// nodes and is the only writer of it.  Each of its 2 warps owns an 8 (y) x 8
+// (z) patch (lane: two y rows 4 apart, one z) and all 8 x-rows of the tile,
+// so every lane keeps 2 x 8 x 3 fp64 accumulators in registers (48 DFMAs per
+// point for ~20 other instructions).  The CTA streams, in tile-key order, every
 // point whose P^3 support meets the tile (points are pre-sorted by the tile
 // of their support start i0, so those points sit in 4 x 4 contiguous
 // key ranges), stages the slices of their separable weights that fall on the
-// tile in shared memory (wx[8], wy[8], wz[16], f[3] per point), and every lane
-// applies acc[x][c] += wx[x] * (wy * wz * f_c): three DFMAs per grid node per
-// point, no shared-memory read-modify-write, no global atomics.  The per-node
+// tile in shared memory (wx[8], wy[8], wz[16], f[3] per point; cp.async,
+// double-buffered so the next chunk's copies overlap this chunk's FMAs), and every lane
+// applies acc[y][x][c] += wx[x] * (wy * wz * f_c): three DFMAs per grid node
+// per point, no shared-memory read-modify-write, no global atomics.  The per-node
 // summation order is the stable point order, so results are deterministic.
 //
 // Roofline: FP64 FMA (2 a P^3 flops per point, ~100 flop/B); HBM traffic is
@@ -20,23 +22,35 @@ namespace fsecu {
 
 namespace {
 
-constexpr int TX = 8, TY = 8, TZ = 16, CH = 128;
+constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = 2;
 
-struct SpreadSmem {
+struct Stage {
     double wx[CH][TX];
     double wy[CH][TY];
     double wz[CH][TZ];
-    double f[CH][3];
+    double f[CH][4];
     int iy[CH], iz[CH];
-    int warp_cnt[4];
 };
 
-__global__ void __launch_bounds__(128) k_spread(GridParams g, const int32_t* __restrict__ i0s,
-                                                const double* __restrict__ w,
-                                                const double* __restrict__ fs, int a, int c0,
-                                                const int32_t* __restrict__ tstart,
-                                                double* __restrict__ X) {
-    __shared__ SpreadSmem sm;
+__device__ __forceinline__ void cpa8(void* dst, const void* src, int bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+                 : "memory");
+}
+
+// Walk over the CTA's point chunks: the 4 x 4 (x, y) coarse-tile columns
+// whose starts can reach the tile, each a contiguous key range.
+struct Cursor {
+    int kx, ky, base, qend;
+};
+
+__global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32_t* __restrict__ i0s,
+                                                       const double* __restrict__ w,
+                                                       const double* __restrict__ fs, int a, int c0,
+                                                       const int32_t* __restrict__ tstart,
+                                                       double* __restrict__ X) {
+    __shared__ __align__(16) Stage st[2];
+    __shared__ int cnts[3][NWARP];
     const int P = g.P;
     const int tile = blockIdx.x;
     const int tz = tile % g.ncz;
@@ -44,105 +58,154 @@ __global__ void __launch_bounds__(128) k_spread(GridParams g, const int32_t* __r
     const int tx = tile / (g.ncz * g.ncy);
     const int x0n = tx * TX, y0n = ty * TY, z0n = tz * TZ;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wy_off = (warp & 1) * 4, wz_off = (warp >> 1) * 8;
+    // warp w owns z in [z0n + 8w, +8); lane owns rows y0n + ly and y0n + ly + 4
+    const int wz_off = warp * 8;
     const int ly = lane >> 3, lz = lane & 7;
-    const int wy_lo = y0n + wy_off, wz_lo = z0n + wz_off;
+    const int wz_lo = z0n + wz_off;
 
-    double acc[TX][3];
+    double acc[2][TX][3];
 #pragma unroll
-    for (int r = 0; r < TX; ++r) acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int r = 0; r < TX; ++r) acc[h][r][0] = acc[h][r][1] = acc[h][r][2] = 0.0;
 
     // support starts that reach the tile: i0 in [n0 - P + 1, n0 + T - 1]
     const int ix_lo = x0n - P + 1, iy_lo = y0n - P + 1, iz_lo = z0n - P + 1;
     const int kx_lo = ix_lo < 0 ? 0 : (ix_lo >> 3);
     const int ky_lo = iy_lo < 0 ? 0 : (iy_lo >> 3);
     const int kz_lo = iz_lo < 0 ? 0 : (iz_lo >> 4);
+    auto range = [&](Cursor& c) {  // load [base, qend) of column (kx, ky)
+        const int64_t kb = (static_cast<int64_t>(c.kx) * g.ncy + c.ky) * g.ncz;
+        c.base = tstart[(kb + kz_lo) * 8];
+        c.qend = tstart[(kb + tz) * 8 + 8];
+    };
+    auto next_nonempty = [&](Cursor& c) {  // advance columns until a chunk exists
+        while (c.kx <= tx && c.base >= c.qend) {
+            if (++c.ky > ty) {
+                c.ky = ky_lo;
+                ++c.kx;
+            }
+            if (c.kx <= tx) range(c);
+        }
+    };
+    // per-chunk metadata: which of this thread's point is kept (support meets the tile)
+    auto meta = [&](const Cursor& c, int& q, int& ix, int& iy, int& iz) -> bool {
+        q = c.base + tid;
+        if (q >= c.qend) return false;
+        ix = i0s[3 * q];
+        iy = i0s[3 * q + 1];
+        iz = i0s[3 * q + 2];
+        return ix >= ix_lo && ix <= x0n + TX - 1 && iy >= iy_lo && iy <= y0n + TY - 1 &&
+               iz >= iz_lo && iz <= z0n + TZ - 1;
+    };
+    // asynchronous staging of the kept points' weight slices (zero outside the support)
+    auto stage = [&](Stage& S, int slot, int q, int ix, int iy, int iz) {
+        const double* wq = w + static_cast<int64_t>(q) * 3 * P;
+#pragma unroll
+        for (int r = 0; r < TX; ++r) {
+            const int p = x0n + r - ix;
+            const bool in = p >= 0 && p < P;
+            cpa8(&S.wx[slot][r], in ? wq + p : wq, in ? 8 : 0);
+        }
+#pragma unroll
+        for (int r = 0; r < TY; ++r) {
+            const int p = y0n + r - iy;
+            const bool in = p >= 0 && p < P;
+            cpa8(&S.wy[slot][r], in ? wq + P + p : wq, in ? 8 : 0);
+        }
+#pragma unroll
+        for (int r = 0; r < TZ; ++r) {
+            const int p = z0n + r - iz;
+            const bool in = p >= 0 && p < P;
+            cpa8(&S.wz[slot][r], in ? wq + 2 * P + p : wq, in ? 8 : 0);
+        }
+        const double* fq = fs + static_cast<int64_t>(q) * a + c0;
+        cpa8(&S.f[slot][0], fq, 8);
+        cpa8(&S.f[slot][1], fq + 1, 8);
+        cpa8(&S.f[slot][2], fq + 2, 8);
+        S.iy[slot] = iy;
+        S.iz[slot] = iz;
+    };
 
-    for (int kx = kx_lo; kx <= tx; ++kx)
-        for (int ky = ky_lo; ky <= ty; ++ky) {
-            const int64_t kb = (static_cast<int64_t>(kx) * g.ncy + ky) * g.ncz;
-            const int qbeg = tstart[(kb + kz_lo) * 8];
-            const int qend = tstart[(kb + tz) * 8 + 8];
-            for (int base = qbeg; base < qend; base += CH) {
-                const int q = base + tid;
-                int ix = 0, iy = 0, iz = 0;
-                bool keep = false;
-                if (q < qend) {
-                    ix = i0s[3 * q];
-                    iy = i0s[3 * q + 1];
-                    iz = i0s[3 * q + 2];
-                    keep = ix >= ix_lo && ix <= x0n + TX - 1 && iy >= iy_lo &&
-                           iy <= y0n + TY - 1 && iz >= iz_lo && iz <= z0n + TZ - 1;
-                }
-                // deterministic compaction: warp ballot + per-warp prefix
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (lane == 0) sm.warp_cnt[warp] = __popc(bal);
-                __syncthreads();
-                int wbase = 0, total = 0;
+    Cursor cur;
+    cur.kx = kx_lo;
+    cur.ky = ky_lo;
+    range(cur);
+    next_nonempty(cur);
+    int q = 0, ix = 0, iy = 0, iz = 0;
+    bool keep = cur.kx <= tx && meta(cur, q, ix, iy, iz);
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) cnts[0][warp] = __popc(bal);
+    __syncthreads();
+    if (keep) stage(st[0], (warp ? cnts[0][0] : 0) + __popc(bal & ((1u << lane) - 1u)), q, ix, iy, iz);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    int k = 0, b = 0;
+    while (cur.kx <= tx) {
+        // metadata of the next chunk (overlaps the copies in flight)
+        Cursor nxt = cur;
+        nxt.base += CH;
+        next_nonempty(nxt);
+        const bool more = nxt.kx <= tx;
+        const int kn = k == 2 ? 0 : k + 1;
+        keep = more && meta(nxt, q, ix, iy, iz);
+        bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) cnts[kn][warp] = __popc(bal);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();  // chunk k staged; everyone is done with buffer b ^ 1
+        if (keep)
+            stage(st[b ^ 1], (warp ? cnts[kn][0] : 0) + __popc(bal & ((1u << lane) - 1u)), q, ix,
+                  iy, iz);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const Stage& S = st[b];
+        const int total = cnts[k][0] + cnts[k][1];
+        for (int p = 0; p < total; ++p) {
+            const int izp = S.iz[p];
+            // warp-uniform skip when the support misses this warp's z range
+            if (izp > wz_lo + 7 || izp + P <= wz_lo) continue;
+            const double wzv = S.wz[p][wz_off + lz];
+            const double wy0 = S.wy[p][ly] * wzv, wy1 = S.wy[p][ly + 4] * wzv;
+            const double2 f01 = *reinterpret_cast<const double2*>(&S.f[p][0]);
+            const double f2 = S.f[p][2];
+            const double u00 = wy0 * f01.x, u01 = wy0 * f01.y, u02 = wy0 * f2;
+            const double u10 = wy1 * f01.x, u11 = wy1 * f01.y, u12 = wy1 * f2;
+            const double2* wxp = reinterpret_cast<const double2*>(&S.wx[p][0]);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int c = sm.warp_cnt[k];
-                    wbase += (k < warp) ? c : 0;
-                    total += c;
-                }
-                if (keep) {
-                    const int slot = wbase + __popc(bal & ((1u << lane) - 1u));
-                    const double* wq = w + static_cast<int64_t>(q) * 3 * P;
-#pragma unroll
-                    for (int r = 0; r < TX; ++r) {
-                        const int p = x0n + r - ix;
-                        sm.wx[slot][r] = (p >= 0 && p < P) ? wq[p] : 0.0;
-                    }
-#pragma unroll
-                    for (int r = 0; r < TY; ++r) {
-                        const int p = y0n + r - iy;
-                        sm.wy[slot][r] = (p >= 0 && p < P) ? wq[P + p] : 0.0;
-                    }
-#pragma unroll
-                    for (int r = 0; r < TZ; ++r) {
-                        const int p = z0n + r - iz;
-                        sm.wz[slot][r] = (p >= 0 && p < P) ? wq[2 * P + p] : 0.0;
-                    }
-                    const double* fq = fs + static_cast<int64_t>(q) * a + c0;
-                    sm.f[slot][0] = fq[0];
-                    sm.f[slot][1] = fq[1];
-                    sm.f[slot][2] = fq[2];
-                    sm.iy[slot] = iy;
-                    sm.iz[slot] = iz;
-                }
-                __syncthreads();
-                for (int p = 0; p < total; ++p) {
-                    const int iyp = sm.iy[p], izp = sm.iz[p];
-                    // warp-uniform skip when the support misses this warp's patch
-                    if (iyp > wy_lo + 3 || iyp + P <= wy_lo || izp > wz_lo + 7 ||
-                        izp + P <= wz_lo)
-                        continue;
-                    const double wyz = sm.wy[p][wy_off + ly] * sm.wz[p][wz_off + lz];
-                    const double u0 = wyz * sm.f[p][0];
-                    const double u1 = wyz * sm.f[p][1];
-                    const double u2 = wyz * sm.f[p][2];
-#pragma unroll
-                    for (int r = 0; r < TX; ++r) {
-                        const double wxr = sm.wx[p][r];
-                        acc[r][0] = fma(wxr, u0, acc[r][0]);
-                        acc[r][1] = fma(wxr, u1, acc[r][1]);
-                        acc[r][2] = fma(wxr, u2, acc[r][2]);
-                    }
-                }
-                __syncthreads();
+            for (int r2 = 0; r2 < TX / 2; ++r2) {
+                const double2 wxr = wxp[r2];
+                acc[0][2 * r2][0] = fma(wxr.x, u00, acc[0][2 * r2][0]);
+                acc[0][2 * r2][1] = fma(wxr.x, u01, acc[0][2 * r2][1]);
+                acc[0][2 * r2][2] = fma(wxr.x, u02, acc[0][2 * r2][2]);
+                acc[1][2 * r2][0] = fma(wxr.x, u10, acc[1][2 * r2][0]);
+                acc[1][2 * r2][1] = fma(wxr.x, u11, acc[1][2 * r2][1]);
+                acc[1][2 * r2][2] = fma(wxr.x, u12, acc[1][2 * r2][2]);
+                acc[0][2 * r2 + 1][0] = fma(wxr.y, u00, acc[0][2 * r2 + 1][0]);
+                acc[0][2 * r2 + 1][1] = fma(wxr.y, u01, acc[0][2 * r2 + 1][1]);
+                acc[0][2 * r2 + 1][2] = fma(wxr.y, u02, acc[0][2 * r2 + 1][2]);
+                acc[1][2 * r2 + 1][0] = fma(wxr.y, u10, acc[1][2 * r2 + 1][0]);
+                acc[1][2 * r2 + 1][1] = fma(wxr.y, u11, acc[1][2 * r2 + 1][1]);
+                acc[1][2 * r2 + 1][2] = fma(wxr.y, u12, acc[1][2 * r2 + 1][2]);
             }
         }
+        cur = nxt;
+        k = kn;
+        b ^= 1;
+    }
 
-    const int y = wy_lo + ly, z = wz_lo + lz;
-    if (y >= g.Mt || z >= g.Mt) return;
+    const int z = wz_lo + lz;
+    if (z >= g.Mt) return;
     const int64_t rowpitch = g.rowp;
 #pragma unroll
-    for (int r = 0; r < TX; ++r) {
-        const int x = x0n + r;
-        if (x >= g.Mt) break;
-        const int64_t off = x * g.plane + y * rowpitch + z;
+    for (int h = 0; h < 2; ++h) {
+        const int y = y0n + ly + 4 * h;
+        if (y >= g.Mt) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) X[(c0 + c) * g.comp + off] = acc[r][c];
+        for (int r = 0; r < TX; ++r) {
+            const int x = x0n + r;
+            if (x >= g.Mt) break;
+            const int64_t off = x * g.plane + y * rowpitch + z;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) X[(c0 + c) * g.comp + off] = acc[h][r][c];
+        }
     }
 }
 
@@ -163,7 +226,7 @@ void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    double* X) {
     (void)n;
     const unsigned tiles = static_cast<unsigned>(g.ncx) * g.ncy * g.ncz;
-    k_spread<<<tiles, 128, 0, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
+    k_spread<<<tiles, NWARP * 32, 0, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
