@@ -160,22 +160,34 @@ def peaks():
     return p
 
 
-def stage_models(w, cfg, n, nt):
+# FP64 flops of one accepted real-space pair: r^2 (5),
+# rsqrt + x (6), two 8-term Horner tables (28), kernel combine + accumulate
+PAIR_FLOPS = {0: 60.0, 1: 90.0, 2: 50.0}
+
+
+def stage_models(w, cfg, n, nt, rs_pairs=None):
     """Algorithmic work per launch: flops or bytes."""
     a = 9 if w["kind"] == 1 else 3
     P, D = cfg.P, cfg.D
-    H = D * D * (D // 2 + 1)
     Mt = cfg.Mtilde
-    return {
+    Dh = D // 2 + 1
+    R = 8.0 * Mt ** 3            # compact real grid, one component
+    B = 16.0 * Mt * Mt * Dh      # after the z pass
+    Cs = 16.0 * Mt * D * Dh      # after the y pass
+    G = 8.0 * D * D * Dh         # real half-spectrum multiplier
+    models = {
         # FP64 FMA-bound: 2 a P^3 flops per source, 2*3 P^3 per target
         "spread": ("fp64", 2.0 * a * P ** 3 * n),
         "gather": ("fp64", 2.0 * 3 * P ** 3 * nt),
-        # HBM-bound: one read+write per transform of the real grid and half spectrum,
-        # pruned forward (only Mtilde of D x-planes carry data in the 2D pass)
-        "fft_forward": ("hbm", a * (8.0 * Mt * D * (D + 2) * 2 + 16.0 * H * 2)),
-        "fft_inverse": ("hbm", 3 * (8.0 * Mt * D * (D + 2) * 2 + 16.0 * H * 2)),
-        "kscale": ("hbm", H * (16.0 * a + 8 + 48)),
+        # HBM-bound pruned passes, each reading its input and writing its output once:
+        # z (R -> B), y (B -> C); fused x-pass + multiplier (C, G -> C); inverse y, z
+        "fft_forward": ("hbm", a * (R + B) + a * (B + Cs)),
+        "kscale": ("hbm", a * Cs + G + 3 * Cs),
+        "fft_inverse": ("hbm", 3 * (Cs + B) + 3 * (B + R)),
     }
+    if rs_pairs:
+        models["realspace"] = ("fp64", PAIR_FLOPS[w["kind"]] * rs_pairs)
+    return models
 
 
 # ------------------------------------------------------------------ ours
@@ -228,7 +240,17 @@ def run_ours(args, dist: Dist):
     clk = clocks.stop()
     dist.barrier()
     max_ms = dist.max(dev_ms)
-    kms /= args.steps
+    # stage breakdown from extra untimed steps with the real-space stream
+    # serialised (the overlapped events in the timed steps interleave)
+    ctx.set_overlap(False)
+    kms[:] = 0
+    nbrk = 2
+    tm = fse.StageTimings()
+    for _ in range(nbrk):
+        step(tm)
+        kms += np.array(ctx.kernel_ms())
+    ctx.set_overlap(True)
+    kms /= nbrk
 
     # e2e through the host-buffer C-ABI call, pinned inputs
     hp = ctx.host_alloc(system.positions.shape)
@@ -255,7 +277,8 @@ def run_ours(args, dist: Dist):
                 "fft_forward": kms[3], "kscale": kms[4], "fft_inverse": kms[5],
                 "target_prep": kms[6], "gather": kms[7], "realspace_binning": kms[8],
                 "realspace": kms[9], "call": kms[10]}
-    models = stage_models(w, cfg, n, nt)
+    rs_cand, rs_pairs = ctx.realspace_counts()
+    models = stage_models(w, cfg, n, nt, rs_pairs)
     pk = peaks()
     fp64_peak = args.fp64_peak
     if fp64_peak is None:
@@ -305,7 +328,9 @@ def run_ours(args, dist: Dist):
         "roofline": roof,
         "stage_roofline": stage_roof,
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-        "stage_timings_s": {k: v / args.steps for k, v in tm.as_dict().items()},
+        "stage_timings_s": {k: v / nbrk for k, v in tm.as_dict().items()},
+        "realspace_work": {"candidates": int(rs_cand), "pairs": int(rs_pairs),
+                           "pair_flops": PAIR_FLOPS[w["kind"]]},
         "gpu_launches": int(launches),
         "gpu_launches_note": "our kernels (cuFFT library launches not counted)",
         "clocks": clk,

@@ -97,6 +97,13 @@ uint64_t fse_cuda_launch_count(const fse_cuda_ctx* ctx);
 fse_status fse_cuda_kernel_ms(fse_cuda_ctx* ctx, double* out, int n);
 /* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
 fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);
+/* overlap the real-space sum (second stream) with the Fourier part of total sums
+ * (default 1; 0 serialises them so fse_cuda_kernel_ms reports isolated stage times;
+ * env FSE_SERIAL sets the default to 0).  Results are identical either way. */
+fse_status fse_cuda_set_overlap(fse_cuda_ctx* ctx, int on);
+/* work of the last real-space pair kernel: (target, source) candidates tested and
+ * accepted pairs (0 < r^2 <= rc^2) -- the real-space roofline numerator */
+fse_status fse_cuda_realspace_counts(fse_cuda_ctx* ctx, uint64_t* candidates, uint64_t* pairs);
 
 /* ---- config: replaces fse::make_config (ewald.cpp:103-134) -------------- */
 fse_status fse_make_config(double L, double xi, double rc, int M, int P, double sf,

@@ -214,6 +214,8 @@ def _load():
         lib.fse_cuda_trim.argtypes = [vp]
         lib.fse_cuda_kernel_ms.argtypes = [vp, _dp, C.c_int]
         lib.fse_cuda_fp64_peak.argtypes = [vp, _dp]
+        lib.fse_cuda_set_overlap.argtypes = [vp, C.c_int]
+        lib.fse_cuda_realspace_counts.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         lib.fse_generate_system.argtypes = [C.c_int, i64, C.c_double, C.c_uint64, _dp, _dp]
         lib.fse_generate_workload.argtypes = [C.c_int, i64, C.c_uint64, _dp, _dp, _dp]
         _lib = lib
@@ -334,6 +336,16 @@ class Context:
         out = np.zeros(11)
         self._call(_load().fse_cuda_kernel_ms, _p(out), 11)
         return out.tolist()
+
+    def set_overlap(self, on: bool):
+        """Overlap the real-space sum with the Fourier part (default True)."""
+        self._call(_load().fse_cuda_set_overlap, 1 if on else 0)
+
+    def realspace_counts(self):
+        """(candidates, pairs) of the last real-space pair kernel."""
+        a, b = C.c_uint64(), C.c_uint64()
+        self._call(_load().fse_cuda_realspace_counts, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def measure_fp64_peak(self) -> float:
         v = C.c_double()

@@ -131,6 +131,8 @@ struct fse_cuda_ctx {
     DevBuf work;
     int* d_flags = nullptr;  // [0] s0 flags, [1] s1 flags, [2] equality flag
     int* h_flags = nullptr;  // pinned
+    bool overlap = std::getenv("FSE_SERIAL") == nullptr;  // real space on s1 alongside s0
+    unsigned long long* d_counts = nullptr;  // real-space candidates / accepted pairs
 };
 
 namespace {
@@ -388,10 +390,11 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(max_items));
     launch_fill_items(L, tgt.start, ioff, cg.ncell, per, items);
     FSE_CU(cudaEventRecord(c->ev[EV_RPAIR], c->s1));
+    FSE_CU(cudaMemsetAsync(c->d_counts, 0, 2 * sizeof(unsigned long long), c->s1));
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
                          tgt.pz, tgt.start, items, max_items, ioff + cg.ncell, tgt.perm, xi, rc,
-                         d_uR);
+                         c->d_counts, d_uR);
     else if (nt > 0)
         FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
 }
@@ -468,7 +471,7 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         launch_quad_table(L, g, qtab);
         Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, tas ? 1 : 0, qtab);
         FSE_CU(cudaEventRecord(c->ev[EV_PREP], c->s0));
-        static const bool serial = std::getenv("FSE_SERIAL") != nullptr;  // profiling aid
+        const bool serial = !c->overlap;
         if (want_r && !serial) {
             FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_PREP], 0));
             enqueue_real();
@@ -699,6 +702,8 @@ fse_status fse_cuda_create(int device, fse_cuda_ctx** out) {
         for (auto& e : c->ev) FSE_CU(cudaEventCreate(&e));
         for (auto& e : c->mark) FSE_CU(cudaEventCreate(&e));
         FSE_CU(cudaMalloc(&c->d_flags, 8 * sizeof(int)));
+        FSE_CU(cudaMalloc(&c->d_counts, 2 * sizeof(unsigned long long)));
+        FSE_CU(cudaMemset(c->d_counts, 0, 2 * sizeof(unsigned long long)));
         FSE_CU(cudaMallocHost(&c->h_flags, 8 * sizeof(int)));
     } catch (const Error& e) {
         fse_status st = e.code;
@@ -722,6 +727,7 @@ void fse_cuda_destroy(fse_cuda_ctx* c) {
     for (auto& e : c->mark)
         if (e) cudaEventDestroy(e);
     if (c->d_flags) cudaFree(c->d_flags);
+    if (c->d_counts) cudaFree(c->d_counts);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->s0) cudaStreamDestroy(c->s0);
     if (c->s1) cudaStreamDestroy(c->s1);
@@ -786,6 +792,21 @@ fse_status fse_cuda_fp64_peak(fse_cuda_ctx* c, double* tflops) {
         if (!tflops) invalid("null pointer");
         *tflops = measure_dfma_tflops(L0(c), buf<double>(c, "peak_scratch", 1));
     });
+}
+
+fse_status fse_cuda_realspace_counts(fse_cuda_ctx* c, uint64_t* candidates, uint64_t* pairs) {
+    return api(c, [&] {
+        if (!candidates || !pairs) invalid("null pointer");
+        unsigned long long h[2] = {0, 0};
+        FSE_CU(cudaStreamSynchronize(c->s1));
+        FSE_CU(cudaMemcpy(h, c->d_counts, sizeof h, cudaMemcpyDeviceToHost));
+        *candidates = h[0];
+        *pairs = h[1];
+    });
+}
+
+fse_status fse_cuda_set_overlap(fse_cuda_ctx* c, int on) {
+    return api(c, [&] { c->overlap = on != 0; });
 }
 
 fse_status fse_cuda_kernel_ms(fse_cuda_ctx* c, double* out, int n) {

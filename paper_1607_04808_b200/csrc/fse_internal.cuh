@@ -153,7 +153,7 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, double* uR);
+                      double xi, double rc, unsigned long long* counts, double* uR);
 int realspace_item_size();  // targets per work item
 void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
                         int32_t* cnt);

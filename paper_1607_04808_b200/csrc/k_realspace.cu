@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     const double* __restrict__ tpy, const double* __restrict__ tpz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
     const uint32_t* __restrict__ tperm, const int32_t* __restrict__ nitems_dev, double xi,
-    double rc2, double origin, double side, FastTest ft, double* __restrict__ u) {
+    double rc2, double origin, double side, FastTest ft, unsigned long long* __restrict__ counts,
+    double* __restrict__ u) {
     constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
     constexpr int F0 = KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2);
     constexpr int F1 = KIND == FSE_STOKESLET ? 1 : 3;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     double acc[3] = {0.0, 0.0, 0.0};
     __syncwarp();
     const int total = nb_pref[27];
+    unsigned long long ncand = 0, npair = 0;  // work counters (roofline)
     // Chunks sample the neighbourhood with a coprime stride S ~ 0.618 total,
     // so every chunk mixes sources from all 27 buckets and each lane accepts
     // about the same number of pairs per chunk (bucket-ordered chunks left
@@ -325,6 +327,10 @@ __global__ void __launch_bounds__(TPB) k_realspace(
         // a loop per word)
         uint64_t lo = mask[0] | (static_cast<uint64_t>(mask[1]) << 32);
         uint64_t hi = mask[2] | (static_cast<uint64_t>(mask[3]) << 32);
+        if (valid) {
+            ncand += cnt;
+            npair += __popcll(lo) + __popcll(hi);
+        }
         while (lo | hi) {
             int j;
             if (lo) {
@@ -338,6 +344,15 @@ __global__ void __launch_bounds__(TPB) k_realspace(
             pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
         }
         __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+        npair += __shfl_xor_sync(0xffffffffu, npair, o);
+    }
+    if (lane == 0) {
+        atomicAdd(counts, ncand);
+        atomicAdd(counts + 1, npair);
     }
     if (valid) {
         const int64_t m = tperm[q];
@@ -452,7 +467,7 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, double* uR) {
+                      double xi, double rc, unsigned long long* counts, double* uR) {
     (void)ns;
     if (max_items <= 0) return;
     ensure_tables();
@@ -466,7 +481,8 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
         FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
         kern<<<b, TPB, sm, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy, tpz, tcell_start,
-                                  items, tperm, nitems_dev, xi, rc2, cg.origin, cg.side, ft, uR);
+                                  items, tperm, nitems_dev, xi, rc2, cg.origin, cg.side, ft, counts,
+                                  uR);
     };
     if (kind == FSE_STOKESLET)
         tail ? go(k_realspace<FSE_STOKESLET, true>, sm3) : go(k_realspace<FSE_STOKESLET, false>, sm3);
