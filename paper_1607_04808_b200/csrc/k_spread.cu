@@ -1,18 +1,19 @@
 // k_spread.cu -- Gaussian spreading (ewald.cpp:136-214), atomics-free.
 //
 // Ownership instead of atomics: one CTA owns an 8 x 8 x 16 tile of grid
-// nodes and is the only writer of it.  Each of its 2 warps owns an 8 (y) x 8
-// (z) patch (lane: two y rows 4 apart, one z) and all 8 x-rows of the tile,
-// so every lane keeps 2 x 8 x 3 fp64 accumulators in registers (48 DFMAs per
-// point for ~20 other instructions).  The CTA streams, in tile-key order, every
+// nodes and is the only writer of it.  Each of its 2 warps owns the z-half
+// (8 z) of all 8 x 8 (x, y) rows, and accumulates it on the FP64 tensor
+// cores: for every group of 4 points (one k-step of mma.m8n8k4.f64)
+//     G_c[(x, y)][z] += sum_p (wx_p[x] wy_p[y]) (f_{c,p} wz_p[z]),
+// 8 x-m-tiles x 3 component-n-tiles = 24 MMAs per group from 12 fragment
+// products (1 DMUL each).  The CTA streams, in tile-key order, every
 // point whose P^3 support meets the tile (points are pre-sorted by the tile
 // of their support start i0, so those points sit in 4 x 4 contiguous
 // key ranges), stages the slices of their separable weights that fall on the
 // tile in shared memory (wx[8], wy[8], wz[16], f[3] per point; cp.async,
 // double-buffered so the next chunk's copies overlap this chunk's FMAs), and every lane
-// applies acc[y][x][c] += wx[x] * (wy * wz * f_c): three DFMAs per grid node
-// per point, no shared-memory read-modify-write, no global atomics.  The per-node
-// summation order is the stable point order, so results are deterministic.
+// accumulates in registers: no shared-memory read-modify-write, no global
+// atomics; fixed order (deterministic).
 //
 // Roofline: FP64 FMA (2 a P^3 flops per point, ~100 flop/B); HBM traffic is
 // the weights (3P doubles per point) plus one write of the grid.
@@ -31,6 +32,12 @@ struct Stage {
     double f[CH][4];
     int iy[CH], iz[CH];
 };
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ void cpa8(void* dst, const void* src, int bytes) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -58,16 +65,16 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
     const int tx = tile / (g.ncz * g.ncy);
     const int x0n = tx * TX, y0n = ty * TY, z0n = tz * TZ;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // warp w owns z in [z0n + 8w, +8); lane owns rows y0n + ly and y0n + ly + 4
+    // warp w owns z in [z0n + 8w, +8) of all 8 x 8 (x, y) rows of the tile
     const int wz_off = warp * 8;
-    const int ly = lane >> 3, lz = lane & 7;
     const int wz_lo = z0n + wz_off;
 
-    double acc[2][TX][3];
+    // MMA accumulators: C[x][c] holds G_c[x0n + x][y0n + lane/4][wz_lo + 2 (lane%4) + {0,1}]
+    double C[TX][3][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int r = 0; r < TX; ++r)
 #pragma unroll
-        for (int r = 0; r < TX; ++r) acc[h][r][0] = acc[h][r][1] = acc[h][r][2] = 0.0;
+        for (int c = 0; c < 3; ++c) C[r][c][0] = C[r][c][1] = 0.0;
 
     // support starts that reach the tile: i0 in [n0 - P + 1, n0 + T - 1]
     const int ix_lo = x0n - P + 1, iy_lo = y0n - P + 1, iz_lo = z0n - P + 1;
@@ -158,32 +165,35 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const Stage& S = st[b];
         const int total = cnts[k][0] + cnts[k][1];
-        for (int p = 0; p < total; ++p) {
-            const int izp = S.iz[p];
-            // warp-uniform skip when the support misses this warp's z range
-            if (izp > wz_lo + 7 || izp + P <= wz_lo) continue;
-            const double wzv = S.wz[p][wz_off + lz];
-            const double wy0 = S.wy[p][ly] * wzv, wy1 = S.wy[p][ly + 4] * wzv;
-            const double2 f01 = *reinterpret_cast<const double2*>(&S.f[p][0]);
-            const double f2 = S.f[p][2];
-            const double u00 = wy0 * f01.x, u01 = wy0 * f01.y, u02 = wy0 * f2;
-            const double u10 = wy1 * f01.x, u11 = wy1 * f01.y, u12 = wy1 * f2;
-            const double2* wxp = reinterpret_cast<const double2*>(&S.wx[p][0]);
+        // groups of 4 points = one k-step of m8n8k4:
+        //   A[(x, y)][p] = wx_p[x] wy_p[y]   (m-tile = one x, rows y)
+        //   B[p][(c, z)] = f_{c,p} wz_p[z]   (n-tile = one component, 8 z of this warp)
+        for (int p0 = 0; p0 < total; p0 += 4) {
+            // warp-uniform skip when no support of the group meets this warp's z range
+            bool hit = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int izp = S.iz[min(p0 + j, total - 1)];
+                hit |= !(izp > wz_lo + 7 || izp + P <= wz_lo);
+            }
+            if (!hit) continue;
+            const int p = p0 + (lane & 3);
+            const bool pv = p < total;
+            const int pp = pv ? p : p0;
+            const double wyv = pv ? S.wy[pp][lane >> 2] : 0.0;
+            const double wzv = pv ? S.wz[pp][wz_off + (lane >> 2)] : 0.0;
+            const double2 f01 = *reinterpret_cast<const double2*>(&S.f[pp][0]);
+            const double bf[3] = {f01.x * wzv, f01.y * wzv, S.f[pp][2] * wzv};
+            const double2* wxp = reinterpret_cast<const double2*>(&S.wx[pp][0]);
 #pragma unroll
             for (int r2 = 0; r2 < TX / 2; ++r2) {
                 const double2 wxr = wxp[r2];
-                acc[0][2 * r2][0] = fma(wxr.x, u00, acc[0][2 * r2][0]);
-                acc[0][2 * r2][1] = fma(wxr.x, u01, acc[0][2 * r2][1]);
-                acc[0][2 * r2][2] = fma(wxr.x, u02, acc[0][2 * r2][2]);
-                acc[1][2 * r2][0] = fma(wxr.x, u10, acc[1][2 * r2][0]);
-                acc[1][2 * r2][1] = fma(wxr.x, u11, acc[1][2 * r2][1]);
-                acc[1][2 * r2][2] = fma(wxr.x, u12, acc[1][2 * r2][2]);
-                acc[0][2 * r2 + 1][0] = fma(wxr.y, u00, acc[0][2 * r2 + 1][0]);
-                acc[0][2 * r2 + 1][1] = fma(wxr.y, u01, acc[0][2 * r2 + 1][1]);
-                acc[0][2 * r2 + 1][2] = fma(wxr.y, u02, acc[0][2 * r2 + 1][2]);
-                acc[1][2 * r2 + 1][0] = fma(wxr.y, u10, acc[1][2 * r2 + 1][0]);
-                acc[1][2 * r2 + 1][1] = fma(wxr.y, u11, acc[1][2 * r2 + 1][1]);
-                acc[1][2 * r2 + 1][2] = fma(wxr.y, u12, acc[1][2 * r2 + 1][2]);
+                const double a0 = wxr.x * wyv, a1 = wxr.y * wyv;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    dmma(C[2 * r2][c][0], C[2 * r2][c][1], a0, bf[c]);
+                    dmma(C[2 * r2 + 1][c][0], C[2 * r2 + 1][c][1], a1, bf[c]);
+                }
             }
         }
         cur = nxt;
@@ -191,20 +201,24 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         b ^= 1;
     }
 
-    const int z = wz_lo + lz;
-    if (z >= g.Mt) return;
-    const int64_t rowpitch = g.rowp;
+    const int y = y0n + (lane >> 2), z = wz_lo + 2 * (lane & 3);
+    if (y >= g.Mt || z >= g.Mt) return;
+    const bool z1 = z + 1 < g.Mt;
+    const bool vec = z1 && (g.Mt % 2 == 0);  // 16-byte aligned pairs
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int y = y0n + ly + 4 * h;
-        if (y >= g.Mt) continue;
+    for (int r = 0; r < TX; ++r) {
+        const int x = x0n + r;
+        if (x >= g.Mt) break;
+        const int64_t off = x * g.plane + y * g.rowp + z;
 #pragma unroll
-        for (int r = 0; r < TX; ++r) {
-            const int x = x0n + r;
-            if (x >= g.Mt) break;
-            const int64_t off = x * g.plane + y * rowpitch + z;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) X[(c0 + c) * g.comp + off] = acc[h][r][c];
+        for (int c = 0; c < 3; ++c) {
+            double* dst = X + (c0 + c) * g.comp + off;
+            if (vec) {
+                *reinterpret_cast<double2*>(dst) = make_double2(C[r][c][0], C[r][c][1]);
+            } else {
+                dst[0] = C[r][c][0];
+                if (z1) dst[1] = C[r][c][1];
+            }
         }
     }
 }
