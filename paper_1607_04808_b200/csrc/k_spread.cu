@@ -25,12 +25,16 @@ namespace {
 
 constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = 2;
 
+// element-major staging ([element][point], point stride CHP = CH + 4): the
+// per-thread staging writes of a warp are consecutive doubles and the MMA
+// fragment reads (4 points x 8 rows) spread over all banks
+constexpr int CHP = CH + 4;
 struct Stage {
-    double wx[CH][TX];
-    double wy[CH][TY];
-    double wz[CH][TZ];
-    double f[CH][4];
-    int iy[CH], iz[CH];
+    double wx[TX][CHP];
+    double wy[TY][CHP];
+    double wz[TZ][CHP];
+    double f[3][CHP];
+    int iz[CH];
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -112,25 +116,24 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         for (int r = 0; r < TX; ++r) {
             const int p = x0n + r - ix;
             const bool in = p >= 0 && p < P;
-            cpa8(&S.wx[slot][r], in ? wq + p : wq, in ? 8 : 0);
+            cpa8(&S.wx[r][slot], in ? wq + p : wq, in ? 8 : 0);
         }
 #pragma unroll
         for (int r = 0; r < TY; ++r) {
             const int p = y0n + r - iy;
             const bool in = p >= 0 && p < P;
-            cpa8(&S.wy[slot][r], in ? wq + P + p : wq, in ? 8 : 0);
+            cpa8(&S.wy[r][slot], in ? wq + P + p : wq, in ? 8 : 0);
         }
 #pragma unroll
         for (int r = 0; r < TZ; ++r) {
             const int p = z0n + r - iz;
             const bool in = p >= 0 && p < P;
-            cpa8(&S.wz[slot][r], in ? wq + 2 * P + p : wq, in ? 8 : 0);
+            cpa8(&S.wz[r][slot], in ? wq + 2 * P + p : wq, in ? 8 : 0);
         }
         const double* fq = fs + static_cast<int64_t>(q) * a + c0;
-        cpa8(&S.f[slot][0], fq, 8);
-        cpa8(&S.f[slot][1], fq + 1, 8);
-        cpa8(&S.f[slot][2], fq + 2, 8);
-        S.iy[slot] = iy;
+        cpa8(&S.f[0][slot], fq, 8);
+        cpa8(&S.f[1][slot], fq + 1, 8);
+        cpa8(&S.f[2][slot], fq + 2, 8);
         S.iz[slot] = iz;
     };
 
@@ -180,20 +183,14 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
             const int p = p0 + (lane & 3);
             const bool pv = p < total;
             const int pp = pv ? p : p0;
-            const double wyv = pv ? S.wy[pp][lane >> 2] : 0.0;
-            const double wzv = pv ? S.wz[pp][wz_off + (lane >> 2)] : 0.0;
-            const double2 f01 = *reinterpret_cast<const double2*>(&S.f[pp][0]);
-            const double bf[3] = {f01.x * wzv, f01.y * wzv, S.f[pp][2] * wzv};
-            const double2* wxp = reinterpret_cast<const double2*>(&S.wx[pp][0]);
+            const double wyv = pv ? S.wy[lane >> 2][pp] : 0.0;
+            const double wzv = pv ? S.wz[wz_off + (lane >> 2)][pp] : 0.0;
+            const double bf[3] = {S.f[0][pp] * wzv, S.f[1][pp] * wzv, S.f[2][pp] * wzv};
 #pragma unroll
-            for (int r2 = 0; r2 < TX / 2; ++r2) {
-                const double2 wxr = wxp[r2];
-                const double a0 = wxr.x * wyv, a1 = wxr.y * wyv;
+            for (int r = 0; r < TX; ++r) {
+                const double ar = S.wx[r][pp] * wyv;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    dmma(C[2 * r2][c][0], C[2 * r2][c][1], a0, bf[c]);
-                    dmma(C[2 * r2 + 1][c][0], C[2 * r2 + 1][c][1], a1, bf[c]);
-                }
+                for (int c = 0; c < 3; ++c) dmma(C[r][c][0], C[r][c][1], ar, bf[c]);
             }
         }
         cur = nxt;
