@@ -55,6 +55,7 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM wr"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA %"),
     ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "regs"),
@@ -100,5 +101,30 @@ def full(path):
         print(f"| {short(r[ki])} | " + " | ".join(cells) + " |")
 
 
+STAGE_OF = {"k_spread": "spread", "k_gather_mma": "gather", "k_realspace": "realspace",
+            "k_xscale": "kscale"}
+
+
+def traffic(path):
+    """profiles/traffic.json: dram read+write bytes per launch by bench stage name."""
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    res = {}
+    for r in rows[2:]:
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(m)
+            tot += float(r[i].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+                                                   "Gbyte": 1e9}.get(units[i], 1)
+        name = short(r[ki]).split("<")[0]
+        if name in STAGE_OF:
+            res[STAGE_OF[name]] = tot
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2])
