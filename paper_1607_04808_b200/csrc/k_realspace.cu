@@ -20,12 +20,14 @@
 //   rotlet:    c = inv^2 Chat(x)
 //   stresslet: c1 = -2 inv^2 Dhat(x), c2 = xi^2 Ehat(x),
 //              Dhat = 3 erfc x + s x (3 + 2x^2) e^{-x^2},  Ehat = 2 s x e^{-x^2}
-// Those are tabulated on [0, 6.5) as 128 piecewise degree-7 Chebyshev fits
-// (monomial in the local t), computed on the host in long double from
-// erfcl/expl, so a pair costs one rsqrt and two 8-term Horner evaluations
-// instead of erfc + exp + divisions.  Max abs fit error 2.6e-16 (Ahat, Chat),
-// 1.0e-15 (Dhat ~ 3), 4e-16 (Ehat).  x >= 6.5 (only for xi rc > 6.5) uses
-// erfc/exp.
+// With erfc x = e^{-x^2} erfcx(x) they all are e^{-x^2} times polynomials in
+// x and erfcx(x).  erfcx is tabulated on [0, 6.5) as 128 piecewise degree-7
+// Chebyshev fits (monomial in the local t, built in long double from
+// erfcl/expl; max abs error 1.6e-16, rel 3.3e-16) and e^{-x^2} is computed
+// (exp): one 8-byte table load per coefficient per pair -- the pair loop is
+// shared-memory-bandwidth bound, so this halves its dominant traffic relative
+// to tabulating two functions.  x >= 6.5 (only for xi rc > 6.5) uses the
+// erfc/exp formulas directly.
 //
 // Candidate test: the closed-ball test is decided in fp32 on coordinates
 // relative to the item's cell centre (FP32 pipe, off the FP64 pipe that
@@ -51,13 +53,8 @@ constexpr double kInvSqrtPi = 0.5641895835477562869;
 
 constexpr int kNI = 128, kDeg = 7;
 constexpr double kXMax = 6.5;
-constexpr int kNumFn = 4;  // Ahat, Chat, Dhat, Ehat
-__constant__ double c_fn[kNumFn][kDeg + 1][kNI];
+__constant__ double c_erfcx[kDeg + 1][kNI];
 
-// both tabulated functions of a kind, interleaved: one LDS.128 per coefficient
-struct Tab {
-    double2 c[kDeg + 1][kNI];
-};
 
 struct FastTest {
     double rm;        // max |relative coordinate| of the fast path
@@ -86,17 +83,6 @@ FastTest fp32_bounds(double rc, double side) {
     return f;
 }
 
-__device__ __forceinline__ double2 horner2(const Tab& tb, int iv, double t) {
-    double2 acc = tb.c[kDeg][iv];
-#pragma unroll
-    for (int j = kDeg - 1; j >= 0; --j) {
-        const double2 c = tb.c[j][iv];
-        acc.x = fma(acc.x, t, c.x);
-        acc.y = fma(acc.y, t, c.y);
-    }
-    return acc;
-}
-
 // exact functions (fallback beyond the table)
 __device__ __forceinline__ void fn_exact(int which, double x, double* out) {
     const double e = exp(-x * x), ec = erfc(x), s = 2.0 * kInvSqrtPi;
@@ -117,18 +103,31 @@ __device__ __forceinline__ double exact_d2(double rx, double ry, double rz) {
 // end of the table (xi rc >= 6.5), so the exact formulas take over there.
 template <int KIND, bool TAIL>
 __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2, double xi,
-                                     const double* f, const Tab& tab, double acc[3]) {
+                                     const double* f, const double (*tabx)[kNI], double acc[3]) {
     const double inv = rsqrt(r2);
     const double rn = r2 * inv;
     const double xr = xi * rn;
     double F0, F1 = 0.0;
     if (!TAIL || xr < kXMax) {
+        // erfcx(x) from the table (one 8-byte load per coefficient), e^{-x^2}
+        // computed: half the shared-memory traffic of two tabulated functions
         const double uu = xr * (kNI / kXMax);
         const int iv = min(static_cast<int>(uu), kNI - 1);
         const double t = 2.0 * (uu - iv) - 1.0;
-        const double2 F = horner2(tab, iv, t);
-        F0 = F.x;
-        F1 = F.y;
+        double ex = tabx[kDeg][iv];
+#pragma unroll
+        for (int j = kDeg - 1; j >= 0; --j) ex = fma(ex, t, tabx[j][iv]);
+        const double E = exp(-xr * xr);
+        const double sx = 2.0 * kInvSqrtPi * xr;
+        if (KIND == FSE_STOKESLET) {
+            F0 = E * (ex - sx);
+            F1 = E * (ex + sx);
+        } else if (KIND == FSE_ROTLET) {
+            F0 = E * (ex + sx);
+        } else {
+            F0 = E * (3.0 * ex + sx * (3.0 + 2.0 * xr * xr));
+            F1 = 2.0 * sx * E;
+        }
     } else {
         fn_exact(KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2), xr, &F0);
         if (KIND != FSE_ROTLET) fn_exact(KIND == FSE_STOKESLET ? 1 : 3, xr, &F1);
@@ -199,8 +198,6 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     double rc2, double origin, double side, FastTest ft, unsigned long long* __restrict__ counts,
     double* __restrict__ u) {
     constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
-    constexpr int F0 = KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2);
-    constexpr int F1 = KIND == FSE_STOKESLET ? 1 : 3;
     constexpr int W = TPB / 32;
     // per-warp source chunk (each warp is an independent work item), in
     // dynamic shared memory: WarpChunk<A>[W]
@@ -213,10 +210,10 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     auto& sf = wc.sf;
     auto& nb_start = wc.nb_start;
     auto& nb_pref = wc.nb_pref;
-    __shared__ Tab tab;
+    __shared__ double tabx[kDeg + 1][kNI];
     for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += blockDim.x) {
         const int j = e / kNI, iv = e % kNI;
-        tab.c[j][iv] = make_double2(c_fn[F0][j][iv], KIND != FSE_ROTLET ? c_fn[F1][j][iv] : 0.0);
+        tabx[j][iv] = c_erfcx[j][iv];
     }
     __syncthreads();  // the only CTA-wide barrier
 
@@ -341,7 +338,7 @@ __global__ void __launch_bounds__(TPB) k_realspace(
                 hi &= hi - 1;
             }
             const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
-            pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
+            pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tabx, acc);
         }
         __syncwarp();
     }
@@ -379,51 +376,41 @@ __global__ void k_fill_items(const int32_t* __restrict__ off, int64_t ncell,
     }
 }
 
-// long-double screened functions of x (see the header comment)
-long double fn_ld(int which, long double x) {
-    const long double s = 2.0L / sqrtl(3.141592653589793238462643383279502884L);
-    const long double e = expl(-x * x), ec = erfcl(x);
-    switch (which) {
-        case 0: return ec - s * x * e;
-        case 1: return ec + s * x * e;
-        case 2: return 3.0L * ec + s * x * (3.0L + 2.0L * x * x) * e;
-        default: return 2.0L * s * x * e;
-    }
-}
+// erfcx(x) = e^{x^2} erfc(x) in long double
+long double erfcx_ld(long double x) { return expl(x * x) * erfcl(x); }
 
-// Chebyshev fit on each interval, converted to monomials in t in [-1, 1]
-void build_tables(double out[kNumFn][kDeg + 1][kNI]) {
+// Chebyshev fit of erfcx on each interval, converted to monomials in t in [-1, 1]
+void build_table(double out[kDeg + 1][kNI]) {
     const int n = kDeg + 1;
     const long double PI = 3.141592653589793238462643383279502884L;
-    for (int fnid = 0; fnid < kNumFn; ++fnid)
-        for (int iv = 0; iv < kNI; ++iv) {
-            const long double a = kXMax * iv / static_cast<long double>(kNI);
-            const long double b = kXMax * (iv + 1) / static_cast<long double>(kNI);
-            long double fv[n], cheb[n];
-            for (int k = 0; k < n; ++k) {
-                const long double t = cosl(PI * (k + 0.5L) / n);
-                fv[k] = fn_ld(fnid, 0.5L * (a + b) + 0.5L * (b - a) * t);
-            }
-            for (int j = 0; j < n; ++j) {
-                long double sum = 0;
-                for (int k = 0; k < n; ++k) sum += fv[k] * cosl(PI * j * (k + 0.5L) / n);
-                cheb[j] = sum * 2.0L / n;
-            }
-            cheb[0] *= 0.5L;
-            long double mono[n] = {}, Tprev[n] = {}, Tcur[n] = {}, Tnext[n];
-            Tprev[0] = 1;
-            Tcur[1] = 1;
-            for (int j = 0; j < n; ++j) mono[j] += cheb[0] * Tprev[j] + cheb[1] * Tcur[j];
-            for (int d = 2; d < n; ++d) {
-                for (int j = 0; j < n; ++j) Tnext[j] = -Tprev[j] + (j > 0 ? 2 * Tcur[j - 1] : 0);
-                for (int j = 0; j < n; ++j) mono[j] += cheb[d] * Tnext[j];
-                for (int j = 0; j < n; ++j) {
-                    Tprev[j] = Tcur[j];
-                    Tcur[j] = Tnext[j];
-                }
-            }
-            for (int j = 0; j < n; ++j) out[fnid][j][iv] = static_cast<double>(mono[j]);
+    for (int iv = 0; iv < kNI; ++iv) {
+        const long double a = kXMax * iv / static_cast<long double>(kNI);
+        const long double b = kXMax * (iv + 1) / static_cast<long double>(kNI);
+        long double fv[n], cheb[n];
+        for (int k = 0; k < n; ++k) {
+            const long double t = cosl(PI * (k + 0.5L) / n);
+            fv[k] = erfcx_ld(0.5L * (a + b) + 0.5L * (b - a) * t);
         }
+        for (int j = 0; j < n; ++j) {
+            long double sum = 0;
+            for (int k = 0; k < n; ++k) sum += fv[k] * cosl(PI * j * (k + 0.5L) / n);
+            cheb[j] = sum * 2.0L / n;
+        }
+        cheb[0] *= 0.5L;
+        long double mono[n] = {}, Tprev[n] = {}, Tcur[n] = {}, Tnext[n];
+        Tprev[0] = 1;
+        Tcur[1] = 1;
+        for (int j = 0; j < n; ++j) mono[j] += cheb[0] * Tprev[j] + cheb[1] * Tcur[j];
+        for (int d = 2; d < n; ++d) {
+            for (int j = 0; j < n; ++j) Tnext[j] = -Tprev[j] + (j > 0 ? 2 * Tcur[j - 1] : 0);
+            for (int j = 0; j < n; ++j) mono[j] += cheb[d] * Tnext[j];
+            for (int j = 0; j < n; ++j) {
+                Tprev[j] = Tcur[j];
+                Tcur[j] = Tnext[j];
+            }
+        }
+        for (int j = 0; j < n; ++j) out[j][iv] = static_cast<double>(mono[j]);
+    }
 }
 
 void ensure_tables() {
@@ -431,13 +418,13 @@ void ensure_tables() {
     int dev = 0;
     FSE_CU(cudaGetDevice(&dev));
     if (dev < 64 && ready[dev]) return;
-    static double tab[kNumFn][kDeg + 1][kNI];
+    static double tab[kDeg + 1][kNI];
     static bool built = false;
     if (!built) {
-        build_tables(tab);
+        build_table(tab);
         built = true;
     }
-    FSE_CU(cudaMemcpyToSymbol(c_fn, tab, sizeof tab));
+    FSE_CU(cudaMemcpyToSymbol(c_erfcx, tab, sizeof tab));
     if (dev < 64) ready[dev] = true;
 }
 
