@@ -193,7 +193,16 @@ __device__ __forceinline__ void rfft(double2* v, int sgn, const double2* tab) {
     }
 }
 
-// Column FFT of length D1*D2 on `ncol` columns stored at buf[pad(c*D + n)].
+// Shared-memory column layout of the register engines: column stride
+// D + D1 + 1 (odd) and one pad element after every D2 elements, so the
+// pass-2 loads (stride D2 across lanes) and the columns of the load/store
+// phases (stride one column across lanes) fall on distinct bank groups.
+template <int D1, int D2>
+__device__ __forceinline__ int ridx(int c, int n) {
+    return c * (D1 * D2 + D1 + 1) + n + n / D2;
+}
+
+// Column FFT of length D1*D2 on `ncol` columns stored at buf[ridx(c, n)].
 // Requires ncol*D2 <= blockDim.x and ncol*D1 <= blockDim.x (one item per thread).
 // twD: W_D^t, t < D; tab: small-size twiddles (tw_off_of layout).
 template <int D1, int D2>
@@ -209,7 +218,7 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
         c1 = tid / D2;
         n2 = tid - c1 * D2;
 #pragma unroll
-        for (int n1 = 0; n1 < D1; ++n1) v[n1] = buf[pad(c1 * D + n1 * D2 + n2)];
+        for (int n1 = 0; n1 < D1; ++n1) v[n1] = buf[ridx<D1, D2>(c1, n1 * D2 + n2)];
         rfft<D1>(v, sgn, tab);
         int t = 0;  // n2 * k1 mod D
 #pragma unroll
@@ -226,7 +235,7 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
     __syncthreads();
     if (a1) {
 #pragma unroll
-        for (int k1 = 0; k1 < D1; ++k1) buf[pad(c1 * D + k1 * D2 + n2)] = v[k1];
+        for (int k1 = 0; k1 < D1; ++k1) buf[ridx<D1, D2>(c1, k1 * D2 + n2)] = v[k1];
     }
     __syncthreads();
     // pass 2: item (c, k1)
@@ -237,13 +246,13 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
         c2 = tid / D1;
         k1 = tid - c2 * D1;
 #pragma unroll
-        for (int j = 0; j < D2; ++j) u[j] = buf[pad(c2 * D + k1 * D2 + j)];
+        for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c2, k1 * D2 + j)];
         rfft<D2>(u, sgn, tab);
     }
     __syncthreads();
     if (a2) {
 #pragma unroll
-        for (int k2 = 0; k2 < D2; ++k2) buf[pad(c2 * D + k1 + D1 * k2)] = u[k2];
+        for (int k2 = 0; k2 < D2; ++k2) buf[ridx<D1, D2>(c2, k1 + D1 * k2)] = u[k2];
     }
     __syncthreads();
 }

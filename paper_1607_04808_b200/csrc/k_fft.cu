@@ -194,6 +194,17 @@ __device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, c
     }
 }
 
+// column-buffer index: Stockham engine pads one element in 8; the register
+// engines use freg::ridx (odd column stride, one pad per D2 elements)
+template <int ENG>
+__device__ __forceinline__ int cidx(int c, int n, int D) {
+    if constexpr (ENG == 0) {
+        return pad(c * D + n);
+    } else {
+        return freg::ridx<Eng<ENG>::D1, Eng<ENG>::D2>(c, n);
+    }
+}
+
 extern __shared__ __align__(16) unsigned char fse_smem[];
 
 // Asynchronous global -> shared copies (LDGSTS): every load of a pass is in
@@ -233,11 +244,11 @@ __global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* 
     const int c0 = blockIdx.x * ncol;
     const int nc = min(ncol, ncol_total - c0);
     for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
-        a[pad(e)] = data[static_cast<int64_t>(c0) * pl.D + e];  // contiguous columns
+        a[cidx<ENG>(e / pl.D, e % pl.D, pl.D)] = data[static_cast<int64_t>(c0) * pl.D + e];
     __syncthreads();
     double2* r = fft_cols<ENG>(a, b, nc, pl, tw, sgn);
     for (int e = threadIdx.x; e < nc * pl.D; e += blockDim.x)
-        data[static_cast<int64_t>(c0) * pl.D + e] = r[pad(e)];
+        data[static_cast<int64_t>(c0) * pl.D + e] = r[cidx<ENG>(e / pl.D, e % pl.D, pl.D)];
 }
 
 // ------------------------------------------------------------------ z forward
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
         const double* row = R + row0[c];
         const bool h1 = has1[c];
         for (int n = threadIdx.x; n < D; n += blockDim.x) {
-            double* z = reinterpret_cast<double*>(a + pad(c * D + n));
+            double* z = reinterpret_cast<double*>(a + cidx<ENG>(c, n, D));
             if (n < Mt) {
                 cp8(z, row + n);
                 cp8(z + 1, row + (h1 ? Mt + n : n), h1 ? 8 : 0);
@@ -288,8 +299,8 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
     // split: X0[k] = (Z[k] + conj Z[-k]) / 2, X1[k] = (Z[k] - conj Z[-k]) / (2i)
     for (int e = threadIdx.x; e < nc * Dh; e += blockDim.x) {
         const int c = static_cast<int>(fdiv(e, fDh)), k = e - c * Dh;
-        const double2 zk = r[pad(c * D + k)];
-        const double2 zm = r[pad(c * D + (k == 0 ? 0 : D - k))];
+        const double2 zk = r[cidx<ENG>(c, k, D)];
+        const double2 zm = r[cidx<ENG>(c, (k == 0 ? 0 : D - k), D)];
         const double2 x0 = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
         const double2 x1 = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
         double2* dst = B + brow[c] * Dh + k;
@@ -322,12 +333,12 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
     const double2* src = INV ? Cp : Bp;
     for (int e = threadIdx.x; e < nc * nin; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;  // lanes walk kz
-        cp16(a + pad(c * D + j), src + static_cast<int64_t>(j) * Dh + c);
+        cp16(a + cidx<ENG>(c, j, D), src + static_cast<int64_t>(j) * Dh + c);
     }
     if (!INV)
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int jj = static_cast<int>(fdiv(e, fnc)), c = e - jj * nc;
-            a[pad(c * D + Mt + jj)] = make_double2(0.0, 0.0);
+            a[cidx<ENG>(c, Mt + jj, D)] = make_double2(0.0, 0.0);
         }
     cp_wait_all();
     __syncthreads();
@@ -336,7 +347,7 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
     double2* dst = INV ? Bp : Cp;
     for (int e = threadIdx.x; e < nc * nout; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;
-        dst[static_cast<int64_t>(j) * Dh + c] = r[pad(c * D + j)];
+        dst[static_cast<int64_t>(j) * Dh + c] = r[cidx<ENG>(c, j, D)];
     }
 }
 
@@ -423,11 +434,11 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         const double2* src = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;  // lanes walk kz
-            cp16(a + pad((comp * nc + c) * D + i), src + static_cast<int64_t>(i) * slab + c);
+            cp16(a + cidx<ENG>(comp * nc + c, i, D), src + static_cast<int64_t>(i) * slab + c);
         }
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int ii = static_cast<int>(fdiv(e, fnc)), c = e - ii * nc;
-            a[pad((comp * nc + c) * D + Mt + ii)] = make_double2(0.0, 0.0);
+            a[cidx<ENG>(comp * nc + c, Mt + ii, D)] = make_double2(0.0, 0.0);
         }
     }
     cp_wait_all();
@@ -446,7 +457,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         const double gval = Gs[e];
         double2 gh[A];
 #pragma unroll
-        for (int q = 0; q < A; ++q) gh[q] = r[pad((q * nc + c) * D + kx)];
+        for (int q = 0; q < A; ++q) gh[q] = r[cidx<ENG>(q * nc + c, kx, D)];
         double2 out[3];
         apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
         if (kx == half || ky == half || kz == half) {
@@ -461,7 +472,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         }
 #pragma unroll
         for (int p = 0; p < 3; ++p)
-            r[pad((p * nc + c) * D + kx)] = make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
+            r[cidx<ENG>(p * nc + c, kx, D)] = make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
     }
     __syncthreads();
     double2* other = (r == a) ? sb : a;
@@ -470,7 +481,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         double2* dst = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;
-            dst[static_cast<int64_t>(i) * slab + c] = r2[pad((comp * nc + c) * D + i)];
+            dst[static_cast<int64_t>(i) * slab + c] = r2[cidx<ENG>(comp * nc + c, i, D)];
         }
     }
 }
@@ -514,8 +525,8 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
             x1.y = 0.0;
         }
         // Z[k] = X0 + i X1 ; Z[D-k] = conj(X0) + i conj(X1)
-        a[pad(c * D + k)] = make_double2(x0.x - x1.y, x0.y + x1.x);
-        if (k != 0 && k != D / 2) a[pad(c * D + D - k)] = make_double2(x0.x + x1.y, -x0.y + x1.x);
+        a[cidx<ENG>(c, k, D)] = make_double2(x0.x - x1.y, x0.y + x1.x);
+        if (k != 0 && k != D / 2) a[cidx<ENG>(c, D - k, D)] = make_double2(x0.x + x1.y, -x0.y + x1.x);
     }
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, +1);
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
         double* row = W + row0[c];
         const bool h1 = has1[c];
         for (int n = threadIdx.x; n < Mt; n += blockDim.x) {
-            const double2 z = r[pad(c * D + n)];
+            const double2 z = r[cidx<ENG>(c, n, D)];
             row[n] = z.x;
             if (h1) row[Mt + n] = z.y;
         }
@@ -642,6 +653,8 @@ HostFftPlan make_fft_plan(int D) {
 namespace {
 
 size_t col_elems(const HostFftPlan& h, int cols) {
+    if (h.eng > 0)  // freg::ridx layout
+        return static_cast<size_t>(cols) * (h.dev.D + h.D1 + 1) + 8;
     return static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
 }
 
