@@ -95,6 +95,42 @@ uint64_t fse_cuda_launch_count(const fse_cuda_ctx* ctx);
  * [2] spread kernel [3] forward FFTs [4] k-space scale [5] inverse FFTs [6] target prep
  * [7] gather kernel [8] real-space binning [9] real-space pair kernel [10] whole call */
 fse_status fse_cuda_kernel_ms(fse_cuda_ctx* ctx, double* out, int n);
+/* ---- z-slab decomposition over several GPUs (no reference counterpart:
+ * the reference is single-process).  Slab `rank` of `nslabs` owns the x-planes
+ * [x_lo, x_lo + nx) of the M~ grid and the ky rows [ky_lo, ky_lo + nky) of the
+ * k-space pass; every rank holds all points.  Per evaluation:
+ *   fse_cuda_slab_forward  -> spectrum send buffer, nslabs blocks of block_complex
+ *   all-to-all (block s -> rank s; received blocks in source-rank order)
+ *   fse_cuda_slab_scale    (in place on the received buffer)
+ *   all-to-all back        (block r -> rank r)
+ *   fse_cuda_slab_inverse  -> this rank's partial velocities (NT x 3)
+ *   sum of the partials over ranks = total_sum.
+ * The exchanges are the caller's (bench.py / slabs.py use NCCL via torch.distributed).
+ * nslabs = 1 reproduces fse_cuda_total_sum_dev. */
+typedef struct {
+    int x_lo, nx, nxs;      /* this slab's x-planes; nxs planes per slab */
+    int ky_lo, nky, nkys;   /* this rank's ky rows; nkys rows per block */
+    int64_t block_complex;  /* complex values per spectrum block (a * nxs * nkys * (D/2+1)) */
+} fse_slab_info;
+fse_status fse_cuda_slab_info(const fse_config* cfg, int kind, int rank, int nslabs,
+                              fse_slab_info* out);
+/* spread of all sources onto this slab's planes, z and y FFT passes (device pointers;
+ * d_spec: nslabs * block_complex complex doubles) */
+fse_status fse_cuda_slab_forward(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                 const double* d_pos, const double* d_str, int64_t n, int rank,
+                                 int nslabs, double* d_spec);
+/* x-FFT, k-space multiplier, inverse x-FFT for this rank's ky rows, in place on the
+ * received spectrum (blocks in source-rank order) */
+fse_status fse_cuda_slab_scale(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                               const fse_green* green, int rank, int nslabs, double* d_spec);
+/* inverse y/z passes and this slab's share of the quadrature for all targets, plus the
+ * real-space sum and self term of targets [nt*rank/nslabs, nt*(rank+1)/nslabs):
+ * d_u (NT x 3, device) = this rank's partial velocities */
+fse_status fse_cuda_slab_inverse(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                 const double* d_pos, const double* d_str, int64_t n,
+                                 double* d_spec, int rank, int nslabs, const double* d_tgt,
+                                 int64_t nt, int tas, double* d_u);
+
 /* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
 fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);
 /* overlap the real-space sum (second stream) with the Fourier part of total sums

@@ -104,6 +104,21 @@ class StageTimings(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class SlabInfo(C.Structure):
+    """fse_slab_info (include/fse_cuda.h): this rank's part of the z-slab decomposition."""
+    _fields_ = [("x_lo", C.c_int), ("nx", C.c_int), ("nxs", C.c_int), ("ky_lo", C.c_int),
+                ("nky", C.c_int), ("nkys", C.c_int), ("block_complex", C.c_int64)]
+
+
+def slab_info(cfg, kind, rank, nslabs) -> SlabInfo:
+    out = SlabInfo()
+    st = _load().fse_cuda_slab_info(C.byref(cfg), int(kind), int(rank), int(nslabs),
+                                    C.byref(out))
+    if st != 0:
+        _raise(st, "fse_cuda_slab_info: invalid slab request (P <= 25 needed for nslabs > 1)")
+    return out
+
+
 @dataclass
 class SourceSystem:
     """fse::SourceSystem (kernels.hpp:59-66): positions (N,3), strengths (N,a)."""
@@ -215,6 +230,14 @@ def _load():
         lib.fse_cuda_kernel_ms.argtypes = [vp, _dp, C.c_int]
         lib.fse_cuda_fp64_peak.argtypes = [vp, _dp]
         lib.fse_cuda_set_overlap.argtypes = [vp, C.c_int]
+        lib.fse_cuda_slab_info.argtypes = [C.POINTER(EwaldConfig), C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(SlabInfo)]
+        lib.fse_cuda_slab_forward.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
+                                              C.c_int, C.c_int, vp]
+        lib.fse_cuda_slab_scale.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, C.c_int,
+                                            C.c_int, vp]
+        lib.fse_cuda_slab_inverse.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
+                                              vp, C.c_int, C.c_int, vp, i64, C.c_int, vp]
         lib.fse_cuda_realspace_counts.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         lib.fse_generate_system.argtypes = [C.c_int, i64, C.c_double, C.c_uint64, _dp, _dp]
         lib.fse_generate_workload.argtypes = [C.c_int, i64, C.c_uint64, _dp, _dp, _dp]
@@ -395,6 +418,21 @@ class Context:
                    C.c_void_p(d_str), int(n), float(box_side), C.c_void_p(d_tgt), int(nt),
                    int(targets_are_sources), green.handle, C.c_void_p(d_u),
                    C.byref(timings) if timings is not None else None)
+
+    # -- z-slab decomposition (device pointers; see fse_cuda_slab_* and slabs.py)
+    def slab_forward(self, cfg, kind, d_pos, d_str, n, rank, nslabs, d_spec):
+        self._call(_load().fse_cuda_slab_forward, C.byref(cfg), int(kind), C.c_void_p(d_pos),
+                   C.c_void_p(d_str), int(n), int(rank), int(nslabs), C.c_void_p(d_spec))
+
+    def slab_scale(self, cfg, kind, green, rank, nslabs, d_spec):
+        self._call(_load().fse_cuda_slab_scale, C.byref(cfg), int(kind), green.handle,
+                   int(rank), int(nslabs), C.c_void_p(d_spec))
+
+    def slab_inverse(self, cfg, kind, d_pos, d_str, n, d_spec, rank, nslabs, d_tgt, nt, tas,
+                     d_u):
+        self._call(_load().fse_cuda_slab_inverse, C.byref(cfg), int(kind), C.c_void_p(d_pos),
+                   C.c_void_p(d_str), int(n), C.c_void_p(d_spec), int(rank), int(nslabs),
+                   C.c_void_p(d_tgt), int(nt), int(tas), C.c_void_p(d_u))
 
     def fourier_sum(self, system: SourceSystem, cfg: EwaldConfig, kind, targets, green,
                     timings: StageTimings | None = None):

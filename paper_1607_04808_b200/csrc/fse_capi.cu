@@ -76,7 +76,24 @@ GridParams make_grid_params(const fse_config& c) {
     g.ncy = (g.Mt + 7) / 8;
     g.ncz = (g.Mt + 15) / 16;
     g.nkeys = static_cast<int64_t>(g.ncx) * g.ncy * g.ncz * 8;
+    g.x_lo = 0;
+    g.nx = g.Mt;
+    g.nxs = g.Mt;
+    g.ky_lo = 0;
+    g.nky = g.D;
+    g.nkys = g.D;
     return g;
+}
+
+void set_slab(GridParams& g, int r, int G) {
+    if (G <= 1) return;
+    g.nxs = ((g.Mt + G - 1) / G + 7) / 8 * 8;  // x-planes per slab, whole spread tiles
+    g.x_lo = std::min(r * g.nxs, g.Mt);
+    g.nx = std::min(g.nxs, g.Mt - g.x_lo);
+    g.comp = static_cast<int64_t>(g.nx) * g.plane;
+    g.nkys = (g.D + G - 1) / G;
+    g.ky_lo = std::min(r * g.nkys, g.D);
+    g.nky = std::min(g.nkys, g.D - g.ky_lo);
 }
 
 namespace {
@@ -487,11 +504,11 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         for (int c0 = 0; c0 < a; c0 += 3)
             launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
         FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
-        launch_fft_forward_zy(L, fp.host, fp.tw, g.Mt, a, X, Bs, Cs);
+        launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT1], c->s0));
         launch_fft_xscale(L, fp.host, fp.tw, g, kind, green->d_half, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_SCALE], c->s0));
-        launch_fft_inverse_yz(L, fp.host, fp.tw, g.Mt, 3, Cs, Bs, X);
+        launch_fft_inverse_yz(L, fp.host, fp.tw, g, a, Cs, Bs, X);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT2], c->s0));
 
         Sorted tg = tas ? src : prep_points(c, g, "ft_", d_tgt, nullptr, 0, nt, 1, qtab);
@@ -997,6 +1014,138 @@ fse_status fse_cuda_total_sum_dev(fse_cuda_ctx* c, const fse_config* cfg, int ki
     return api(c, [&] {
         run_sum(c, cfg, kind, d_pos, d_str, n, box_side, d_tgt, nt, tas, green, d_u, tm, true,
                 true);
+    });
+}
+
+// ------------------------------------------------------------------ z-slabs
+// slab r of G owns x-planes [x_lo, x_lo + nx) of the M~ grid and the
+// ky rows [ky_lo, ky_lo + nky) of the x-pass.  Every rank holds all points; the
+// exchanges are the two spectrum all-to-alls and one sum of the per-rank
+// partial velocities (the caller runs them, e.g. NCCL via torch.distributed).
+namespace {
+
+GridParams slab_params(const fse_config* cfg, int rank, int nslabs) {
+    check_cfg(cfg);
+    if (nslabs < 1 || rank < 0 || rank >= nslabs) invalid("slab: need 0 <= rank < nslabs");
+    GridParams g = make_grid_params(*cfg);
+    set_slab(g, rank, nslabs);
+    if (nslabs > 1 && !gather_slab_enabled(g))
+        invalid("slab: the decomposition needs the tensor-core quadrature (P <= 25)");
+    return g;
+}
+
+int64_t slab_block_elems(const GridParams& g, int a) {
+    return static_cast<int64_t>(a) * g.nxs * g.nkys * g.Dh;
+}
+
+}  // namespace
+
+fse_status fse_cuda_slab_info(const fse_config* cfg, int kind, int rank, int nslabs,
+                              fse_slab_info* out) {
+    try {
+        check_kind(kind);
+        if (!out) invalid("null pointer");
+        const GridParams g = slab_params(cfg, rank, nslabs);
+        out->x_lo = g.x_lo;
+        out->nx = g.nx;
+        out->nxs = g.nxs;
+        out->ky_lo = g.ky_lo;
+        out->nky = g.nky;
+        out->nkys = g.nkys;
+        out->block_complex = slab_block_elems(g, arity_of(kind));
+        return FSE_OK;
+    } catch (const Error& e) {
+        return e.code;
+    } catch (...) {
+        return FSE_ERUNTIME;
+    }
+}
+
+fse_status fse_cuda_slab_forward(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                 const double* d_pos, const double* d_str, int64_t n, int rank,
+                                 int nslabs, double* d_spec) {
+    return api(c, [&] {
+        check_kind(kind);
+        if (!d_spec || (n > 0 && (!d_pos || !d_str))) invalid("null pointer");
+        const int a = arity_of(kind);
+        const GridParams g = slab_params(cfg, rank, nslabs);
+        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+        Launch L = L0(c);
+        double* qtab = buf<double>(c, "qtab", g.P);
+        launch_quad_table(L, g, qtab);
+        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
+        double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
+        double2* Bs = buf<double2>(c, "B", static_cast<size_t>(a) * g.nx * g.Mt * g.Dh);
+        const FftPlanDev& fp = fft_plan(c, g.D);
+        for (int c0 = 0; c0 < a; c0 += 3)
+            launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
+        launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, reinterpret_cast<double2*>(d_spec));
+        raise_flags(c);  // synchronises s0
+    });
+}
+
+fse_status fse_cuda_slab_scale(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                               const fse_green* green, int rank, int nslabs, double* d_spec) {
+    return api(c, [&] {
+        check_kind(kind);
+        if (!d_spec) invalid("null pointer");
+        const GridParams g = slab_params(cfg, rank, nslabs);
+        check_green(cfg, kind, green);
+        if (green->device != c->device) invalid("green lives on another device");
+        const FftPlanDev& fp = fft_plan(c, g.D);
+        launch_fft_xscale(L0(c), fp.host, fp.tw, g, kind, green->d_half,
+                          reinterpret_cast<double2*>(d_spec));
+        FSE_CU(cudaStreamSynchronize(c->s0));
+    });
+}
+
+fse_status fse_cuda_slab_inverse(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                 const double* d_pos, const double* d_str, int64_t n,
+                                 double* d_spec, int rank, int nslabs, const double* d_tgt,
+                                 int64_t nt, int tas, double* d_u) {
+    return api(c, [&] {
+        check_kind(kind);
+        if (!d_spec || !d_u || (nt > 0 && !d_tgt) || (n > 0 && (!d_pos || !d_str)))
+            invalid("null pointer");
+        const int a = arity_of(kind);
+        const GridParams g = slab_params(cfg, rank, nslabs);
+        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+        Launch L = L0(c);
+        // real space + self term for this rank's share of the targets (stream s1)
+        const int64_t t_lo = nt * rank / nslabs, t_hi = nt * (rank + 1) / nslabs;
+        double* uR = buf<double>(c, "uR", 3 * std::max<int64_t>(t_hi - t_lo, 1));
+        FSE_CU(cudaEventRecord(c->ev[EV_START], c->s0));
+        FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_START], 0));
+        if (t_hi > t_lo)
+            real_part(c, kind, d_pos, d_str, n, cfg->L, cfg->xi, cfg->rc, d_tgt + 3 * t_lo,
+                      t_hi - t_lo, false, uR);
+        FSE_CU(cudaEventRecord(c->ev[EV_JOIN], c->s1));
+        // inverse y/z passes of this slab, then its planes' share of the quadrature
+        double* qtab = buf<double>(c, "qtab", g.P);
+        launch_quad_table(L, g, qtab);
+        double* W = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
+        double2* Bs = buf<double2>(c, "B", static_cast<size_t>(a) * g.nx * g.Mt * g.Dh);
+        const FftPlanDev& fp = fft_plan(c, g.D);
+        launch_fft_inverse_yz(L, fp.host, fp.tw, g, a, reinterpret_cast<double2*>(d_spec), Bs, W);
+        Sorted tg = prep_points(c, g, "ft_", d_tgt, nullptr, 0, nt, 1, qtab);
+        const int64_t nhalf = g.nkeys / 4;
+        int32_t* scnt = buf<int32_t>(c, "scnt", nhalf + 1);
+        int32_t* soff = buf<int32_t>(c, "soff", nhalf + 1);
+        launch_slab_counts(L, tg.tstart, nhalf, scnt);
+        exclusive_scan(c, c->s0, "s0", scnt, soff, nhalf + 1);
+        const int64_t max_items = std::min<int64_t>(nhalf, nt) + (nt + 31) / 32;
+        int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
+        launch_slab_fill(L, soff, nhalf, sitems);
+        if (nt > 0)
+            launch_gather_slab(L, g, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff + nhalf, W,
+                               tg.perm, g.h * g.h * g.h, d_u);
+        FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_JOIN], 0));
+        if (t_hi > t_lo) {
+            const bool self = tas && kind == FSE_STOKESLET;
+            launch_epilogue(L, t_hi - t_lo, d_u + 3 * t_lo, uR, self ? d_str + 3 * t_lo : nullptr,
+                            self ? -4.0 * cfg->xi / std::sqrt(M_PI) : 0.0, d_u + 3 * t_lo);
+        }
+        raise_flags(c);
     });
 }
 

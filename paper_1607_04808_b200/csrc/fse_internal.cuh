@@ -63,7 +63,15 @@ struct GridParams {
     // spread/gather tiling of the support-start space (i0x, i0y, i0z)
     int ncx, ncy, ncz;  // coarse tiles: 8 x 8 x 16
     int64_t nkeys;      // ncx*ncy*ncz*8 fine keys (4 x 4 x 8 sub-tiles)
+    // z-slab decomposition (one GPU: the whole grid, one block).
+    // Real grids hold this slab's x-planes [x_lo, x_lo + nx) (comp = nx*plane);
+    // the spectrum is blocked by nxs x-planes / nkys ky-rows, and this rank's
+    // x-pass covers ky rows [ky_lo, ky_lo + nky).
+    int x_lo, nx, nxs;
+    int ky_lo, nky, nkys;
 };
+// restrict g to slab r of G (x-planes in multiples of 8, ky rows balanced)
+void set_slab(GridParams& g, int r, int G);
 
 GridParams make_grid_params(const fse_config& cfg);
 
@@ -105,6 +113,7 @@ void launch_i32_to_i64(const Launch& L, const int32_t* in, int64_t* out, int64_t
 // k_spread.cu ---------------------------------------------------------------
 // writes the Mt^3 grid of components [c0, c0+3) into X (real view, x-planes
 // of pitch plane, rows of pitch D+2)
+// (tiles of this slab's x-planes only; X holds the slab: x - x_lo)
 void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                    const double* fs, int64_t n, int a, int c0, const int32_t* tstart,
                    double* X);

@@ -205,6 +205,16 @@ __device__ __forceinline__ int cidx(int c, int n, int D) {
     }
 }
 
+// Row (c, x, ky) of the spectrum C in the slab-blocked layout
+// [blk][c][xl][kyl][kz]: the x-slab owner's send buffer is blocked
+// by ky (blk = ky / nkys), the ky-block owner's receive buffer by x (blk =
+// x / nxs).  One GPU: one block, i.e. [c][x][ky][kz].  Returns the offset of
+// element kz = 0 in double2 units.
+__device__ __forceinline__ int64_t spec_row(int blk, int c, int xl, int kyl, int A, int nxs,
+                                            int nkys, int Dh) {
+    return ((((static_cast<int64_t>(blk) * A + c) * nxs + xl) * nkys + kyl) * Dh);
+}
+
 extern __shared__ __align__(16) unsigned char fse_smem[];
 
 // Asynchronous global -> shared copies (LDGSTS): every load of a pass is in
@@ -255,26 +265,26 @@ __global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* 
 // column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
 template <int ENG>
 __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
-                                                 int Mt, int ncomp, int ncol,
+                                                 int Mt, int nx, int ncomp, int ncol,
                                                  const double* __restrict__ R,
                                                  double2* __restrict__ B) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
-    const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
     const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
     const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
-    const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
+    const int64_t vol = static_cast<int64_t>(nx) * Mt * Mt;  // one component of the slab
     const FDiv fDh = make_fdiv(Dh);
     __shared__ int64_t row0[64];  // first R/W row of the pair, in doubles
     __shared__ int64_t brow[64];  // first B row of the pair, in rows of Dh
     __shared__ int has1[64];
     if (threadIdx.x < nc) {
         const int64_t q = q0 + threadIdx.x;
-        const int64_t ci = q / Jp;  // comp * Mt + i
+        const int64_t ci = q / Jp;  // comp * nx + i (slab-local plane i)
         const int jp = static_cast<int>(q - ci * Jp);
-        const int64_t comp = ci / Mt, i = ci - comp * Mt;
+        const int64_t comp = ci / nx, i = ci - comp * nx;
         row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
         brow[threadIdx.x] = ci * Mt + 2 * jp;
         has1[threadIdx.x] = (2 * jp + 1 < Mt);
@@ -314,26 +324,32 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
 // inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
 template <int ENG, bool INV>
 __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
-                                                  int Mt, int ncomp, int ncol,
-                                                  double2* __restrict__ B,
+                                                  int Mt, int nx, int A, int nxs, int nkys,
+                                                  int ncol, double2* __restrict__ B,
                                                   double2* __restrict__ Cb) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1;
     const int ntz = (Dh + ncol - 1) / ncol;
-    const int ci = blockIdx.x / ntz;  // comp * Mt + i
+    const int ci = blockIdx.x / ntz;  // comp * nx + i (slab-local plane i)
     const int tz = blockIdx.x - ci * ntz;
+    const int comp = ci / nx, xl = ci - comp * nx;
     const int kz0 = tz * ncol;
     const int nc = min(ncol, Dh - kz0);
     const FDiv fnc = make_fdiv(nc);
+    const FDiv fky = make_fdiv(nkys);
     double2* Bp = B + static_cast<int64_t>(ci) * Mt * Dh + kz0;   // [j][kz]
-    double2* Cp = Cb + static_cast<int64_t>(ci) * D * Dh + kz0;   // [ky][kz]
+    // C row ky of (comp, xl): spec_row(ky / nkys, comp, xl, ky % nkys) (send layout)
+    auto crow = [&](int ky) -> int64_t {
+        const int blk = static_cast<int>(fdiv(ky, fky));
+        return spec_row(blk, comp, xl, ky - blk * nkys, A, nxs, nkys, Dh) + kz0;
+    };
     const int nin = INV ? D : Mt;
-    const double2* src = INV ? Cp : Bp;
     for (int e = threadIdx.x; e < nc * nin; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;  // lanes walk kz
-        cp16(a + cidx<ENG>(c, j, D), src + static_cast<int64_t>(j) * Dh + c);
+        const double2* src = INV ? Cb + crow(j) + c : Bp + static_cast<int64_t>(j) * Dh + c;
+        cp16(a + cidx<ENG>(c, j, D), src);
     }
     if (!INV)
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
@@ -344,10 +360,10 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, INV ? +1 : -1);
     const int nout = INV ? Mt : D;
-    double2* dst = INV ? Bp : Cp;
     for (int e = threadIdx.x; e < nc * nout; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;
-        dst[static_cast<int64_t>(j) * Dh + c] = r[cidx<ENG>(c, j, D)];
+        double2* dst = INV ? Bp + static_cast<int64_t>(j) * Dh + c : Cb + crow(j) + c;
+        *dst = r[cidx<ENG>(c, j, D)];
     }
 }
 
@@ -416,14 +432,18 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     const double2* tw = stage_twiddles(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Mt = g.Mt;
     const int ntz = (Dh + ncol - 1) / ncol;
-    const int ky = blockIdx.x / ntz;
-    const int tz = blockIdx.x - ky * ntz;
+    const int kyl = blockIdx.x / ntz;  // row of this rank's ky block
+    const int ky = g.ky_lo + kyl;
+    const int tz = blockIdx.x - kyl * ntz;
     const int kz0 = tz * ncol;
     const int nc = min(ncol, Dh - kz0);
     const FDiv fnc = make_fdiv(nc);
-    const int64_t compC = static_cast<int64_t>(Mt) * D * Dh;
-    const int64_t rowoff = static_cast<int64_t>(ky) * Dh + kz0;  // within an i-slab
-    const int64_t slab = static_cast<int64_t>(D) * Dh;
+    const FDiv fnxs = make_fdiv(g.nxs);
+    // C row (comp, x) of this ky in the receive layout (blocked by x / nxs)
+    auto crow = [&](int comp, int i) -> int64_t {
+        const int blk = static_cast<int>(fdiv(i, fnxs));
+        return spec_row(blk, comp, i - blk * g.nxs, kyl, A, g.nxs, g.nkys, Dh) + kz0;
+    };
     // Green's column slice G[kx][ky][kz0 + c] staged with the data
     double* Gs = reinterpret_cast<double*>(const_cast<double2*>(tw) + pl.tw_elems);
     for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
@@ -431,10 +451,9 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         cp8(Gs + e, G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0 + c);
     }
     for (int comp = 0; comp < A; ++comp) {
-        const double2* src = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;  // lanes walk kz
-            cp16(a + cidx<ENG>(comp * nc + c, i, D), src + static_cast<int64_t>(i) * slab + c);
+            cp16(a + cidx<ENG>(comp * nc + c, i, D), Cb + crow(comp, i) + c);
         }
         for (int e = threadIdx.x; e < nc * (D - Mt); e += blockDim.x) {
             const int ii = static_cast<int>(fdiv(e, fnc)), c = e - ii * nc;
@@ -478,10 +497,9 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     double2* other = (r == a) ? sb : a;
     double2* r2 = fft_cols<ENG>(r, other, 3 * nc, pl, tw, +1);
     for (int comp = 0; comp < 3; ++comp) {
-        double2* dst = Cb + comp * compC + rowoff;
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;
-            dst[static_cast<int64_t>(i) * slab + c] = r2[cidx<ENG>(comp * nc + c, i, D)];
+            Cb[crow(comp, i) + c] = r2[cidx<ENG>(comp * nc + c, i, D)];
         }
     }
 }
@@ -490,17 +508,17 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
 // row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
 template <int ENG>
 __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
-                                                 int Mt, int ncomp, int ncol,
+                                                 int Mt, int nx, int ncomp, int ncol,
                                                  const double2* __restrict__ B,
                                                  double* __restrict__ W) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
-    const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
     const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
     const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
-    const int64_t vol = static_cast<int64_t>(Mt) * Mt * Mt;
+    const int64_t vol = static_cast<int64_t>(nx) * Mt * Mt;
     const FDiv fDh = make_fdiv(Dh);
     __shared__ int64_t row0[64];
     __shared__ int64_t brow[64];
@@ -509,7 +527,7 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
         const int64_t q = q0 + threadIdx.x;
         const int64_t ci = q / Jp;
         const int jp = static_cast<int>(q - ci * Jp);
-        const int64_t comp = ci / Mt, i = ci - comp * Mt;
+        const int64_t comp = ci / nx, i = ci - comp * nx;
         row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
         brow[threadIdx.x] = ci * Mt + 2 * jp;
         has1[threadIdx.x] = (2 * jp + 1 < Mt);
@@ -738,10 +756,13 @@ void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw
     ++*L.launches;
 }
 
-void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
-                           int ncomp, const double* R, double2* B, double2* C) {
+void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                           const GridParams& g, int ncomp, const double* R, double2* B,
+                           double2* C) {
     upload_consts();
+    const int Mt = g.Mt, nx = g.nx;
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    if (nx <= 0 || ncomp <= 0) return;  // empty slab
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
@@ -750,9 +771,9 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
             allow_smem(k_zfwd<EV>, sm);
-            const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+            const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             k_zfwd<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
-                p, d_tw, Mt, ncomp, u, R, B);
+                p, d_tw, Mt, nx, ncomp, u, R, B);
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -763,8 +784,9 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             allow_smem(k_ypass<EV, false>, sm);
             const int ntz = (Dh + u - 1) / u;
-            k_ypass<EV, false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz),
-                                 kThreads, sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+            k_ypass<EV, false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz),
+                                 kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs, g.nkys, u,
+                                                      B, C);
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -781,7 +803,8 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     set_buf(p, h, A * u);
     const size_t sm = smem_bytes(h, A * u) + sizeof(double) * u * D;
     const int ntz = (Dh + u - 1) / u;
-    const unsigned blocks = static_cast<unsigned>(D) * ntz;
+    const unsigned blocks = static_cast<unsigned>(g.nky) * ntz;
+    if (blocks == 0) return;
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         if (kind == FSE_STOKESLET) {
@@ -799,10 +822,12 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     ++*L.launches;
 }
 
-void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
-                           int ncomp, double2* C, double2* B, double* W) {
+void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                           const GridParams& g, int A, double2* C, double2* B, double* W) {
     upload_consts();
+    const int Mt = g.Mt, nx = g.nx, ncomp = 3;
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    if (nx <= 0) return;  // empty slab
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
@@ -812,8 +837,9 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             allow_smem(k_ypass<EV, true>, sm);
             const int ntz = (Dh + u - 1) / u;
-            k_ypass<EV, true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * Mt * ntz),
-                                kThreads, sm, L.s>>>(p, d_tw, Mt, ncomp, u, B, C);
+            k_ypass<EV, true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz),
+                                kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u, B,
+                                                     C);
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -823,9 +849,9 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
             allow_smem(k_zinv<EV>, sm);
-            const int64_t npairs = static_cast<int64_t>(ncomp) * Mt * Jp;
+            const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             k_zinv<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
-                p, d_tw, Mt, ncomp, u, B, W);
+                p, d_tw, Mt, nx, ncomp, u, B, W);
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }

@@ -61,14 +61,17 @@ HostFftPlan make_fft_plan(int D);
 void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw, double2* data,
                       int ncols, int inverse);
 
-// R (a x Mt^3 real) -> B (a x Mt x Mt x Dh) -> C (a x Mt x D x Dh)
-void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
-                           int ncomp, const double* R, double2* B, double2* C);
-// C: forward x-FFT, multiply by A_eff(k) G(k) / D^3, inverse x-FFT, in place (3 comps out)
+// R (a x nx x Mt^2 real, this slab's planes) -> B (a x nx x Mt x Dh) -> C (slab-blocked
+// send layout, see spec_row in k_fft.cu; one GPU: a x Mt x D x Dh)
+void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                           const GridParams& g, int ncomp, const double* R, double2* B,
+                           double2* C);
+// C (receive layout, ky rows [ky_lo, ky_lo + nky)): forward x-FFT, multiply by
+// A_eff(k) G(k) / D^3, inverse x-FFT, in place (3 comps out)
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                        const GridParams& g, int kind, const double* G, double2* C);
-// C (3 comps) -> B (j < Mt) -> W (3 x Mt^3 real)
-void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw, int Mt,
-                           int ncomp, double2* C, double2* B, double* W);
+// C (send layout, 3 comps in blocks of A) -> B (j < Mt) -> W (3 x nx x Mt^2 real)
+void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
+                           const GridParams& g, int A, double2* C, double2* B, double* W);
 
 }  // namespace fsecu

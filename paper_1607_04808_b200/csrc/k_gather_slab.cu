@@ -65,8 +65,8 @@ template <int KS>
 __device__ __forceinline__ void stage_slab(const GridParams& g, const double* __restrict__ X,
                                            int x, int y0, int z0, int NY, int NZ, bool vec16,
                                            double* dst) {
-    const double* src0 =
-        X + static_cast<int64_t>(x) * g.plane + static_cast<int64_t>(y0) * g.rowp + z0;
+    const double* src0 = X + static_cast<int64_t>(x - g.x_lo) * g.plane +
+                         static_cast<int64_t>(y0) * g.rowp + z0;  // slab-local plane
     if (vec16) {
         constexpr int NCH = 2 * KS;  // 16-byte chunks per row
         const int total = 3 * NY * NCH;
@@ -111,10 +111,15 @@ __device__ void gather_item(const GridParams& g, const double* __restrict__ X, d
     const int rbase = 8 * MT * warp + (lane >> 2);
     const int tb = lane >> 2;  // B column (target within an n-tile) of this lane
 
-    stage_slab<KS>(g, X, x0, y0, z0, NY, NZ, vec16, slab);
-    cp_commit();
-    for (int xs = 0; xs < NX; ++xs) {
-        if (xs + 1 < NX) {
+    // planes of the union box inside this rank's slab (all of them on one GPU);
+    // with several slabs every rank adds its planes' share of the sum
+    const int xs0 = max(0, g.x_lo - x0), xs1 = min(NX, g.x_lo + g.nx - x0);
+    if (xs0 < xs1) {
+        stage_slab<KS>(g, X, x0 + xs0, y0, z0, NY, NZ, vec16, slab + (xs0 & 1) * buf_elems);
+        cp_commit();
+    }
+    for (int xs = xs0; xs < xs1; ++xs) {
+        if (xs + 1 < xs1) {
             stage_slab<KS>(g, X, x0 + xs + 1, y0, z0, NY, NZ, vec16,
                            slab + ((xs + 1) & 1) * buf_elems);
             cp_commit();

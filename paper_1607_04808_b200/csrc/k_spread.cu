@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
     const int tile = blockIdx.x;
     const int tz = tile % g.ncz;
     const int ty = (tile / g.ncz) % g.ncy;
-    const int tx = tile / (g.ncz * g.ncy);
+    const int tx = g.x_lo / TX + tile / (g.ncz * g.ncy);  // this slab's x tiles
     const int x0n = tx * TX, y0n = ty * TY, z0n = tz * TZ;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // warp w owns z in [z0n + 8w, +8) of all 8 x 8 (x, y) rows of the tile
@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
 #pragma unroll
     for (int r = 0; r < TX; ++r) {
         const int x = x0n + r;
-        if (x >= g.Mt) break;
-        const int64_t off = x * g.plane + y * g.rowp + z;
+        if (x >= g.x_lo + g.nx) break;
+        const int64_t off = (x - g.x_lo) * g.plane + y * g.rowp + z;  // slab-local plane
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double* dst = X + (c0 + c) * g.comp + off;
@@ -236,7 +236,8 @@ void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, con
                    const double* fs, int64_t n, int a, int c0, const int32_t* tstart,
                    double* X) {
     (void)n;
-    const unsigned tiles = static_cast<unsigned>(g.ncx) * g.ncy * g.ncz;
+    const unsigned tiles = static_cast<unsigned>((g.nx + TX - 1) / TX) * g.ncy * g.ncz;
+    if (tiles == 0) return;
     k_spread<<<tiles, NWARP * 32, 0, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
