@@ -63,12 +63,17 @@ def metric_name(w):
 
 # ------------------------------------------------------------------ dist
 class Dist:
-    def __init__(self):
+    def __init__(self, force_group=False):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
-        if self.world > 1:
+        self.grouped = self.world > 1 or force_group
+        if self.grouped:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", str(self.rank))
+            os.environ.setdefault("WORLD_SIZE", str(self.world))
             import torch
             import torch.distributed as td
             self.torch, self.td = torch, td
@@ -79,18 +84,18 @@ class Dist:
             self.dev = torch.device("cuda", self.local) if backend == "nccl" else torch.device("cpu")
 
     def barrier(self):
-        if self.world > 1:
+        if self.grouped:
             self.td.barrier()
 
     def max(self, v: float) -> float:
-        if self.world == 1:
+        if not self.grouped:
             return v
         t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
 
     def close(self):
-        if self.world > 1:
+        if self.grouped:
             self.td.destroy_process_group()
 
 
@@ -188,6 +193,144 @@ def stage_models(w, cfg, n, nt, rs_pairs=None):
     if rs_pairs:
         models["realspace"] = ("fp64", PAIR_FLOPS[w["kind"]] * rs_pairs)
     return models
+
+
+# ------------------------------------------------------------------ ours, z-slabs
+def run_slabs(args, dist: Dist):
+    """N > 1: one evaluation of the workload decomposed into N z-slabs
+    (paper_1607_04808_b200/slabs.py): the same system on every rank,
+    NCCL all-to-all spectrum transposes and one sum of partial velocities.
+    Total work fixed as N grows: strong scaling."""
+    import torch
+    import paper_1607_04808_b200 as fse
+    from paper_1607_04808_b200.slabs import SlabSum, TorchExchange
+
+    w = WORKLOADS[args.workload]
+    ctx = fse.Context(dist.local)
+    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED)  # replicated inputs
+    targets = system.positions if tgt is None else tgt
+    n, nt = system.size(), targets.shape[0]
+    tas = tgt is None
+    cfg = fse.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    green = ctx.precompute_mollified_green(int(fse.green_kind_for(w["kind"])), cfg.Ltilde,
+                                           cfg.Mtilde, cfg.sf)
+    d_pos = ctx.dev_alloc(system.positions.nbytes)
+    d_str = ctx.dev_alloc(system.strengths.nbytes)
+    d_tgt = d_pos if tas else ctx.dev_alloc(targets.nbytes)
+    d_u = ctx.dev_alloc(8 * 3 * nt)
+    hp = ctx.host_alloc(system.positions.shape)
+    hs = ctx.host_alloc(system.strengths.shape)
+    hp[...] = system.positions
+    hs[...] = system.strengths
+    ht = hp if tas else ctx.host_alloc(targets.shape)
+    if not tas:
+        ht[...] = targets
+    u_host = ctx.host_alloc((nt, 3))
+
+    def upload():
+        ctx.memcpy(d_pos, hp.ctypes.data, hp.nbytes)
+        ctx.memcpy(d_str, hs.ctypes.data, hs.nbytes)
+        if not tas:
+            ctx.memcpy(d_tgt, ht.ctypes.data, ht.nbytes)
+
+    upload()
+    ex = TorchExchange()
+    ss = SlabSum(ctx, cfg, w["kind"], dist.rank, dist.world)
+
+    def step():
+        ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.launch_count
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count - launches0
+    clk = clocks.stop()
+    dist.barrier()
+    max_ms = dist.max(dev_ms)
+
+    # phase breakdown (untimed step, host-synchronised phases)
+    import torch as _t
+    send_t = None
+    ph = {}
+    t0 = time.perf_counter()
+    ss.forward(d_pos, d_str, n)
+    ph["forward"] = time.perf_counter() - t0
+    from paper_1607_04808_b200.slabs import torch_view
+    send_t = torch_view(ss.d_send, ss.block_doubles * ss.nslabs)
+    recv_t = torch_view(ss.d_recv, ss.block_doubles * ss.nslabs)
+    t0 = time.perf_counter()
+    ex.all_to_all(send_t, recv_t)
+    ph["all_to_all"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ss.scale(green)
+    ph["scale"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ex.all_to_all(recv_t, send_t)
+    ph["all_to_all_back"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ss.inverse(d_pos, d_str, n, d_tgt, nt, tas, d_u)
+    ph["inverse_gather_realspace"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ex.all_reduce_sum(torch_view(d_u, 3 * nt))
+    ph["sum_partials"] = time.perf_counter() - t0
+    del _t
+
+    # e2e: pinned host inputs -> device every step, result back on every rank
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        upload()
+        step()
+        ctx.memcpy(u_host.ctypes.data, d_u, u_host.nbytes)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    h2d = hp.nbytes + hs.nbytes + (0 if tas else ht.nbytes)
+
+    # roofline: the step's algorithmic FP64 work per rank over the step time
+    a = 9 if w["kind"] == 1 else 3
+    flops = 2.0 * a * cfg.P ** 3 * n + 2.0 * 3 * cfg.P ** 3 * nt
+    fp64_peak = args.fp64_peak or ctx.measure_fp64_peak()
+    ach = flops / dist.world / (max_ms / args.steps * 1e-3) / 1e12
+    value = nt * args.steps / (max_ms * 1e-3)
+    line = {
+        "metric": metric_name(w), "value": value, "unit": "targets/s", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}), "
+                "same system on every rank, no dataset",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
+                   "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
+                   "parallelism": f"z-slabs x{dist.world} (NCCL all-to-all transposes)",
+                   "slab": {"x_lo": ss.info.x_lo, "nx": ss.info.nx, "ky_lo": ss.info.ky_lo,
+                            "nky": ss.info.nky},
+                   "l2": "working set >> 126 MB L2; no flush needed"},
+        "e2e": {"value": nt * max(1, args.steps) / e2e_s, "unit": "targets/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * 3 * nt),
+                "api": "slabs.SlabSum.run (fse_cuda_slab_* + torch.distributed NCCL)"},
+        "roofline": {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": ach / fp64_peak, "kernel": "step (spread + quadrature work / rank)",
+                     "traffic": None},
+        "phase_s_rank0": ph,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "cpu_baseline": None,
+    }
+    if dist.rank == 0:
+        print(json.dumps(line))
+    ss.free()
+    for p in (d_pos, d_str, d_u) + (() if tas else (d_tgt,)):
+        ctx.dev_free(p)
 
 
 # ------------------------------------------------------------------ ours
@@ -457,6 +600,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent full evaluations per GPU instead of z-slabs")
+    ap.add_argument("--slabs", action="store_true",
+                    help="use the z-slab path also at N = 1 (one slab, NCCL group of one)")
     ap.add_argument("--ref-frac", type=int, default=64,
                     help="--impl reference: sample = 1/ref_frac of the points per step")
     ap.add_argument("--fp64-peak", type=float, default=None,
@@ -464,10 +611,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
-    dist = Dist()
+    dist = Dist(force_group=args.slabs and args.impl == "ours")
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif (dist.world > 1 and not args.replicas) or args.slabs:
+            run_slabs(args, dist)
         else:
             run_ours(args, dist)
     finally:
