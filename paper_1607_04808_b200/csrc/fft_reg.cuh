@@ -257,5 +257,105 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
     __syncthreads();
 }
 
+// ---- two-level passes with caller-supplied global I/O (the "v2" kernels in
+// k_fft.cu): pass 1 loads straight from global memory into registers and
+// pass 2 stores straight from registers, so the only shared-memory round trip
+// of a plain transform is the transpose between the passes.
+//
+// Item mapping: CF (column-fastest) -- consecutive threads walk the columns,
+// for passes whose columns are adjacent in memory (y, x); otherwise
+// consecutive threads walk n2 (pass 1) / k1 (pass 2), for rows (z).
+
+template <int D1, int D2, bool CF>
+__device__ __forceinline__ bool item1(int ncol, int& c, int& n2) {
+    const int tid = threadIdx.x;
+    if (tid >= ncol * D2) return false;
+    if (CF) {
+        n2 = tid / ncol;
+        c = tid - n2 * ncol;
+    } else {
+        c = tid / D2;
+        n2 = tid - c * D2;
+    }
+    return true;
+}
+
+template <int D1, int D2, bool CF>
+__device__ __forceinline__ bool item2(int ncol, int& c, int& k1) {
+    const int tid = threadIdx.x;
+    if (tid >= ncol * D1) return false;
+    if (CF) {
+        k1 = tid / ncol;
+        c = tid - k1 * ncol;
+    } else {
+        c = tid / D1;
+        k1 = tid - c * D1;
+    }
+    return true;
+}
+
+// pass 1: v[n1] = load(c, n1 D2 + n2) for n1 < NZ1 (rows n1 >= NZ1 are known
+// zeros: zero-padded inputs), FFT_D1, twiddle W_D^{n2 k1}, store the transpose
+// into buf[ridx(c, k1 D2 + n2)].  No barriers inside.
+template <int D1, int D2, bool CF, int NZ1, class LOAD>
+__device__ __forceinline__ void pass1(double2* buf, int ncol, int sgn, const double2* twD,
+                                      const double2* tab, LOAD load) {
+    constexpr int D = D1 * D2;
+    int c, n2;
+    if (!item1<D1, D2, CF>(ncol, c, n2)) return;
+    double2 v[D1];
+#pragma unroll
+    for (int n1 = 0; n1 < D1; ++n1) v[n1] = n1 < NZ1 ? load(c, n1 * D2 + n2) : make_double2(0.0, 0.0);
+    rfft<D1>(v, sgn, tab);
+    int t = 0;  // n2 * k1 mod D
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) {
+        if (k1 > 0) {
+            double2 w = twD[t];
+            if (sgn > 0) w.y = -w.y;
+            v[k1] = cmul(v[k1], w);
+        }
+        t += n2;
+        if (t >= D) t -= D;
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) buf[ridx<D1, D2>(c, k1 * D2 + n2)] = v[k1];
+}
+
+// pass 2 (after a barrier): u[j] = buf[ridx(c, k1 D2 + j)], FFT_D2, then
+// store(c, k1 + D1 k2, u[k2]) for k2 < NOUT2 (outputs k2 >= NOUT2 are not
+// needed: pruned windows).  No barriers inside.
+template <int D1, int D2, bool CF, int NOUT2, class STORE>
+__device__ __forceinline__ void pass2(const double2* buf, int ncol, int sgn, const double2* tab,
+                                      STORE store) {
+    int c, k1;
+    if (!item2<D1, D2, CF>(ncol, c, k1)) return;
+    double2 u[D2];
+#pragma unroll
+    for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c, k1 * D2 + j)];
+    rfft<D2>(u, sgn, tab);
+#pragma unroll
+    for (int k2 = 0; k2 < NOUT2; ++k2) store(c, k1 + D1 * k2, u[k2]);
+}
+
+// pass 2 back into buf in natural order (for a following shared-memory stage):
+// loads, barrier, stores (every thread of the CTA must call it)
+template <int D1, int D2, bool CF>
+__device__ __forceinline__ void pass2_smem(double2* buf, int ncol, int sgn, const double2* tab) {
+    int c = 0, k1 = 0;
+    const bool act = item2<D1, D2, CF>(ncol, c, k1);
+    double2 u[D2];
+    if (act) {
+#pragma unroll
+        for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c, k1 * D2 + j)];
+        rfft<D2>(u, sgn, tab);
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+        for (int k2 = 0; k2 < D2; ++k2) buf[ridx<D1, D2>(c, k1 + D1 * k2)] = u[k2];
+    }
+}
+
 }  // namespace freg
 }  // namespace fsecu

@@ -559,6 +559,233 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
     }
 }
 
+// ================================================================ v2 kernels
+// Register engines (ENG > 0) with direct global I/O (freg::pass1 / pass2):
+// the first pass of each transform loads its columns straight from global
+// memory into registers (the zero-padded half is never loaded: NZ1) and the
+// last pass stores straight to global memory (only the kept window: NOUT2),
+// so a plain transform makes one shared-memory round trip (the transpose)
+// instead of three (staging, transpose, unstaging).
+
+// z forward: column c = row pair (comp, i, jp), rows contiguous -> n2-fastest
+template <int ENG>
+__global__ void __launch_bounds__(256, 2) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
+                                                  int Mt, int nx, int ncomp, int ncol,
+                                                  const double* __restrict__ R,
+                                                  double2* __restrict__ B) {
+    constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tab = tw + D;
+    const int Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
+    const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
+    const int64_t vol = static_cast<int64_t>(nx) * Mt * Mt;
+    const FDiv fDh = make_fdiv(Dh);
+    __shared__ int64_t row0[64];
+    __shared__ int64_t brow[64];
+    __shared__ int has1[64];
+    if (threadIdx.x < nc) {
+        const int64_t q = q0 + threadIdx.x;
+        const int64_t ci = q / Jp;
+        const int jp = static_cast<int>(q - ci * Jp);
+        const int64_t comp = ci / nx, i = ci - comp * nx;
+        row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
+        brow[threadIdx.x] = ci * Mt + 2 * jp;
+        has1[threadIdx.x] = (2 * jp + 1 < Mt);
+    }
+    __syncthreads();
+    freg::pass1<D1, D2, false, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
+        double2 z = make_double2(0.0, 0.0);
+        if (n < Mt) {
+            const double* row = R + row0[c];
+            z.x = __ldg(row + n);
+            if (has1[c]) z.y = __ldg(row + Mt + n);
+        }
+        return z;
+    });
+    __syncthreads();
+    freg::pass2_smem<D1, D2, false>(a, nc, -1, tab);
+    __syncthreads();
+    // split: X0[k] = (Z[k] + conj Z[-k]) / 2, X1[k] = (Z[k] - conj Z[-k]) / (2i)
+    for (int e = threadIdx.x; e < nc * Dh; e += blockDim.x) {
+        const int c = static_cast<int>(fdiv(e, fDh)), k = e - c * Dh;
+        const double2 zk = a[freg::ridx<D1, D2>(c, k)];
+        const double2 zm = a[freg::ridx<D1, D2>(c, k == 0 ? 0 : D - k)];
+        const double2 x0 = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        const double2 x1 = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+        double2* dst = B + brow[c] * Dh + k;
+        dst[0] = x0;
+        if (has1[c]) dst[Dh] = x1;
+    }
+}
+
+// y passes: column c = (comp, slab plane xl, kz0 + c), columns adjacent in kz -> c-fastest
+template <int ENG, bool INV>
+__global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
+                                                   int Mt, int nx, int A, int nxs, int nkys,
+                                                   int ncol, double2* __restrict__ B,
+                                                   double2* __restrict__ Cb) {
+    constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tab = tw + D;
+    const int Dh = D / 2 + 1;
+    const int ntz = (Dh + ncol - 1) / ncol;
+    const int ci = blockIdx.x / ntz;
+    const int tz = blockIdx.x - ci * ntz;
+    const int comp = ci / nx, xl = ci - comp * nx;
+    const int kz0 = tz * ncol;
+    const int nc = min(ncol, Dh - kz0);
+    const FDiv fky = make_fdiv(nkys);
+    double2* Bp = B + static_cast<int64_t>(ci) * Mt * Dh + kz0;
+    auto crow = [&](int ky) -> int64_t {
+        const int blk = static_cast<int>(fdiv(ky, fky));
+        return spec_row(blk, comp, xl, ky - blk * nkys, A, nxs, nkys, Dh) + kz0;
+    };
+    if (!INV) {
+        freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
+            return n < Mt ? Bp[static_cast<int64_t>(n) * Dh + c] : make_double2(0.0, 0.0);
+        });
+        __syncthreads();
+        freg::pass2<D1, D2, true, D2>(a, nc, -1, tab,
+                                      [&](int c, int k, double2 v) { Cb[crow(k) + c] = v; });
+    } else {
+        freg::pass1<D1, D2, true, D1>(a, nc, +1, tw, tab,
+                                      [&](int c, int n) { return Cb[crow(n) + c]; });
+        __syncthreads();
+        freg::pass2<D1, D2, true, D2 / 2>(a, nc, +1, tab, [&](int c, int k, double2 v) {
+            Bp[static_cast<int64_t>(k) * Dh + c] = v;  // k < Mt by NOUT2
+        });
+    }
+}
+
+// x pass + multiplier: columns (comp, kz0 + c), c-fastest
+template <int ENG, int KIND>
+__global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
+                                                    GridParams g, int ncol,
+                                                    const double* __restrict__ G,
+                                                    double2* __restrict__ Cb) {
+    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tab = tw + D;
+    const int Dh = D / 2 + 1, Mt = g.Mt;
+    const int ntz = (Dh + ncol - 1) / ncol;
+    const int kyl = blockIdx.x / ntz;
+    const int ky = g.ky_lo + kyl;
+    const int tz = blockIdx.x - kyl * ntz;
+    const int kz0 = tz * ncol;
+    const int nc = min(ncol, Dh - kz0);
+    const FDiv fnc = make_fdiv(nc);
+    const FDiv fnxs = make_fdiv(g.nxs);
+    auto crow = [&](int comp, int i) -> int64_t {
+        const int blk = static_cast<int>(fdiv(i, fnxs));
+        return spec_row(blk, comp, i - blk * g.nxs, kyl, A, g.nxs, g.nkys, Dh) + kz0;
+    };
+    // forward x-FFT of the A components (pass 1 straight from global memory)
+    freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
+        const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
+        return n < Mt ? Cb[crow(comp, n) + c] : make_double2(0.0, 0.0);
+    });
+    __syncthreads();
+    freg::pass2_smem<D1, D2, true>(a, A * nc, -1, tab);
+    __syncthreads();
+    // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
+    // Hermitian average (see k_kscale.cu), 1/D^3 folded in
+    const int half = D / 2;
+    for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
+        const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
+        const int kz = kz0 + c;
+        double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
+        const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
+                                    __dmul_rn(k[2], k[2]));
+        const double rem = exp(-(1.0 - g.eta) * k2 * g.inv4xi2);
+        const double gval = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz);
+        double2 gh[A];
+#pragma unroll
+        for (int q = 0; q < A; ++q) gh[q] = a[freg::ridx<D1, D2>(q * nc + c, kx)];
+        double2 out[3];
+        apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
+        if (kx == half || ky == half || kz == half) {
+            if (kx == half) k[0] = -k[0];
+            if (ky == half) k[1] = -k[1];
+            if (kz == half) k[2] = -k[2];
+            double2 o2[3];
+            apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, o2);
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+                out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+            a[freg::ridx<D1, D2>(p * nc + c, kx)] =
+                make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
+    }
+    __syncthreads();
+    // inverse x-FFT of the 3 results (pass 1 in place from shared memory:
+    // every item reads and writes only its own (column, n2) elements)
+    freg::pass1<D1, D2, true, D1>(a, 3 * nc, +1, tw, tab,
+                                  [&](int col, int n) { return a[freg::ridx<D1, D2>(col, n)]; });
+    __syncthreads();
+    freg::pass2<D1, D2, true, D2 / 2>(a, 3 * nc, +1, tab, [&](int col, int k, double2 v) {
+        const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
+        Cb[crow(comp, k) + c] = v;  // k < Mt by NOUT2
+    });
+}
+
+// z inverse: row pairs, Hermitian extension loaded straight from B, n2-fastest
+template <int ENG>
+__global__ void __launch_bounds__(256, 2) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
+                                                  int Mt, int nx, int ncomp, int ncol,
+                                                  const double2* __restrict__ B,
+                                                  double* __restrict__ W) {
+    constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
+    double2* a = reinterpret_cast<double2*>(fse_smem);
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tab = tw + D;
+    const int Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
+    const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
+    const int nc = static_cast<int>(npairs - q0 < ncol ? npairs - q0 : ncol);
+    const int64_t vol = static_cast<int64_t>(nx) * Mt * Mt;
+    __shared__ int64_t row0[64];
+    __shared__ int64_t brow[64];
+    __shared__ int has1[64];
+    if (threadIdx.x < nc) {
+        const int64_t q = q0 + threadIdx.x;
+        const int64_t ci = q / Jp;
+        const int jp = static_cast<int>(q - ci * Jp);
+        const int64_t comp = ci / nx, i = ci - comp * nx;
+        row0[threadIdx.x] = comp * vol + (i * Mt + 2 * jp) * Mt;
+        brow[threadIdx.x] = ci * Mt + 2 * jp;
+        has1[threadIdx.x] = (2 * jp + 1 < Mt);
+    }
+    __syncthreads();
+    freg::pass1<D1, D2, false, D1>(a, nc, +1, tw, tab, [&](int c, int n) {
+        // Z[n] = X0 + i X1 (n <= D/2); conj(X0[D-n]) + i conj(X1[D-n]) above
+        const bool lo = n <= D / 2;
+        const int k = lo ? n : D - n;
+        const double2* src = B + brow[c] * Dh + k;
+        double2 x0 = src[0];
+        double2 x1 = has1[c] ? src[Dh] : make_double2(0.0, 0.0);
+        if (k == 0 || k == D / 2) {  // C2R: self-conjugate bins are real
+            x0.y = 0.0;
+            x1.y = 0.0;
+        }
+        return lo ? make_double2(x0.x - x1.y, x0.y + x1.x)
+                  : make_double2(x0.x + x1.y, -x0.y + x1.x);
+    });
+    __syncthreads();
+    freg::pass2<D1, D2, false, D2 / 2>(a, nc, +1, tab, [&](int c, int n, double2 v) {
+        double* row = W + row0[c];  // n < Mt by NOUT2
+        row[n] = v.x;
+        if (has1[c]) row[Mt + n] = v.y;
+    });
+}
+
 int maxit_host(int p) { return (16 + p - 1) / p; }
 bool is_reg_radix(int p) {
     return p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 11 || p == 13;
@@ -606,6 +833,25 @@ double2 cexp_neg(long double num, long double den) {
 }
 
 constexpr int kThreads = 256;
+
+// which passes use the direct-I/O register kernels (bit 0 z fwd, 1 y fwd,
+// 2 x-pass, 3 y inv, 4 z inv).  Measured at D = 624 (24 x 26): z fwd, x-pass
+// and z inv gain, y inv loses (register spills at the 2-CTA/SM cap), y fwd
+// is even; at D = 1200 (30 x 40, 40-element pass-2 registers) every v2
+// pass loses.  FSE_FFT_V2 overrides (profiling aid).
+int v2_mask_env() {
+    static const int m = [] {
+        const char* e = std::getenv("FSE_FFT_V2");
+        return e ? std::atoi(e) : -1;
+    }();
+    return m;
+}
+template <int ENG>
+int v2_mask_for() {
+    const int e = v2_mask_env();
+    if (e >= 0) return e;
+    return ENG == 2 ? 0 : (1 | 2 | 4 | 16);
+}
 constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
 
 }  // namespace
@@ -770,10 +1016,20 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
-            allow_smem(k_zfwd<EV>, sm);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
-            k_zfwd<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
-                p, d_tw, Mt, nx, ncomp, u, R, B);
+            const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
+            if constexpr (EV > 0) {
+                if (v2_mask_for<EV>() & 1) {
+                    allow_smem(k_zfwd2<EV>, sm);
+                    k_zfwd2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                } else {
+                    allow_smem(k_zfwd<EV>, sm);
+                    k_zfwd<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                }
+            } else {
+                allow_smem(k_zfwd<EV>, sm);
+                k_zfwd<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+            }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -782,11 +1038,23 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
-            allow_smem(k_ypass<EV, false>, sm);
             const int ntz = (Dh + u - 1) / u;
-            k_ypass<EV, false><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz),
-                                 kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs, g.nkys, u,
-                                                      B, C);
+            const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
+            if constexpr (EV > 0) {
+                if (v2_mask_for<EV>() & 2) {
+                    allow_smem(k_ypass2<EV, false>, sm);
+                    k_ypass2<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                                                                   g.nkys, u, B, C);
+                } else {
+                    allow_smem(k_ypass<EV, false>, sm);
+                    k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                                                                  g.nkys, u, B, C);
+                }
+            } else {
+                allow_smem(k_ypass<EV, false>, sm);
+                k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                                                              g.nkys, u, B, C);
+            }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -798,15 +1066,32 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     upload_consts();
     const int A = arity_of(kind);
     const int D = h.dev.D, Dh = D / 2 + 1;
-    const int u = std::min(units_fit(h, A, sizeof(double) * static_cast<size_t>(D)), Dh);
+    // v2 (register engines) reads G from global memory; v1 stages it
+    int xmask = 0;
+    with_engine(h.eng, [&](auto E) { xmask = v2_mask_for<decltype(E)::value>(); });
+    const size_t gcol = (h.eng > 0 && (xmask & 4)) ? 0 : sizeof(double) * static_cast<size_t>(D);
+    const int u = std::min(units_fit(h, A, gcol), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
-    const size_t sm = smem_bytes(h, A * u) + sizeof(double) * u * D;
+    const size_t sm = smem_bytes(h, A * u) + gcol * u;
     const int ntz = (Dh + u - 1) / u;
     const unsigned blocks = static_cast<unsigned>(g.nky) * ntz;
     if (blocks == 0) return;
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
+        if constexpr (EV > 0) if (v2_mask_for<EV>() & 4) {
+            if (kind == FSE_STOKESLET) {
+                allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            } else if (kind == FSE_STRESSLET) {
+                allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            } else {
+                allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            }
+            return;
+        }
         if (kind == FSE_STOKESLET) {
             allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
             k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
@@ -835,11 +1120,23 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
-            allow_smem(k_ypass<EV, true>, sm);
             const int ntz = (Dh + u - 1) / u;
-            k_ypass<EV, true><<<static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz),
-                                kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u, B,
-                                                     C);
+            const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
+            if constexpr (EV > 0) {
+                if (v2_mask_for<EV>() & 8) {
+                    allow_smem(k_ypass2<EV, true>, sm);
+                    k_ypass2<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
+                                                                  u, B, C);
+                } else {
+                    allow_smem(k_ypass<EV, true>, sm);
+                    k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                                                                 B, C);
+                }
+            } else {
+                allow_smem(k_ypass<EV, true>, sm);
+                k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                                                             B, C);
+            }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
@@ -848,10 +1145,20 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             FftPlan p = h.dev;
             set_buf(p, h, u);
             const size_t sm = smem_bytes(h, u);
-            allow_smem(k_zinv<EV>, sm);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
-            k_zinv<EV><<<static_cast<unsigned>((npairs + u - 1) / u), kThreads, sm, L.s>>>(
-                p, d_tw, Mt, nx, ncomp, u, B, W);
+            const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
+            if constexpr (EV > 0) {
+                if (v2_mask_for<EV>() & 16) {
+                    allow_smem(k_zinv2<EV>, sm);
+                    k_zinv2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                } else {
+                    allow_smem(k_zinv<EV>, sm);
+                    k_zinv<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                }
+            } else {
+                allow_smem(k_zinv<EV>, sm);
+                k_zinv<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+            }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
