@@ -686,6 +686,13 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
         return spec_row(blk, comp, i - blk * g.nxs, kyl, A, g.nxs, g.nkys, Dh) + kz0;
     };
     // forward x-FFT of the A components (pass 1 straight from global memory)
+    // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (one exp per q per CTA
+    // instead of one per element): rem = ex[kx] * ex[ky] * ex[kz]
+    double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
+    for (int q = threadIdx.x; q < D; q += blockDim.x) {
+        const double kq = kax(q, D, g.dk);
+        ex[q] = exp(-(1.0 - g.eta) * (kq * kq) * g.inv4xi2);
+    }
     freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
         return n < Mt ? Cb[crow(comp, n) + c] : make_double2(0.0, 0.0);
@@ -696,13 +703,14 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
     // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
     // Hermitian average (see k_kscale.cu), 1/D^3 folded in
     const int half = D / 2;
+    const double ex_y = ex[ky];
     for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
         const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
         const int kz = kz0 + c;
         double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
         const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
                                     __dmul_rn(k[2], k[2]));
-        const double rem = exp(-(1.0 - g.eta) * k2 * g.inv4xi2);
+        const double rem = ex[kx] * ex_y * ex[kz];
         const double gval = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz);
         double2 gh[A];
 #pragma unroll
@@ -1073,7 +1081,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     const int u = std::min(units_fit(h, A, gcol), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
-    const size_t sm = smem_bytes(h, A * u) + gcol * u;
+    const size_t sm = smem_bytes(h, A * u) + gcol * u + (gcol ? 0 : sizeof(double) * D);
     const int ntz = (Dh + u - 1) / u;
     const unsigned blocks = static_cast<unsigned>(g.nky) * ntz;
     if (blocks == 0) return;
