@@ -322,21 +322,24 @@ __global__ void __launch_bounds__(TPB) k_realspace(
         // accepted pairs in ascending source order, one 128-bit mask per lane
         // (a single loop over all four words balances the lanes better than
         // a loop per word)
-        uint64_t lo = mask[0] | (static_cast<uint64_t>(mask[1]) << 32);
-        uint64_t hi = mask[2] | (static_cast<uint64_t>(mask[3]) << 32);
         if (valid) {
             ncand += cnt;
-            npair += __popcll(lo) + __popcll(hi);
+            npair += __popc(mask[0]) + __popc(mask[1]) + __popc(mask[2]) + __popc(mask[3]);
         }
-        while (lo | hi) {
-            int j;
-            if (lo) {
-                j = __ffsll(static_cast<long long>(lo)) - 1;
-                lo &= lo - 1;
-            } else {
-                j = 63 + __ffsll(static_cast<long long>(hi));
-                hi &= hi - 1;
+        // the four words as a shift register: m0 is the current word
+        uint32_t m0 = mask[0], m1 = mask[1], m2 = mask[2], m3 = mask[3];
+        int wbase = 0;
+        while (true) {
+            while (m0 == 0u && (m1 | m2 | m3)) {
+                m0 = m1;
+                m1 = m2;
+                m2 = m3;
+                m3 = 0u;
+                wbase += 32;
             }
+            if (m0 == 0u) break;
+            const int j = wbase + __ffs(m0) - 1;
+            m0 &= m0 - 1u;
             const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
             pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tabx, acc);
         }
