@@ -95,6 +95,13 @@ uint64_t fse_cuda_launch_count(const fse_cuda_ctx* ctx);
  * [2] spread kernel [3] forward FFTs [4] k-space scale [5] inverse FFTs [6] target prep
  * [7] gather kernel [8] real-space binning [9] real-space pair kernel [10] whole call */
 fse_status fse_cuda_kernel_ms(fse_cuda_ctx* ctx, double* out, int n);
+/* fse::freespace_solve (greens.hpp:76, greens.cpp:115-139): rhs and out are
+ * M~^3 host arrays [i][j][k] on the green's grid (M~ = green Mtilde); the free-space
+ * convolution of rhs with the green's kernel (harmonic: 1/r, biharmonic: r),
+ * unscaled by h^3 as in the reference. */
+fse_status fse_cuda_freespace_solve(fse_cuda_ctx* ctx, const fse_green* green, const double* rhs,
+                                    double* out);
+
 /* ---- z-slab decomposition over several GPUs (no reference counterpart:
  * the reference is single-process).  Slab `rank` of `nslabs` owns the x-planes
  * [x_lo, x_lo + nx) of the M~ grid and the ky rows [ky_lo, ky_lo + nky) of the

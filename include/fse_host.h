@@ -31,6 +31,32 @@ enum {
 int fse_generate_workload(int which, int64_t n, uint64_t seed, double* pos, double* str,
                           double* tgt);
 
+/* ---- closed-form truncation-error estimates and parameter selection (host scalar
+ * math).  Replace fse::fourier_error_estimate, real_error_estimate,
+ * error_budget, reference_velocity_rms and select_parameters
+ * (/root/reference/proj/include/fse/estimates.hpp:11-40, estimates.cpp:13-126).
+ * Status codes as in fse_cuda.h (FSE_EINVAL = std::invalid_argument). */
+#include "fse_cuda.h"
+
+typedef struct {
+    int kind;
+    double xi, rc, k_inf, L, R;
+    double Q;                      /* sum of squared strength components */
+    double predicted_real_rms;
+    double predicted_fourier_rms;
+} fse_error_budget_t;
+
+fse_status fse_fourier_error_estimate(int kind, double Q, double xi, double k_inf, double L,
+                                      double R, double* out);
+fse_status fse_real_error_estimate(int kind, double Q, double xi, double rc, double L,
+                                   double* out);
+fse_status fse_error_budget(int kind, const fse_config* cfg, double Q, fse_error_budget_t* out);
+fse_status fse_reference_velocity_rms(int kind, double Q, double L, uint64_t N, double* out);
+/* smallest rc and even M meeting the relative RMS tolerance; *feasible = 0 when the
+ * real-space budget needs rc > L sqrt(3) (direct summation recommended) */
+fse_status fse_select_parameters(int kind, uint64_t N, double L, double Q, double xi, double tol,
+                                 fse_config* out, int* feasible);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,8 @@ from .api import (CellList, Context, DomainError, EwaldConfig, FseError, FseRunt
                   fourier_sum, generate_system, generate_workload, green_kind_for, kspace_scale,
                   library_path, load_mollified_green, make_config, precompute_mollified_green,
                   real_space_sum, rms_error, save_mollified_green, self_interaction, spread,
-                  strength_arity, strength_quadratic_sum, total_sum)
+                  strength_arity, strength_quadratic_sum, total_sum, ErrorBudget,
+                  error_budget, fourier_error_estimate, real_error_estimate,
+                  reference_velocity_rms, select_parameters, freespace_solve)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

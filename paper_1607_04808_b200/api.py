@@ -104,6 +104,54 @@ class StageTimings(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ErrorBudget(C.Structure):
+    """fse::ErrorBudget (estimates.hpp:11-17): predicted RMS truncation errors."""
+    _fields_ = [("kind", C.c_int), ("xi", C.c_double), ("rc", C.c_double),
+                ("k_inf", C.c_double), ("L", C.c_double), ("R", C.c_double), ("Q", C.c_double),
+                ("predicted_real_rms", C.c_double), ("predicted_fourier_rms", C.c_double)]
+
+
+def _est(fn, *args):
+    v = C.c_double()
+    st = fn(*args, C.byref(v))
+    if st != 0:
+        _raise(st, f"{fn.__name__}: bad arguments")
+    return v.value
+
+
+def fourier_error_estimate(kind, Q, xi, k_inf, L, R) -> float:  # estimates.cpp:14-29
+    return _est(_load().fse_fourier_error_estimate, int(kind), float(Q), float(xi),
+                float(k_inf), float(L), float(R))
+
+
+def real_error_estimate(kind, Q, xi, rc, L) -> float:  # estimates.cpp:31-47
+    return _est(_load().fse_real_error_estimate, int(kind), float(Q), float(xi), float(rc),
+                float(L))
+
+
+def reference_velocity_rms(kind, Q, L, N) -> float:  # estimates.cpp:64-79
+    return _est(_load().fse_reference_velocity_rms, int(kind), float(Q), float(L), int(N))
+
+
+def error_budget(kind, cfg, Q) -> ErrorBudget:  # estimates.cpp:49-62
+    b = ErrorBudget()
+    st = _load().fse_error_budget(int(kind), C.byref(cfg), float(Q), C.byref(b))
+    if st != 0:
+        _raise(st, "error_budget: bad arguments")
+    return b
+
+
+def select_parameters(kind, N, L, Q, xi, tol):  # estimates.cpp:81-126
+    """-> (EwaldConfig, feasible)"""
+    cfg = EwaldConfig()
+    feas = C.c_int()
+    st = _load().fse_select_parameters(int(kind), int(N), float(L), float(Q), float(xi),
+                                       float(tol), C.byref(cfg), C.byref(feas))
+    if st != 0:
+        _raise(st, "select_parameters: bad arguments or no feasible grid size")
+    return cfg, bool(feas.value)
+
+
 class SlabInfo(C.Structure):
     """fse_slab_info (include/fse_cuda.h): this rank's part of the z-slab decomposition."""
     _fields_ = [("x_lo", C.c_int), ("nx", C.c_int), ("nxs", C.c_int), ("ky_lo", C.c_int),
@@ -230,6 +278,7 @@ def _load():
         lib.fse_cuda_kernel_ms.argtypes = [vp, _dp, C.c_int]
         lib.fse_cuda_fp64_peak.argtypes = [vp, _dp]
         lib.fse_cuda_set_overlap.argtypes = [vp, C.c_int]
+        lib.fse_cuda_freespace_solve.argtypes = [vp, vp, _dp, _dp]
         lib.fse_cuda_slab_info.argtypes = [C.POINTER(EwaldConfig), C.c_int, C.c_int, C.c_int,
                                            C.POINTER(SlabInfo)]
         lib.fse_cuda_slab_forward.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
@@ -239,6 +288,17 @@ def _load():
         lib.fse_cuda_slab_inverse.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
                                               vp, C.c_int, C.c_int, vp, i64, C.c_int, vp]
         lib.fse_cuda_realspace_counts.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        lib.fse_fourier_error_estimate.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double,
+                                                   C.c_double, C.c_double, _dp]
+        lib.fse_real_error_estimate.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double,
+                                                C.c_double, _dp]
+        lib.fse_error_budget.argtypes = [C.c_int, C.POINTER(EwaldConfig), C.c_double,
+                                         C.POINTER(ErrorBudget)]
+        lib.fse_reference_velocity_rms.argtypes = [C.c_int, C.c_double, C.c_double, C.c_uint64,
+                                                   _dp]
+        lib.fse_select_parameters.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_double,
+                                              C.c_double, C.c_double, C.POINTER(EwaldConfig),
+                                              C.POINTER(C.c_int)]
         lib.fse_generate_system.argtypes = [C.c_int, i64, C.c_double, C.c_uint64, _dp, _dp]
         lib.fse_generate_workload.argtypes = [C.c_int, i64, C.c_uint64, _dp, _dp, _dp]
         _lib = lib
@@ -419,6 +479,16 @@ class Context:
                    int(targets_are_sources), green.handle, C.c_void_p(d_u),
                    C.byref(timings) if timings is not None else None)
 
+    def freespace_solve(self, green: MollifiedGreen, rhs) -> np.ndarray:
+        """fse::freespace_solve (greens.cpp:115-139): rhs (M~, M~, M~) on the green's grid."""
+        M = green.Mtilde
+        r = _f64(rhs)
+        if r.shape != (M, M, M):
+            raise InvalidArgument("freespace_solve: rhs extents must match green")
+        out = np.empty((M, M, M))
+        self._call(_load().fse_cuda_freespace_solve, green.handle, _p(r), _p(out))
+        return out
+
     # -- z-slab decomposition (device pointers; see fse_cuda_slab_* and slabs.py)
     def slab_forward(self, cfg, kind, d_pos, d_str, n, rank, nslabs, d_spec):
         self._call(_load().fse_cuda_slab_forward, C.byref(cfg), int(kind), C.c_void_p(d_pos),
@@ -584,6 +654,10 @@ def total_sum(system, kind, cfg, targets, green, timings=None):
 
 def real_space_sum(system, kind, xi, rc, targets):
     return default_context().real_space_sum(system, kind, xi, rc, targets)
+
+
+def freespace_solve(green, rhs):  # greens.hpp:76
+    return green._ctx.freespace_solve(green, rhs)
 
 
 def build_cell_list(system, rc, domain_pad=0.0):

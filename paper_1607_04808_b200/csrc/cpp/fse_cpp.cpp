@@ -19,12 +19,14 @@
 #include <string>
 #include <vector>
 
+#include "fse/estimates.hpp"
 #include "fse/ewald.hpp"
 #include "fse/fft.hpp"
 #include "fse/greens.hpp"
 #include "fse/kernels.hpp"
 #include "fse/realspace.hpp"
 #include "fse_cuda.h"
+#include "fse_host.h"
 
 static_assert(sizeof(fse::EwaldConfig) == sizeof(fse_config), "EwaldConfig <-> fse_config");
 static_assert(offsetof(fse::EwaldConfig, Mtilde) == offsetof(fse_config, Mtilde), "layout");
@@ -107,6 +109,58 @@ EwaldConfig make_config(double L, double xi, double rc, int M, int P, double sf)
         fse_make_config(L, xi, rc, M, P, sf, reinterpret_cast<fse_config*>(&c), err, sizeof err);
     if (st != FSE_OK) detail::raise(st, err);
     return c;
+}
+
+// ------------------------------------------------------------------ estimates.hpp
+double fourier_error_estimate(KernelKind kind, double Q, double xi, double k_inf, double L,
+                              double R) {
+    double v = 0;
+    const fse_status st = fse_fourier_error_estimate(static_cast<int>(kind), Q, xi, k_inf, L, R, &v);
+    if (st != FSE_OK) detail::raise(st, "fourier_error_estimate: bad arguments");
+    return v;
+}
+
+double real_error_estimate(KernelKind kind, double Q, double xi, double rc, double L) {
+    double v = 0;
+    const fse_status st = fse_real_error_estimate(static_cast<int>(kind), Q, xi, rc, L, &v);
+    if (st != FSE_OK) detail::raise(st, "real_error_estimate: bad arguments");
+    return v;
+}
+
+ErrorBudget error_budget(KernelKind kind, const EwaldConfig& cfg, double Q) {
+    fse_error_budget_t b;
+    const fse_status st = fse_error_budget(static_cast<int>(kind), detail::cfg_of(cfg), Q, &b);
+    if (st != FSE_OK) detail::raise(st, "error_budget: bad arguments");
+    ErrorBudget out;
+    out.kind = kind;
+    out.xi = b.xi;
+    out.rc = b.rc;
+    out.k_inf = b.k_inf;
+    out.L = b.L;
+    out.R = b.R;
+    out.Q = b.Q;
+    out.predicted_real_rms = b.predicted_real_rms;
+    out.predicted_fourier_rms = b.predicted_fourier_rms;
+    return out;
+}
+
+double reference_velocity_rms(KernelKind kind, double Q, double L, std::size_t N) {
+    double v = 0;
+    const fse_status st = fse_reference_velocity_rms(static_cast<int>(kind), Q, L, N, &v);
+    if (st != FSE_OK) detail::raise(st, "reference_velocity_rms: bad arguments");
+    return v;
+}
+
+SelectedParameters select_parameters(KernelKind kind, std::size_t N, double L, double Q,
+                                     double xi, double tol) {
+    SelectedParameters sel;
+    int feasible = 1;
+    const fse_status st = fse_select_parameters(static_cast<int>(kind), N, L, Q, xi, tol,
+                                                reinterpret_cast<fse_config*>(&sel.config),
+                                                &feasible);
+    if (st != FSE_OK) detail::raise(st, "select_parameters: bad arguments");
+    sel.feasible = feasible != 0;
+    return sel;
 }
 
 // ------------------------------------------------------------------ kernels.hpp
@@ -218,6 +272,21 @@ MollifiedGreen precompute_mollified_green(GreenKind kind, double Ltilde, int Mti
     check(fse_cuda_green_download(ctx(), dg->h, g.fourier.data()));
     g.device = dg;
     return g;
+}
+
+ScalarGrid freespace_solve(const MollifiedGreen& green, const ScalarGrid& rhs) {  // greens.cpp:115-139
+    const int M = green.Mtilde;
+    if (rhs.extents[0] != M || rhs.extents[1] != M || rhs.extents[2] != M ||
+        rhs.values.size() != rhs.size())
+        throw std::invalid_argument("freespace_solve: rhs extents must match green");
+    ScalarGrid out;
+    out.extents[0] = out.extents[1] = out.extents[2] = M;
+    out.h = green.h;
+    out.origin = rhs.origin;
+    out.values.resize(rhs.size());
+    check(fse_cuda_freespace_solve(ctx(), detail::device_green(green), rhs.values.data(),
+                                   out.values.data()));
+    return out;
 }
 
 void save_mollified_green(const MollifiedGreen& green, const std::string& path) {

@@ -913,6 +913,45 @@ fse_status fse_cuda_green_download(fse_cuda_ctx* c, const fse_green* g, double* 
     });
 }
 
+// fse::freespace_solve (greens.cpp:115-139): zero-pad the M~^3 right-hand side
+// to D^3, multiply its transform by the Green's table, transform back and keep
+// the M~^3 window -- the hot path's pruned FFT passes with one component and
+// the scalar multiplier (G / D^3; G is real and even, so the real-to-complex
+// transforms are exact).
+fse_status fse_cuda_freespace_solve(fse_cuda_ctx* c, const fse_green* green, const double* rhs,
+                                    double* out) {
+    return api(c, [&] {
+        if (!green || !rhs || !out) invalid("null pointer");
+        if (green->device != c->device) invalid("green lives on another device");
+        GridParams g{};
+        g.Mt = green->Mtilde;
+        g.D = 2 * g.Mt;
+        g.Dh = g.D / 2 + 1;
+        g.P = 2;
+        g.rowp = g.Mt;
+        g.plane = static_cast<int64_t>(g.Mt) * g.Mt;
+        g.comp = static_cast<int64_t>(g.Mt) * g.plane;
+        g.h = green->h;
+        g.dk = M_PI / green->Ltilde;
+        g.invD3 = 1.0 / (static_cast<double>(g.D) * g.D * g.D);  // fft.cpp:34
+        g.x_lo = 0;
+        g.nx = g.nxs = g.Mt;
+        g.ky_lo = 0;
+        g.nky = g.nkys = g.D;
+        const size_t vol = static_cast<size_t>(g.comp);
+        double* R = buf<double>(c, "R", vol);
+        double2* Bs = buf<double2>(c, "B", static_cast<size_t>(g.Mt) * g.Mt * g.Dh);
+        double2* Cs = buf<double2>(c, "C", static_cast<size_t>(g.Mt) * g.D * g.Dh);
+        FSE_CU(cudaMemcpyAsync(R, rhs, vol * sizeof(double), cudaMemcpyHostToDevice, c->s0));
+        const FftPlanDev& fp = fft_plan(c, g.D);
+        Launch L = L0(c);
+        launch_fft_forward_zy(L, fp.host, fp.tw, g, 1, R, Bs, Cs);
+        launch_fft_xscale(L, fp.host, fp.tw, g, KIND_SCALAR_X, green->d_half, Cs);
+        launch_fft_inverse_yz(L, fp.host, fp.tw, g, 1, Cs, Bs, R, 1);
+        d2h(c, out, R, vol * sizeof(double));
+    });
+}
+
 fse_status fse_cuda_green_info(const fse_green* g, int* kind, double* Ltilde, double* h,
                                double* R, int* Mtilde) {
     if (!g) return FSE_EINVAL;

@@ -368,6 +368,14 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
 }
 
 // ------------------------------------------------------------------ x pass + scale
+// KIND_SCALAR: fse::freespace_solve (greens.cpp:115-139): one component,
+// multiplied by the (real, even) Green's table only.
+constexpr int KIND_SCALAR = 3;
+template <int KIND>
+constexpr int arity_k() { return KIND == FSE_STRESSLET ? 9 : (KIND == KIND_SCALAR ? 1 : 3); }
+template <int KIND>
+constexpr int nout_k() { return KIND == KIND_SCALAR ? 1 : 3; }
+
 template <int KIND>
 __device__ __forceinline__ void apply(const double k[3], double k2, double gval, double rem,
                                       double inv4xi2, const double2* g, double2* out) {
@@ -405,6 +413,8 @@ __device__ __forceinline__ void apply(const double k[3], double k2, double gval,
             const double vi = k2 * (ai[p] + bi[p] + k[p] * tri) - 2.0 * k[p] * kgki;
             out[p] = make_double2(b * vi, -b * vr);
         }
+    } else if (KIND == KIND_SCALAR) {
+        out[0] = make_double2(gval * g[0].x, gval * g[0].y);
     } else {
         const double cm = -gval * rem;
         const double vr[3] = {g[1].x * k[2] - g[2].x * k[1], g[2].x * k[0] - g[0].x * k[2],
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
                                                    GridParams g, int ncol,
                                                    const double* __restrict__ G,
                                                    double2* __restrict__ Cb) {
-    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         for (int q = 0; q < A; ++q) gh[q] = r[cidx<ENG>(q * nc + c, kx, D)];
         double2 out[3];
         apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
-        if (kx == half || ky == half || kz == half) {
+        if (KIND != KIND_SCALAR && (kx == half || ky == half || kz == half)) {
             if (kx == half) k[0] = -k[0];
             if (ky == half) k[1] = -k[1];
             if (kz == half) k[2] = -k[2];
@@ -490,13 +500,13 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
                 out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
         }
 #pragma unroll
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < NO; ++p)
             r[cidx<ENG>(p * nc + c, kx, D)] = make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
     }
     __syncthreads();
     double2* other = (r == a) ? sb : a;
-    double2* r2 = fft_cols<ENG>(r, other, 3 * nc, pl, tw, +1);
-    for (int comp = 0; comp < 3; ++comp) {
+    double2* r2 = fft_cols<ENG>(r, other, NO * nc, pl, tw, +1);
+    for (int comp = 0; comp < NO; ++comp) {
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;
             Cb[crow(comp, i) + c] = r2[cidx<ENG>(comp * nc + c, i, D)];
@@ -667,7 +677,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
                                                     double2* __restrict__ Cb) {
-    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
     const double2* tw = stage_twiddles(a, pl, tw_g);
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
         for (int q = 0; q < A; ++q) gh[q] = a[freg::ridx<D1, D2>(q * nc + c, kx)];
         double2 out[3];
         apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
-        if (kx == half || ky == half || kz == half) {
+        if (KIND != KIND_SCALAR && (kx == half || ky == half || kz == half)) {
             if (kx == half) k[0] = -k[0];
             if (ky == half) k[1] = -k[1];
             if (kz == half) k[2] = -k[2];
@@ -728,17 +738,17 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
                 out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
         }
 #pragma unroll
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < NO; ++p)
             a[freg::ridx<D1, D2>(p * nc + c, kx)] =
                 make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
     }
     __syncthreads();
     // inverse x-FFT of the 3 results (pass 1 in place from shared memory:
     // every item reads and writes only its own (column, n2) elements)
-    freg::pass1<D1, D2, true, D1>(a, 3 * nc, +1, tw, tab,
+    freg::pass1<D1, D2, true, D1>(a, NO * nc, +1, tw, tab,
                                   [&](int col, int n) { return a[freg::ridx<D1, D2>(col, n)]; });
     __syncthreads();
-    freg::pass2<D1, D2, true, D2 / 2>(a, 3 * nc, +1, tab, [&](int col, int k, double2 v) {
+    freg::pass2<D1, D2, true, D2 / 2>(a, NO * nc, +1, tab, [&](int col, int k, double2 v) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
         Cb[crow(comp, k) + c] = v;  // k < Mt by NOUT2
     });
@@ -1072,7 +1082,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                        const GridParams& g, int kind, const double* G, double2* C) {
     upload_consts();
-    const int A = arity_of(kind);
+    const int A = kind == KIND_SCALAR ? 1 : arity_of(kind);
     const int D = h.dev.D, Dh = D / 2 + 1;
     // v2 (register engines) reads G from global memory; v1 stages it
     int xmask = 0;
@@ -1094,6 +1104,9 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
             } else if (kind == FSE_STRESSLET) {
                 allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
                 k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            } else if (kind == KIND_SCALAR) {
+                allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
             } else {
                 allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
                 k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
@@ -1106,6 +1119,9 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
         } else if (kind == FSE_STRESSLET) {
             allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
             k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+        } else if (kind == KIND_SCALAR) {
+            allow_smem(k_xscale<EV, KIND_SCALAR>, sm);
+            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
         } else {
             allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
             k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
@@ -1116,9 +1132,10 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
 }
 
 void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
-                           const GridParams& g, int A, double2* C, double2* B, double* W) {
+                           const GridParams& g, int A, double2* C, double2* B, double* W,
+                           int ncomp) {
     upload_consts();
-    const int Mt = g.Mt, nx = g.nx, ncomp = 3;
+    const int Mt = g.Mt, nx = g.nx;
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     if (nx <= 0) return;  // empty slab
     with_engine(h.eng, [&](auto E) {

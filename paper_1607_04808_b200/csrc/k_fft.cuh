@@ -72,6 +72,9 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
                        const GridParams& g, int kind, const double* G, double2* C);
 // C (send layout, 3 comps in blocks of A) -> B (j < Mt) -> W (3 x nx x Mt^2 real)
 void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
-                           const GridParams& g, int A, double2* C, double2* B, double* W);
+                           const GridParams& g, int A, double2* C, double2* B, double* W,
+                           int ncomp = 3);
+// x-pass multiplier kind of fse::freespace_solve (one component, times G only)
+constexpr int KIND_SCALAR_X = 3;
 
 }  // namespace fsecu
