@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "fse/estimates.hpp"
 #include "fse/ewald.hpp"
 #include "fse/greens.hpp"
 #include "fse/kernels.hpp"
@@ -135,6 +136,57 @@ int main() {
             direct_sum(two, KernelKind::Stokeslet, two.positions, true);
         } catch (const std::domain_error&) { ok = true; }
         report(ok, "coincident points -> std::domain_error");
+    }
+    // estimates.hpp: the criterion-2 workload selection (test_estimates.cpp:84-93) and
+    // the selected configuration meeting its own budget
+    {
+        SourceSystem s = make_system(KernelKind::Stokeslet, 20000, 2.0, 2026);
+        double Q = 0;
+        for (const auto& f : s.strengths)
+            for (int k = 0; k < f.arity; ++k) Q += f.c[k] * f.c[k];
+        SelectedParameters sel = select_parameters(KernelKind::Stokeslet, 20000, 2.0, Q, 7.0, 0.5e-8);
+        ErrorBudget b = error_budget(KernelKind::Stokeslet, sel.config, Q);
+        const double ref = reference_velocity_rms(KernelKind::Stokeslet, Q, 2.0, 20000);
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "select_parameters: M=%d P=%d rc=%.4f real %.2e fourier %.2e",
+                      sel.config.M, sel.config.P, sel.config.rc, b.predicted_real_rms,
+                      b.predicted_fourier_rms);
+        report(sel.feasible && sel.config.P == 16 && sel.config.M % 2 == 0 &&
+                   b.predicted_real_rms <= 0.25 * 0.5e-8 * ref * (1 + 1e-12) &&
+                   b.predicted_fourier_rms <= 0.25 * 0.5e-8 * ref * (1 + 1e-12),
+               buf);
+    }
+    // greens.hpp freespace_solve: Gaussian Poisson oracle (test_greens.cpp:117-120)
+    {
+        const int M = 48;
+        const double a = 200.0;
+        MollifiedGreen g = precompute_mollified_green(GreenKind::Harmonic, 1.0, M,
+                                                      1.0 + std::sqrt(3.0));
+        ScalarGrid rhs;
+        rhs.extents[0] = rhs.extents[1] = rhs.extents[2] = M;
+        rhs.h = 1.0 / M;
+        rhs.values.resize(rhs.size());
+        const double pref = std::pow(a / M_PI, 1.5);
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < M; ++j)
+                for (int k = 0; k < M; ++k) {
+                    const double x = i * rhs.h - 0.5, y = j * rhs.h - 0.5, z = k * rhs.h - 0.5;
+                    rhs.at(i, j, k) = pref * std::exp(-a * (x * x + y * y + z * z));
+                }
+        ScalarGrid phi = freespace_solve(g, rhs);
+        double err = 0, mx = 0;
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < M; ++j)
+                for (int k = 0; k < M; ++k) {
+                    const double x = i * rhs.h - 0.5, y = j * rhs.h - 0.5, z = k * rhs.h - 0.5;
+                    const double r = std::sqrt(x * x + y * y + z * z);
+                    const double ex = r < 1e-12 ? 2.0 * std::sqrt(a / M_PI) : std::erf(std::sqrt(a) * r) / r;
+                    err = std::max(err, std::abs(phi.at(i, j, k) - ex));
+                    mx = std::max(mx, std::abs(ex));
+                }
+        char buf[120];
+        std::snprintf(buf, sizeof buf, "freespace_solve Gaussian oracle: %.2e < 1e-10", err / mx);
+        report(err / mx < 1e-10, buf);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
     return failures ? 1 : 0;
