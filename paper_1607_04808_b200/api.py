@@ -32,7 +32,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfse_b200.so")
+# FSE_LIB_PATH: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FSE_LIB_PATH") or os.path.join(_HERE, "libfse_b200.so")
 
 
 class FseError(Exception):

@@ -36,6 +36,10 @@ namespace {
 constexpr int SW = 4;      // warps per CTA
 constexpr int MAXT = 32;   // targets per item
 constexpr int RS = 34;     // slab row stride (doubles): 32 + 2 keeps A-fragment loads at 2 wavefronts
+#ifndef FSE_GATHER_NST
+#define FSE_GATHER_NST 2
+#endif
+constexpr int NST = FSE_GATHER_NST;  // slab buffers (cp.async pipeline depth)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -114,21 +118,22 @@ __device__ void gather_item(const GridParams& g, const double* __restrict__ X, d
     // planes of the union box inside this rank's slab (all of them on one GPU);
     // with several slabs every rank adds its planes' share of the sum
     const int xs0 = max(0, g.x_lo - x0), xs1 = min(NX, g.x_lo + g.nx - x0);
-    if (xs0 < xs1) {
-        stage_slab<KS>(g, X, x0 + xs0, y0, z0, NY, NZ, vec16, slab + (xs0 & 1) * buf_elems);
+    // NST-stage cp.async pipeline: slab xs + NST - 1 is in flight while xs is used
+#pragma unroll
+    for (int st = 0; st < NST - 1; ++st) {
+        if (xs0 + st < xs1)
+            stage_slab<KS>(g, X, x0 + xs0 + st, y0, z0, NY, NZ, vec16,
+                           slab + ((xs0 + st) % NST) * buf_elems);
         cp_commit();
     }
     for (int xs = xs0; xs < xs1; ++xs) {
-        if (xs + 1 < xs1) {
-            stage_slab<KS>(g, X, x0 + xs + 1, y0, z0, NY, NZ, vec16,
-                           slab + ((xs + 1) & 1) * buf_elems);
-            cp_commit();
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
+        if (xs + NST - 1 < xs1)
+            stage_slab<KS>(g, X, x0 + xs + NST - 1, y0, z0, NY, NZ, vec16,
+                           slab + ((xs + NST - 1) % NST) * buf_elems);
+        cp_commit();
+        cp_wait<NST - 1>();
         __syncthreads();
-        const double* A = slab + (xs & 1) * buf_elems + rbase * RS + (lane & 3);
+        const double* A = slab + (xs % NST) * buf_elems + rbase * RS + (lane & 3);
         double wxt[NT];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) wxt[nt] = wxs[xs * MAXT + 8 * nt + tb];
@@ -160,7 +165,7 @@ __device__ void gather_item(const GridParams& g, const double* __restrict__ X, d
 }
 
 template <int MT, int KS>
-__global__ void __launch_bounds__(SW * 32, 3) k_gather_mma(
+__global__ void __launch_bounds__(SW * 32, NST == 2 ? 3 : 2) k_gather_mma(
     GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
     const int32_t* __restrict__ nitems_dev, const double* __restrict__ X,
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_mma(
     if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // CTA-uniform
     constexpr int ROWS = 8 * MT * SW;
     double* slab = gsm;                    // [2][ROWS][RS]
-    double* wxs = slab + 2 * ROWS * RS;    // [nx][MAXT]
+    double* wxs = slab + NST * ROWS * RS;  // [nx][MAXT]
     double* b0s = wxs + 32 * MAXT;         // [KS][4][32] B fragments (wz)
     const int e = items[2 * blockIdx.x], bi = items[2 * blockIdx.x + 1];
     const int c = e >> 1, h = e & 1;
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_mma(
         tinfo[tid] = ti;
     }
     // pad rows of both slab buffers stay zero
-    for (int idx = tid; idx < 2 * ROWS * RS; idx += SW * 32) {
+    for (int idx = tid; idx < NST * ROWS * RS; idx += SW * 32) {
         const int r = (idx / RS) % ROWS;
         if (r >= 3 * NY) slab[idx] = 0.0;
     }
@@ -269,7 +274,7 @@ int mt_for(int P) { return (3 * (P + 7) + 8 * SW - 1) / (8 * SW); }
 
 size_t slab_smem_bytes(const GridParams& g) {
     const int rows = 8 * mt_for(g.P) * SW;
-    return sizeof(double) * (2 * static_cast<size_t>(rows) * RS + 32 * MAXT + 8 * 4 * 32);
+    return sizeof(double) * (NST * static_cast<size_t>(rows) * RS + 32 * MAXT + 8 * 4 * 32);
 }
 
 bool gather_slab_enabled(const GridParams& g) {
