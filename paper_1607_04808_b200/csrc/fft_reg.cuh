@@ -140,7 +140,7 @@ __host__ __device__ constexpr int first_radix(int n) {
 }
 // composite register sizes that own a twiddle table, in table order
 // (only the composite sizes the engines in k_fft.cu use; twid<> static_asserts)
-constexpr int kRegSizes[] = {15, 22, 24, 26, 30, 32, 40};
+constexpr int kRegSizes[] = {15, 20, 22, 24, 26, 30, 32, 40};
 constexpr int kNumRegSizes = sizeof(kRegSizes) / sizeof(int);
 __host__ __device__ constexpr int tw_off_of(int n) {
     int off = 0;

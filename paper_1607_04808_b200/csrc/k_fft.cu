@@ -30,6 +30,7 @@
 // Twiddles come from host tables computed in long double, staged in shared
 // memory per CTA.
 #include <cmath>
+#include <complex>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -160,26 +161,49 @@ __device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int nco
     return cur;
 }
 
-// engine table: ENG -> (D1, D2)
+// engine table: ENG -> (D1, D2).  BLUE engines evaluate a length-N transform
+// (N = pl.D, with a prime factor the register DFTs lack, e.g. 298 = 2 x 149)
+// by Bluestein's chirp-z identity nk = (n^2 + k^2 - (k - n)^2) / 2 as a
+// circular convolution of length Mb = D1 D2 >= 2N - 1 on the register engine.
 template <int ENG>
 struct Eng {
     static constexpr int D1 = 1, D2 = 1;
+    static constexpr bool BLUE = false;
 };
 template <>
 struct Eng<1> {
     static constexpr int D1 = 24, D2 = 26;
+    static constexpr bool BLUE = false;
 };
 template <>
 struct Eng<2> {
     static constexpr int D1 = 30, D2 = 40;
+    static constexpr bool BLUE = false;
 };
 template <>
 struct Eng<3> {
     static constexpr int D1 = 22, D2 = 32;
+    static constexpr bool BLUE = false;
 };
 template <>
 struct Eng<4> {
     static constexpr int D1 = 11, D2 = 22;
+    static constexpr bool BLUE = false;
+};
+template <>
+struct Eng<5> {  // Bluestein, Mb = 400: N <= 200 (cfg1: 194 = 2 x 97)
+    static constexpr int D1 = 20, D2 = 20;
+    static constexpr bool BLUE = true;
+};
+template <>
+struct Eng<6> {  // Bluestein, Mb = 624: N <= 312 (cfg3: 298 = 2 x 149)
+    static constexpr int D1 = 24, D2 = 26;
+    static constexpr bool BLUE = true;
+};
+template <>
+struct Eng<7> {  // Bluestein, Mb = 1024: N <= 512
+    static constexpr int D1 = 32, D2 = 32;
+    static constexpr bool BLUE = true;
 };
 
 template <int ENG>
@@ -187,9 +211,47 @@ __device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, c
                                              const double2* __restrict__ tw, int sgn) {
     if constexpr (ENG == 0) {
         return fft_stockham(a, b, ncol, pl, tw, sgn);
-    } else {
+    } else if constexpr (!Eng<ENG>::BLUE) {
         constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2;
         freg::fft_cols_2l<D1, D2>(a, ncol, sgn, tw, tw + D1 * D2);
+        return a;
+    } else {
+        // Bluestein: X_k = w_k sum_n (x_n w_n) conj(w_{k-n}), w_n = e^{-i pi n^2 / N}
+        // (conjugated for the inverse); the convolution with the precomputed
+        // transform Bh of the chirp (1/Mb folded in) runs on the Mb-point engine.
+        constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, Mb = D1 * D2;
+        const int N = pl.D;
+        const double2* tab = tw + Mb;
+        const double2* chirp = tab + freg::tw_total();
+        const double2* bh = chirp + N + (sgn < 0 ? 0 : Mb);
+        for (int e = threadIdx.x; e < ncol * Mb; e += blockDim.x) {
+            const int c = e / Mb, n = e - c * Mb;
+            const int idx = freg::ridx<D1, D2>(c, n);
+            double2 v = make_double2(0.0, 0.0);
+            if (n < N) {
+                double2 w = chirp[n];
+                if (sgn > 0) w.y = -w.y;
+                v = freg::cmul(a[idx], w);
+            }
+            a[idx] = v;
+        }
+        __syncthreads();
+        freg::fft_cols_2l<D1, D2>(a, ncol, -1, tw, tab);
+        for (int e = threadIdx.x; e < ncol * Mb; e += blockDim.x) {
+            const int c = e / Mb, n = e - c * Mb;
+            const int idx = freg::ridx<D1, D2>(c, n);
+            a[idx] = freg::cmul(a[idx], bh[n]);
+        }
+        __syncthreads();
+        freg::fft_cols_2l<D1, D2>(a, ncol, +1, tw, tab);
+        for (int e = threadIdx.x; e < ncol * N; e += blockDim.x) {
+            const int c = e / N, k = e - c * N;
+            const int idx = freg::ridx<D1, D2>(c, k);
+            double2 w = chirp[k];
+            if (sgn > 0) w.y = -w.y;
+            a[idx] = freg::cmul(a[idx], w);
+        }
+        __syncthreads();
         return a;
     }
 }
@@ -834,13 +896,28 @@ int engine_for(int D, int* D1, int* D2) {
         int D, e, d1, d2;
     };
     const E table[] = {{624, 1, 24, 26}, {1200, 2, 30, 40}, {704, 3, 22, 32}, {242, 4, 11, 22}};
-    if (!std::getenv("FSE_FFT_STOCKHAM"))
-        for (const E& t : table)
-            if (t.D == D) {
+    if (std::getenv("FSE_FFT_STOCKHAM")) return 0;
+    for (const E& t : table)
+        if (t.D == D) {
+            *D1 = t.d1;
+            *D2 = t.d2;
+            return t.e;
+        }
+    // a prime factor beyond the register DFTs (2..13): Bluestein on the
+    // smallest register engine with Mb >= 2D - 1 (FSE_FFT_NOBLUE: Stockham's
+    // generic O(p^2) stage instead)
+    int rem = D;
+    for (int p : {2, 3, 5, 7, 11, 13})
+        while (rem % p == 0) rem /= p;
+    if (rem > 1 && !std::getenv("FSE_FFT_NOBLUE")) {
+        const E blue[] = {{400, 5, 20, 20}, {624, 6, 24, 26}, {1024, 7, 32, 32}};
+        for (const E& t : blue)
+            if (t.D >= 2 * D - 1) {
                 *D1 = t.d1;
                 *D2 = t.d2;
                 return t.e;
             }
+    }
     return 0;
 }
 
@@ -866,6 +943,7 @@ int v2_mask_env() {
 }
 template <int ENG>
 int v2_mask_for() {
+    if (Eng<ENG>::BLUE) return 0;
     const int e = v2_mask_env();
     if (e >= 0) return e;
     return ENG == 2 ? 0 : (1 | 2 | 4 | 16);
@@ -881,11 +959,47 @@ HostFftPlan make_fft_plan(int D) {
     h.dev.D = D;
     h.eng = engine_for(D, &h.D1, &h.D2);
     if (h.eng > 0) {
-        // table: W_D^t (t < D), then the small register-FFT tables
-        for (int t = 0; t < D; ++t) h.tw.push_back(cexp_neg(t, D));
+        const int Mb = h.D1 * h.D2;  // = D for the plain register engines
+        // table: W_Mb^t (t < Mb), then the small register-FFT tables
+        for (int t = 0; t < Mb; ++t) h.tw.push_back(cexp_neg(t, Mb));
         for (int i = 0; i < freg::kNumRegSizes; ++i) {
             const int n = freg::kRegSizes[i];
             for (int t = 0; t < n; ++t) h.tw.push_back(cexp_neg(t, n));
+        }
+        if (Mb != D) {
+            // Bluestein: chirp w_n = e^{-i pi n^2 / D} (n^2 reduced mod 2D, long
+            // double), then Bh = FFT_Mb(b) / Mb for b_m = conj(w_|m|) on the
+            // circular support |m| < D, for the forward and the inverse sign
+            h.blue = true;
+            const long double pi = 3.141592653589793238462643383279502884L;
+            auto w = [&](long long n, int sgn) {
+                const long double ang = sgn * pi * static_cast<long double>((n * n) % (2LL * D)) / D;
+                return std::complex<long double>(cosl(ang), sinl(ang));
+            };
+            for (int n = 0; n < D; ++n) {
+                const std::complex<long double> c = w(n, -1);
+                h.tw.push_back(make_double2(static_cast<double>(c.real()),
+                                            static_cast<double>(c.imag())));
+            }
+            for (int sgn : {-1, +1}) {
+                std::vector<std::complex<long double>> b(Mb, 0.0L), B(Mb);
+                for (int m = 0; m < D; ++m) {
+                    b[m] = std::conj(w(m, sgn));
+                    if (m > 0) b[Mb - m] = b[m];
+                }
+                for (int k = 0; k < Mb; ++k) {  // direct DFT in long double (host, once)
+                    std::complex<long double> acc = 0.0L;
+                    for (int m = 0; m < Mb; ++m) {
+                        const long double ang =
+                            -2.0L * pi * static_cast<long double>((static_cast<long long>(k) * m) % Mb) / Mb;
+                        acc += b[m] * std::complex<long double>(cosl(ang), sinl(ang));
+                    }
+                    B[k] = acc / static_cast<long double>(Mb);
+                }
+                for (int k = 0; k < Mb; ++k)
+                    h.tw.push_back(make_double2(static_cast<double>(B[k].real()),
+                                                static_cast<double>(B[k].imag())));
+            }
         }
         h.dev.nst = 0;
         h.dev.dD = make_fdiv(D);
@@ -935,8 +1049,8 @@ HostFftPlan make_fft_plan(int D) {
 namespace {
 
 size_t col_elems(const HostFftPlan& h, int cols) {
-    if (h.eng > 0)  // freg::ridx layout
-        return static_cast<size_t>(cols) * (h.dev.D + h.D1 + 1) + 8;
+    if (h.eng > 0)  // freg::ridx layout (Bluestein: columns of the Mb-point engine)
+        return static_cast<size_t>(cols) * (h.D1 * h.D2 + h.D1 + 1) + 8;
     return static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
 }
 
@@ -997,6 +1111,9 @@ void with_engine(int eng, F&& f) {
         case 2: f(std::integral_constant<int, 2>{}); break;
         case 3: f(std::integral_constant<int, 3>{}); break;
         case 4: f(std::integral_constant<int, 4>{}); break;
+        case 5: f(std::integral_constant<int, 5>{}); break;
+        case 6: f(std::integral_constant<int, 6>{}); break;
+        case 7: f(std::integral_constant<int, 7>{}); break;
         default: f(std::integral_constant<int, 0>{}); break;
     }
 }
@@ -1036,7 +1153,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
-            if constexpr (EV > 0) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 1) {
                     allow_smem(k_zfwd2<EV>, sm);
                     k_zfwd2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
@@ -1058,7 +1175,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             const int ntz = (Dh + u - 1) / u;
             const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
-            if constexpr (EV > 0) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 2) {
                     allow_smem(k_ypass2<EV, false>, sm);
                     k_ypass2<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
@@ -1097,7 +1214,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     if (blocks == 0) return;
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
-        if constexpr (EV > 0) if (v2_mask_for<EV>() & 4) {
+        if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
                 k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
@@ -1147,7 +1264,7 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             const int ntz = (Dh + u - 1) / u;
             const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
-            if constexpr (EV > 0) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 8) {
                     allow_smem(k_ypass2<EV, true>, sm);
                     k_ypass2<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
@@ -1172,7 +1289,7 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             const size_t sm = smem_bytes(h, u);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
-            if constexpr (EV > 0) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 16) {
                     allow_smem(k_zinv2<EV>, sm);
                     k_zinv2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);

@@ -52,6 +52,7 @@ struct HostFftPlan {
     std::vector<int> radices;
     bool generic = false;     // a non-register (generic DFT) stage is present
     int eng = 0;              // 0: shared-memory Stockham; >0: two-level register engine
+    bool blue = false;        // Bluestein over an Mb = D1 D2 register engine (eng 5..7)
     int D1 = 0, D2 = 0;       // D = D1 * D2 for eng > 0
 };
 
