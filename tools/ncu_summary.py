@@ -102,7 +102,7 @@ def full(path):
 
 
 STAGE_OF = {"k_spread": "spread", "k_gather_mma": "gather", "k_realspace": "realspace",
-            "k_xscale": "kscale"}
+            "k_xscale": "kscale", "k_xscale2": "kscale"}
 
 
 def traffic(path):
