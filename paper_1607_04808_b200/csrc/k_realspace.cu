@@ -181,7 +181,7 @@ __device__ __forceinline__ float rel32(double v, double rm) {
 
 template <int A>
 struct WarpChunk {
-    float4 sr[CH];
+    float sxf[CH], syf[CH], szf[CH];  // SoA: two candidates per packed fp32 op
     double sx[CH], sy[CH], sz[CH];
     double sf[CH][A];
     int nb_start[27], nb_pref[28];
@@ -206,7 +206,9 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     auto& sx = wc.sx;
     auto& sy = wc.sy;
     auto& sz = wc.sz;
-    auto& sr = wc.sr;  // fp32 coordinates relative to the cell centre
+    auto& sxf = wc.sxf;  // fp32 coordinates relative to the cell centre
+    auto& syf = wc.syf;
+    auto& szf = wc.szf;
     auto& sf = wc.sf;
     auto& nb_start = wc.nb_start;
     auto& nb_pref = wc.nb_pref;
@@ -291,31 +293,43 @@ __global__ void __launch_bounds__(TPB) k_realspace(
                 sx[slot] = vx;
                 sy[slot] = vy;
                 sz[slot] = vz;
-                sr[slot] = make_float4(rel32(vx - cxc, ft.rm), rel32(vy - cyc, ft.rm),
-                                             rel32(vz - czc, ft.rm), 0.0f);
+                sxf[slot] = rel32(vx - cxc, ft.rm);
+                syf[slot] = rel32(vy - cyc, ft.rm);
+                szf[slot] = rel32(vz - czc, ft.rm);
 #pragma unroll
                 for (int c = 0; c < A; ++c)
                     sf[slot][c] = sfs[static_cast<int64_t>(sidx) * A + c];
+            } else {  // past the last source: never accepted
+                sxf[slot] = syf[slot] = szf[slot] = 3e38f;
             }
         }
         __syncwarp();
         const int cnt = min(CH, total - base);
         uint32_t mask[CH / 32];
+        // two candidates per step with packed fp32 (FFMA2/FMUL2); slots past
+        // cnt hold +3e38 sentinels, so the trip count is fixed
+        const float2 xf2 = make_float2(xf, xf), yf2 = make_float2(yf, yf),
+                     zf2 = make_float2(zf, zf), neg1 = make_float2(-1.0f, -1.0f);
 #pragma unroll
         for (int wd = 0; wd < CH / 32; ++wd) {
             uint32_t m = 0;
-            const int lim = min(32, cnt - wd * 32);
-            for (int b = 0; b < lim; ++b) {
+#pragma unroll 4
+            for (int b = 0; b < 32; b += 2) {
                 const int j = wd * 32 + b;
-                const float4 rr = sr[j];
-                const float dx = xf - rr.x, dy = yf - rr.y, dz = zf - rr.z;
-                const float d2f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                bool pass = d2f <= ft.lo && d2f > ft.z0;
-                if (!pass && !(d2f > ft.hi)) {  // band, near-coincident or NaN: exact test
-                    const double d2 = exact_d2(x - sx[j], y - sy[j], z - sz[j]);
-                    pass = (d2 != 0.0) && !(d2 > rc2);  // realspace.cpp:140
+                const float2 dx = __ffma2_rn(*reinterpret_cast<const float2*>(&sxf[j]), neg1, xf2);
+                const float2 dy = __ffma2_rn(*reinterpret_cast<const float2*>(&syf[j]), neg1, yf2);
+                const float2 dz = __ffma2_rn(*reinterpret_cast<const float2*>(&szf[j]), neg1, zf2);
+                const float2 d2f = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float d = h ? d2f.y : d2f.x;
+                    bool pass = d <= ft.lo && d > ft.z0;
+                    if (!pass && !(d > ft.hi)) {  // band, near-coincident or NaN: exact test
+                        const double d2 = exact_d2(x - sx[j + h], y - sy[j + h], z - sz[j + h]);
+                        pass = (d2 != 0.0) && !(d2 > rc2);  // realspace.cpp:140
+                    }
+                    m |= static_cast<uint32_t>(pass) << (b + h);
                 }
-                m |= static_cast<uint32_t>(pass) << b;
             }
             mask[wd] = m;
         }
