@@ -150,6 +150,7 @@ struct fse_cuda_ctx {
     int* h_flags = nullptr;  // pinned
     bool overlap = std::getenv("FSE_SERIAL") == nullptr;  // real space on s1 alongside s0
     unsigned long long* d_counts = nullptr;  // real-space candidates / accepted pairs
+    bool str_pending = false;  // strengths still copying on s1 (EV_H2D marks the end)
 };
 
 namespace {
@@ -302,6 +303,12 @@ int bits_for(int64_t nkeys) {
 }
 
 // Sorted point set for the Fourier stages (support-tile order).
+enum {
+    EV_START, EV_PREP, EV_MEMSET, EV_SPREAD, EV_FFT1, EV_SCALE, EV_FFT2, EV_TPREP, EV_QUAD,
+    EV_R0, EV_RPAIR, EV_R1, EV_JOIN, EV_END, EV_H2D, EV_COUNT
+};
+static_assert(EV_COUNT <= NEV, "event pool");
+
 struct Sorted {
     uint32_t* perm = nullptr;
     int32_t* tstart = nullptr;  // nkeys + 1
@@ -330,6 +337,7 @@ Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
     FSE_CU(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (g.nkeys + 1), c->s0));
     launch_histogram(L, keys2, n, counts);
     exclusive_scan(c, c->s0, "s0", counts, s.tstart, g.nkeys + 1);
+    if (d_str && c->str_pending) FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_H2D], 0));
     launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true);
     return s;
 }
@@ -380,11 +388,6 @@ Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, con
     return r;
 }
 
-enum {
-    EV_START, EV_PREP, EV_MEMSET, EV_SPREAD, EV_FFT1, EV_SCALE, EV_FFT2, EV_TPREP, EV_QUAD,
-    EV_R0, EV_RPAIR, EV_R1, EV_JOIN, EV_END, EV_COUNT
-};
-static_assert(EV_COUNT <= NEV, "event pool");
 
 // real-space pair sum on s1 into d_uR (caller order).  No host sync: the
 // pair kernel is launched over an upper bound of work items and reads the
@@ -618,9 +621,19 @@ void run_sum_host(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double
     double* d_str = buf<double>(c, "in_str", a * n);
     double* d_tgt = tas ? d_pos : buf<double>(c, "in_tgt", 3 * nt);
     double* d_u = buf<double>(c, "in_u", 3 * nt);
+    // positions (and targets) on s0, strengths on s1: the support keys and sort
+    // of the positions overlap the strengths' transfer (pinned host memory)
     h2d(c, d_pos, pos, sizeof(double) * 3 * n);
-    h2d(c, d_str, str, sizeof(double) * a * n);
+    if (n > 0) {
+        FSE_CU(cudaMemcpyAsync(d_str, str, sizeof(double) * a * n, cudaMemcpyHostToDevice, c->s1));
+        FSE_CU(cudaEventRecord(c->ev[EV_H2D], c->s1));
+        c->str_pending = true;
+    }
     if (!tas) h2d(c, d_tgt, tgt, sizeof(double) * 3 * nt);
+    struct Clear {
+        fse_cuda_ctx* c;
+        ~Clear() { c->str_pending = false; }
+    } clear{c};
     run_sum(c, cfg, kind, d_pos, d_str, n, box_side, d_tgt, nt, tas ? 1 : 0, green, d_u, tm,
             want_f, want_r);
     d2h(c, u, d_u, sizeof(double) * 3 * nt);
