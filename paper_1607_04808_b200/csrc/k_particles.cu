@@ -65,35 +65,49 @@ __global__ void k_quad_table(GridParams g, double* q) {
 }
 
 // FGG axis weights (ewald.cpp:33-51) for point perm[q], stored at sorted slot q.
+// Each thread builds its point's 3P weights in shared memory (row stride 3P+1,
+// conflict-free); the block then writes its points' rows, which are one
+// contiguous run of w, with consecutive threads on consecutive doubles.
 __global__ void k_payload(GridParams g, const double* __restrict__ pos,
                           const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
                           int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
                           double* __restrict__ w, double* __restrict__ fs, bool fold_prefac) {
-    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (q >= n) return;
-    const int64_t idx = perm[q];
-    const int P = g.P;
-    double* wq = w + q * 3 * P;
+    extern __shared__ double stage[];
+    const int P = g.P, W3 = 3 * P, RS = W3 + 1;
+    const int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x);
+    const int64_t q = q0 + threadIdx.x;
+    if (q < n) {
+        const int64_t idx = perm[q];
+        double* row = stage + threadIdx.x * RS;
 #pragma unroll 1
-    for (int ax = 0; ax < 3; ++ax) {
-        const double x = pos[3 * idx + ax];
-        const double s = __ddiv_rn(__dsub_rn(x, g.origin), g.h);
-        int first = static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
-        const double x0 = (first - s) * g.h;
-        const double e0 = exp(-g.alpha * x0 * x0);
-        const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
-        const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
-        double r = 1.0;
-        for (int p = 0; p < P; ++p) {
-            wq[ax * P + p] = scale * (e0 * r * qtab[p]);
-            r *= ratio;
+        for (int ax = 0; ax < 3; ++ax) {
+            const double x = pos[3 * idx + ax];
+            const double s = __ddiv_rn(__dsub_rn(x, g.origin), g.h);
+            int first = static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
+            const double x0 = (first - s) * g.h;
+            const double e0 = exp(-g.alpha * x0 * x0);
+            const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
+            const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
+            double r = 1.0;
+            for (int p = 0; p < P; ++p) {
+                row[ax * P + p] = scale * (e0 * r * qtab[p]);
+                r *= ratio;
+            }
+            if (first < 0) first = 0;
+            if (first + P > g.Mt) first = g.Mt - P;
+            i0s[3 * q + ax] = first;
         }
-        if (first < 0) first = 0;
-        if (first + P > g.Mt) first = g.Mt - P;
-        i0s[3 * q + ax] = first;
+        if (fs)
+            for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
     }
-    if (fs)
-        for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
+    __syncthreads();
+    const int64_t left = n - q0;
+    const int cnt = static_cast<int>(left < blockDim.x ? left : blockDim.x);
+    double* out = w + q0 * W3;
+    for (int e = threadIdx.x; e < cnt * W3; e += blockDim.x) {
+        const int t = e / W3;
+        out[e] = stage[t * RS + (e - t * W3)];
+    }
 }
 
 __global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts) {
@@ -164,8 +178,19 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
                            const double* qtab, int32_t* i0s, double* w, double* fs,
                            bool fold_prefac) {
     if (n <= 0) return;
-    k_payload<<<blocks_for(n, 128), 128, 0, L.s>>>(g, pos, str, a, perm, n, qtab, i0s, w, fs,
-                                                   fold_prefac);
+    // block size: as many warps (<= 4) as fit 48 KB of staged weight rows;
+    // wider supports take one warp and opt-in shared memory
+    const size_t row_bytes = sizeof(double) * (3 * g.P + 1);
+    int tpb = static_cast<int>((48 * 1024) / row_bytes) / 32 * 32;
+    tpb = tpb < 32 ? 32 : (tpb > 128 ? 128 : tpb);
+    if (row_bytes * tpb > 48 * 1024) {
+        if (row_bytes * tpb > 227 * 1024)
+            throw Error(FSE_EINVAL, "k_payload: Gaussian support too wide");
+        FSE_CU(cudaFuncSetAttribute(k_payload, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(row_bytes * tpb)));
+    }
+    k_payload<<<blocks_for(n, tpb), tpb, row_bytes * tpb, L.s>>>(g, pos, str, a, perm, n, qtab,
+                                                                  i0s, w, fs, fold_prefac);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
