@@ -752,12 +752,16 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
     const int kz0 = tz * ncol;
     const int nc = min(ncol, Dh - kz0);
     const FDiv fnc = make_fdiv(nc);
+    // spectrum row of (comp, x = i, this ky) in units of Dh: spec_row with
+    // blk = i / nxs, xl = i - blk nxs, in 32-bit arithmetic
     const FDiv fnxs = make_fdiv(g.nxs);
-    auto crow = [&](int comp, int i) -> int64_t {
+    const int bstep = (A - 1) * g.nxs;
+    double2* Ck = Cb + kz0;
+    auto at = [&](int comp, int i, int c) -> double2* {
         const int blk = static_cast<int>(fdiv(i, fnxs));
-        return spec_row(blk, comp, i - blk * g.nxs, kyl, A, g.nxs, g.nkys, Dh) + kz0;
+        const int row = (i + blk * bstep + comp * g.nxs) * g.nkys + kyl;
+        return Ck + static_cast<int64_t>(row) * Dh + c;
     };
-    // forward x-FFT of the A components (pass 1 straight from global memory)
     // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (one exp per q per CTA
     // instead of one per element): rem = ex[kx] * ex[ky] * ex[kz]
     double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
@@ -765,9 +769,10 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
         const double kq = kax(q, D, g.dk);
         ex[q] = exp(-(1.0 - g.eta) * (kq * kq) * g.inv4xi2);
     }
+    // forward x-FFT of the A components (pass 1 straight from global memory)
     freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
-        return n < Mt ? Cb[crow(comp, n) + c] : make_double2(0.0, 0.0);
+        return n < Mt ? *at(comp, n, c) : make_double2(0.0, 0.0);
     });
     __syncthreads();
     freg::pass2_smem<D1, D2, true>(a, A * nc, -1, tab);
@@ -812,7 +817,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
     __syncthreads();
     freg::pass2<D1, D2, true, D2 / 2>(a, NO * nc, +1, tab, [&](int col, int k, double2 v) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
-        Cb[crow(comp, k) + c] = v;  // k < Mt by NOUT2
+        *at(comp, k, c) = v;  // k < Mt by NOUT2
     });
 }
 
@@ -1208,6 +1213,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     const int u = std::min(units_fit(h, A, gcol), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
+    // v2: exp factor table (D doubles) after the twiddles
     const size_t sm = smem_bytes(h, A * u) + gcol * u + (gcol ? 0 : sizeof(double) * D);
     const int ntz = (Dh + u - 1) / u;
     const unsigned blocks = static_cast<unsigned>(g.nky) * ntz;
