@@ -712,9 +712,12 @@ __global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __
     const int nc = min(ncol, Dh - kz0);
     const FDiv fky = make_fdiv(nkys);
     double2* Bp = B + static_cast<int64_t>(ci) * Mt * Dh + kz0;
+    // spec_row(blk, comp, xl, ky - blk nkys) in 32-bit arithmetic
+    const int rbase = (comp * nxs + xl) * nkys, bstep = (A * nxs - 1) * nkys;
+    double2* Ck = Cb + kz0;
     auto crow = [&](int ky) -> int64_t {
         const int blk = static_cast<int>(fdiv(ky, fky));
-        return spec_row(blk, comp, xl, ky - blk * nkys, A, nxs, nkys, Dh) + kz0;
+        return static_cast<int64_t>(rbase + blk * bstep + ky) * Dh;
     };
     if (!INV) {
         freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
@@ -722,10 +725,10 @@ __global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __
         });
         __syncthreads();
         freg::pass2<D1, D2, true, D2>(a, nc, -1, tab,
-                                      [&](int c, int k, double2 v) { Cb[crow(k) + c] = v; });
+                                      [&](int c, int k, double2 v) { Ck[crow(k) + c] = v; });
     } else {
         freg::pass1<D1, D2, true, D1>(a, nc, +1, tw, tab,
-                                      [&](int c, int n) { return Cb[crow(n) + c]; });
+                                      [&](int c, int n) { return Ck[crow(n) + c]; });
         __syncthreads();
         freg::pass2<D1, D2, true, D2 / 2>(a, nc, +1, tab, [&](int c, int k, double2 v) {
             Bp[static_cast<int64_t>(k) * Dh + c] = v;  // k < Mt by NOUT2
