@@ -61,6 +61,26 @@ def metric_name(w):
             "1/2/4/8 B200; % of roofline")
 
 
+# ------------------------------------------------------------------ output
+# The JSON line is the only thing on stdout: file descriptor 1 is pointed at
+# stderr for the rest of the run (NCCL's version banner, library prints), and
+# the line goes to a saved copy of the original stdout.
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _stdout_to_stderr():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 # ------------------------------------------------------------------ dist
 class Dist:
     def __init__(self, force_group=False):
@@ -236,9 +256,34 @@ def run_slabs(args, dist: Dist):
     upload()
     ex = TorchExchange()
     ss = SlabSum(ctx, cfg, w["kind"], dist.rank, dist.world)
+    from paper_1607_04808_b200.slabs import PeerExchange, torch_view
+
+    # exchange: peer-direct stores over NVLink (symmetric memory) unless it is
+    # unavailable or disagrees with the all-to-all path on a first evaluation
+    px, why = None, None
+    if args.exchange == "p2p" or (args.exchange == "auto" and dist.world > 1):
+        try:
+            px = PeerExchange(ss.block_doubles * ss.nslabs)
+        except Exception as e:  # noqa: BLE001 -- plumbing fallback, reported in the JSON
+            if args.exchange == "p2p":
+                raise
+            why = f"symmetric memory unavailable ({type(e).__name__}: {str(e)[:160]})"
+    if px is not None:
+        ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+        ref = torch_view(d_u, 3 * nt).clone()
+        ss.run_peers(px, ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+        differ = 0 if torch.equal(ref, torch_view(d_u, 3 * nt)) else 1
+        del ref
+        if dist.max(differ) != 0:
+            if args.exchange == "p2p":
+                raise RuntimeError("peer-direct exchange differs from the all-to-all path")
+            px, why = None, "peer-direct result differed from the all-to-all path"
 
     def step():
-        ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+        if px is not None:
+            ss.run_peers(px, ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+        else:
+            ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
 
     for _ in range(args.warmup):
         step()
@@ -261,31 +306,34 @@ def run_slabs(args, dist: Dist):
     max_ms = dist.max(dev_ms)
 
     # phase breakdown (untimed step, host-synchronised phases)
-    import torch as _t
-    send_t = None
     ph = {}
-    t0 = time.perf_counter()
-    ss.forward(d_pos, d_str, n)
-    ph["forward"] = time.perf_counter() - t0
-    from paper_1607_04808_b200.slabs import torch_view
-    send_t = torch_view(ss.d_send, ss.block_doubles * ss.nslabs)
-    recv_t = torch_view(ss.d_recv, ss.block_doubles * ss.nslabs)
-    t0 = time.perf_counter()
-    ex.all_to_all(send_t, recv_t)
-    ph["all_to_all"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ss.scale(green)
-    ph["scale"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ex.all_to_all(recv_t, send_t)
-    ph["all_to_all_back"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ss.inverse(d_pos, d_str, n, d_tgt, nt, tas, d_u)
-    ph["inverse_gather_realspace"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ex.all_reduce_sum(torch_view(d_u, 3 * nt))
-    ph["sum_partials"] = time.perf_counter() - t0
-    del _t
+
+    def phase(name, fn):
+        t0 = time.perf_counter()
+        fn()
+        ph[name] = time.perf_counter() - t0
+
+    r, G = dist.rank, dist.world
+    if px is not None:
+        fwd, bwd = px.ptrs
+        phase("forward_peer_stores", lambda: ctx.slab_forward_peers(
+            cfg, w["kind"], d_pos, d_str, n, r, G, fwd))
+        phase("barrier", px.barrier)
+        phase("scale_peer_stores", lambda: ctx.slab_scale_peers(
+            cfg, w["kind"], green, r, G, fwd[r], bwd))
+        phase("barrier_back", px.barrier)
+        phase("inverse_gather_realspace", lambda: ctx.slab_inverse(
+            cfg, w["kind"], d_pos, d_str, n, bwd[r], r, G, d_tgt, nt, int(tas), d_u))
+    else:
+        send_t = torch_view(ss.d_send, ss.block_doubles * ss.nslabs)
+        recv_t = torch_view(ss.d_recv, ss.block_doubles * ss.nslabs)
+        phase("forward", lambda: ss.forward(d_pos, d_str, n))
+        phase("all_to_all", lambda: ex.all_to_all(send_t, recv_t))
+        phase("scale", lambda: ss.scale(green))
+        phase("all_to_all_back", lambda: ex.all_to_all(recv_t, send_t))
+        phase("inverse_gather_realspace", lambda: ss.inverse(d_pos, d_str, n, d_tgt, nt, tas,
+                                                             d_u))
+    phase("sum_partials", lambda: ex.all_reduce_sum(torch_view(d_u, 3 * nt)))
 
     # e2e: pinned host inputs -> device every step, result back on every rank
     dist.barrier()
@@ -311,13 +359,18 @@ def run_slabs(args, dist: Dist):
                 "same system on every rank, no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
                    "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
-                   "parallelism": f"z-slabs x{dist.world} (NCCL all-to-all transposes)",
+                   "parallelism": f"z-slabs x{dist.world} (" + (
+                       "peer-direct NVLink stores into symmetric memory" if px is not None
+                       else "NCCL all-to-all transposes") + ")",
+                   "exchange_note": why,
                    "slab": {"x_lo": ss.info.x_lo, "nx": ss.info.nx, "ky_lo": ss.info.ky_lo,
                             "nky": ss.info.nky},
                    "l2": "working set >> 126 MB L2; no flush needed"},
         "e2e": {"value": nt * max(1, args.steps) / e2e_s, "unit": "targets/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * 3 * nt),
-                "api": "slabs.SlabSum.run (fse_cuda_slab_* + torch.distributed NCCL)"},
+                "api": "slabs.SlabSum.run_peers (fse_cuda_slab_*_peers + symmetric memory)"
+                       if px is not None else
+                       "slabs.SlabSum.run (fse_cuda_slab_* + torch.distributed NCCL)"},
         "roofline": {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": ach / fp64_peak, "kernel": "step (spread + quadrature work / rank)",
                      "traffic": None},
@@ -327,7 +380,7 @@ def run_slabs(args, dist: Dist):
         "cpu_baseline": None,
     }
     if dist.rank == 0:
-        print(json.dumps(line))
+        emit(line)
     ss.free()
     for p in (d_pos, d_str, d_u) + (() if tas else (d_tgt,)):
         ctx.dev_free(p)
@@ -480,7 +533,7 @@ def run_ours(args, dist: Dist):
         "cpu_baseline": cpu,
     }
     if dist.rank == 0:
-        print(json.dumps(line))
+        emit(line)
     for p in (d_pos, d_str, d_u) + (() if tas else (d_tgt,)):
         ctx.dev_free(p)
 
@@ -568,7 +621,7 @@ def run_reference(args, dist: Dist):
     for i in range(args.warmup + args.steps):
         r = cpu_reference_sample(w, frac=args.ref_frac, threads=None)
         if r["value"] is None:
-            print(json.dumps({"impl": "reference", "unavailable": r["sample"]}))
+            emit({"impl": "reference", "unavailable": r["sample"]})
             return
         if i >= args.warmup:
             vals.append(r["est_total_s"])
@@ -589,7 +642,7 @@ def run_reference(args, dist: Dist):
         "e2e": {"value": v, "unit": "targets/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def main():
@@ -602,6 +655,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent full evaluations per GPU instead of z-slabs")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="slab exchange: peer-direct stores (p2p), NCCL all-to-all, or p2p "
+                         "with a verified fallback to NCCL (auto, N > 1)")
     ap.add_argument("--slabs", action="store_true",
                     help="use the z-slab path also at N = 1 (one slab, NCCL group of one)")
     ap.add_argument("--ref-frac", type=int, default=64,
@@ -609,6 +665,7 @@ def main():
     ap.add_argument("--fp64-peak", type=float, default=None,
                     help="TFLOP/s; default: measured in-run with a DFMA loop")
     args = ap.parse_args()
+    _stdout_to_stderr()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     dist = Dist(force_group=args.slabs and args.impl == "ours")

@@ -137,6 +137,25 @@ fse_status fse_cuda_slab_inverse(fse_cuda_ctx* ctx, const fse_config* cfg, int k
                                  const double* d_pos, const double* d_str, int64_t n,
                                  double* d_spec, int rank, int nslabs, const double* d_tgt,
                                  int64_t nt, int tas, double* d_u);
+/* Peer-direct exchange (no all-to-all): every rank allocates two exchange buffers
+ * A_s, B_s (nslabs * block_complex each) that all ranks map (CUDA IPC / symmetric
+ * memory over NVLink); dst_bufs[s] is rank s's buffer as seen from this process.
+ *   fse_cuda_slab_forward_peers(dst_bufs = {A_s}): the y pass stores block s of this
+ *       rank's spectrum straight into A_s at block `rank` (what the all-to-all would
+ *       have delivered);
+ *   barrier;
+ *   fse_cuda_slab_scale_peers(d_spec = A_rank, dst_bufs = {B_s}): the x pass reads its
+ *       own A and stores x block r of the results into B_r at block `rank`;
+ *   barrier;
+ *   fse_cuda_slab_inverse(d_spec = B_rank), then the sum of the partials.
+ * nslabs <= 16.  Both calls return after their kernels completed (the caller's
+ * barrier then orders the phases across ranks). */
+fse_status fse_cuda_slab_forward_peers(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                       const double* d_pos, const double* d_str, int64_t n,
+                                       int rank, int nslabs, double* const* dst_bufs);
+fse_status fse_cuda_slab_scale_peers(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                     const fse_green* green, int rank, int nslabs,
+                                     double* d_spec, double* const* dst_bufs);
 
 /* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
 fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);

@@ -288,6 +288,10 @@ def _load():
                                             C.c_int, vp]
         lib.fse_cuda_slab_inverse.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
                                               vp, C.c_int, C.c_int, vp, i64, C.c_int, vp]
+        lib.fse_cuda_slab_forward_peers.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp,
+                                                    i64, C.c_int, C.c_int, C.POINTER(vp)]
+        lib.fse_cuda_slab_scale_peers.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp,
+                                                  C.c_int, C.c_int, vp, C.POINTER(vp)]
         lib.fse_cuda_realspace_counts.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         lib.fse_fourier_error_estimate.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double,
                                                    C.c_double, C.c_double, _dp]
@@ -498,6 +502,17 @@ class Context:
     def slab_scale(self, cfg, kind, green, rank, nslabs, d_spec):
         self._call(_load().fse_cuda_slab_scale, C.byref(cfg), int(kind), green.handle,
                    int(rank), int(nslabs), C.c_void_p(d_spec))
+
+    # peer-direct exchange: dst_bufs[s] = rank s's exchange buffer mapped here
+    def slab_forward_peers(self, cfg, kind, d_pos, d_str, n, rank, nslabs, dst_bufs):
+        ptrs = (C.c_void_p * len(dst_bufs))(*[int(q) for q in dst_bufs])
+        self._call(_load().fse_cuda_slab_forward_peers, C.byref(cfg), int(kind),
+                   C.c_void_p(d_pos), C.c_void_p(d_str), int(n), int(rank), int(nslabs), ptrs)
+
+    def slab_scale_peers(self, cfg, kind, green, rank, nslabs, d_spec, dst_bufs):
+        ptrs = (C.c_void_p * len(dst_bufs))(*[int(q) for q in dst_bufs])
+        self._call(_load().fse_cuda_slab_scale_peers, C.byref(cfg), int(kind), green.handle,
+                   int(rank), int(nslabs), C.c_void_p(d_spec), ptrs)
 
     def slab_inverse(self, cfg, kind, d_pos, d_str, n, d_spec, rank, nslabs, d_tgt, nt, tas,
                      d_u):

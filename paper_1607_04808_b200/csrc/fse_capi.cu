@@ -1079,6 +1079,7 @@ namespace {
 GridParams slab_params(const fse_config* cfg, int rank, int nslabs) {
     check_cfg(cfg);
     if (nslabs < 1 || rank < 0 || rank >= nslabs) invalid("slab: need 0 <= rank < nslabs");
+    if (nslabs > kMaxSlabs) invalid("slab: at most 16 slabs");
     GridParams g = make_grid_params(*cfg);
     set_slab(g, rank, nslabs);
     if (nslabs > 1 && !gather_slab_enabled(g))
@@ -1113,41 +1114,97 @@ fse_status fse_cuda_slab_info(const fse_config* cfg, int kind, int rank, int nsl
     }
 }
 
+namespace {
+
+// block table of a peer-direct exchange: block s -> dst_bufs[s] at block
+// `rank`, uploaded to a small device array (stream-ordered)
+BlockDest peer_blocks(fse_cuda_ctx* c, const GridParams& g, int a, int rank, int nslabs,
+                      double* const* dst_bufs, const char* name) {
+    if (!dst_bufs) invalid("null pointer");
+    if (nslabs > kMaxSlabs) invalid("slab: at most 16 slabs");
+    const int64_t block = slab_block_elems(g, a);
+    double2* h[kMaxSlabs] = {};
+    for (int s = 0; s < nslabs; ++s) {
+        if (!dst_bufs[s]) invalid("null peer buffer");
+        h[s] = reinterpret_cast<double2*>(dst_bufs[s]) + rank * block;
+    }
+    double2** d_tab = buf<double2*>(c, name, kMaxSlabs);
+    FSE_CU(cudaMemcpyAsync(d_tab, h, sizeof h, cudaMemcpyHostToDevice, c->s0));
+    BlockDest d{};
+    d.tab = d_tab;
+    return d;
+}
+
+void slab_forward_impl(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_pos,
+                       const double* d_str, int64_t n, int rank, int nslabs, double* d_spec,
+                       double* const* dst_bufs) {
+    check_kind(kind);
+    if ((!d_spec && !dst_bufs) || (n > 0 && (!d_pos || !d_str))) invalid("null pointer");
+    const int a = arity_of(kind);
+    const GridParams g = slab_params(cfg, rank, nslabs);
+    BlockDest peers{};
+    if (dst_bufs) peers = peer_blocks(c, g, a, rank, nslabs, dst_bufs, "peer_fwd");
+    FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
+    Launch L = L0(c);
+    double* qtab = buf<double>(c, "qtab", g.P);
+    launch_quad_table(L, g, qtab);
+    Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
+    double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
+    double2* Bs = buf<double2>(c, "B", static_cast<size_t>(a) * g.nx * g.Mt * g.Dh);
+    const FftPlanDev& fp = fft_plan(c, g.D);
+    for (int c0 = 0; c0 < a; c0 += 3)
+        launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
+    launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, reinterpret_cast<double2*>(d_spec),
+                          dst_bufs ? &peers : nullptr);
+    raise_flags(c);  // synchronises s0
+}
+
+void slab_scale_impl(fse_cuda_ctx* c, const fse_config* cfg, int kind, const fse_green* green,
+                     int rank, int nslabs, double* d_spec, double* const* dst_bufs) {
+    check_kind(kind);
+    if (!d_spec) invalid("null pointer");
+    const GridParams g = slab_params(cfg, rank, nslabs);
+    check_green(cfg, kind, green);
+    if (green->device != c->device) invalid("green lives on another device");
+    BlockDest peers{};
+    if (dst_bufs) peers = peer_blocks(c, g, arity_of(kind), rank, nslabs, dst_bufs, "peer_bwd");
+    const FftPlanDev& fp = fft_plan(c, g.D);
+    launch_fft_xscale(L0(c), fp.host, fp.tw, g, kind, green->d_half,
+                      reinterpret_cast<double2*>(d_spec), dst_bufs ? &peers : nullptr);
+    FSE_CU(cudaStreamSynchronize(c->s0));
+}
+
+}  // namespace
+
 fse_status fse_cuda_slab_forward(fse_cuda_ctx* c, const fse_config* cfg, int kind,
                                  const double* d_pos, const double* d_str, int64_t n, int rank,
                                  int nslabs, double* d_spec) {
     return api(c, [&] {
-        check_kind(kind);
-        if (!d_spec || (n > 0 && (!d_pos || !d_str))) invalid("null pointer");
-        const int a = arity_of(kind);
-        const GridParams g = slab_params(cfg, rank, nslabs);
-        FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
-        Launch L = L0(c);
-        double* qtab = buf<double>(c, "qtab", g.P);
-        launch_quad_table(L, g, qtab);
-        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
-        double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
-        double2* Bs = buf<double2>(c, "B", static_cast<size_t>(a) * g.nx * g.Mt * g.Dh);
-        const FftPlanDev& fp = fft_plan(c, g.D);
-        for (int c0 = 0; c0 < a; c0 += 3)
-            launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
-        launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, reinterpret_cast<double2*>(d_spec));
-        raise_flags(c);  // synchronises s0
+        if (!d_spec) invalid("null pointer");
+        slab_forward_impl(c, cfg, kind, d_pos, d_str, n, rank, nslabs, d_spec, nullptr);
+    });
+}
+
+fse_status fse_cuda_slab_forward_peers(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                       const double* d_pos, const double* d_str, int64_t n,
+                                       int rank, int nslabs, double* const* dst_bufs) {
+    return api(c, [&] {
+        if (!dst_bufs) invalid("null pointer");
+        slab_forward_impl(c, cfg, kind, d_pos, d_str, n, rank, nslabs, nullptr, dst_bufs);
     });
 }
 
 fse_status fse_cuda_slab_scale(fse_cuda_ctx* c, const fse_config* cfg, int kind,
                                const fse_green* green, int rank, int nslabs, double* d_spec) {
+    return api(c, [&] { slab_scale_impl(c, cfg, kind, green, rank, nslabs, d_spec, nullptr); });
+}
+
+fse_status fse_cuda_slab_scale_peers(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                     const fse_green* green, int rank, int nslabs,
+                                     double* d_spec, double* const* dst_bufs) {
     return api(c, [&] {
-        check_kind(kind);
-        if (!d_spec) invalid("null pointer");
-        const GridParams g = slab_params(cfg, rank, nslabs);
-        check_green(cfg, kind, green);
-        if (green->device != c->device) invalid("green lives on another device");
-        const FftPlanDev& fp = fft_plan(c, g.D);
-        launch_fft_xscale(L0(c), fp.host, fp.tw, g, kind, green->d_half,
-                          reinterpret_cast<double2*>(d_spec));
-        FSE_CU(cudaStreamSynchronize(c->s0));
+        if (!dst_bufs) invalid("null pointer");
+        slab_scale_impl(c, cfg, kind, green, rank, nslabs, d_spec, dst_bufs);
     });
 }
 

@@ -73,6 +73,23 @@ struct GridParams {
 // restrict g to slab r of G (x-planes in multiples of 8, ky rows balanced)
 void set_slab(GridParams& g, int r, int G);
 
+// Destination of each spectrum block that crosses the slab exchange (block b
+// goes to rank b).  Local exchange buffer (one GPU, NCCL path): base + b *
+// stride; peer-direct: tab[b] (a device array) = block `rank` of rank b's
+// buffer, mapped into this process over NVLink, so the pass that produces a
+// block stores it straight into its owner's memory (no send buffer, no NCCL
+// all-to-all).  (A pointer array passed by value would be copied to local
+// memory by the dynamic block index.)
+constexpr int kMaxSlabs = 16;
+struct BlockDest {
+    double2* base;
+    int64_t stride;
+    double2* const* tab;
+};
+__device__ __forceinline__ double2* block_ptr(const BlockDest& d, int b) {
+    return d.tab ? d.tab[b] : d.base + b * d.stride;
+}
+
 GridParams make_grid_params(const fse_config& cfg);
 
 // Device-side constant tables (per call, small): q[p] = exp(-alpha (p h)^2)

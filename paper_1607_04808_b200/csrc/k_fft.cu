@@ -388,7 +388,7 @@ template <int ENG, bool INV>
 __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int A, int nxs, int nkys,
                                                   int ncol, double2* __restrict__ B,
-                                                  double2* __restrict__ Cb) {
+                                                  double2* __restrict__ Cb, BlockDest dst) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
     const double2* tw = stage_twiddles(a, pl, tw_g);
@@ -422,10 +422,17 @@ __global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __r
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, INV ? +1 : -1);
     const int nout = INV ? Mt : D;
+    const int rb = (comp * nxs + xl) * nkys;  // row of (comp, xl, kyl = 0) within a block
     for (int e = threadIdx.x; e < nc * nout; e += blockDim.x) {
         const int j = static_cast<int>(fdiv(e, fnc)), c = e - j * nc;
-        double2* dst = INV ? Bp + static_cast<int64_t>(j) * Dh + c : Cb + crow(j) + c;
-        *dst = r[cidx<ENG>(c, j, D)];
+        double2* out;
+        if (INV) {
+            out = Bp + static_cast<int64_t>(j) * Dh + c;
+        } else {  // block j / nkys goes to its ky owner
+            const int blk = static_cast<int>(fdiv(j, fky));
+            out = block_ptr(dst, blk) + static_cast<int64_t>(rb + j - blk * nkys) * Dh + kz0 + c;
+        }
+        *out = r[cidx<ENG>(c, j, D)];
     }
 }
 
@@ -497,7 +504,7 @@ template <int ENG, int KIND>
 __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
                                                    GridParams g, int ncol,
                                                    const double* __restrict__ G,
-                                                   double2* __restrict__ Cb) {
+                                                   double2* __restrict__ Cb, BlockDest dst) {
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -568,10 +575,14 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
     __syncthreads();
     double2* other = (r == a) ? sb : a;
     double2* r2 = fft_cols<ENG>(r, other, NO * nc, pl, tw, +1);
+    // x block i / nxs goes back to its slab owner
     for (int comp = 0; comp < NO; ++comp) {
         for (int e = threadIdx.x; e < nc * Mt; e += blockDim.x) {
             const int i = static_cast<int>(fdiv(e, fnc)), c = e - i * nc;
-            Cb[crow(comp, i) + c] = r2[cidx<ENG>(comp * nc + c, i, D)];
+            const int blk = static_cast<int>(fdiv(i, fnxs));
+            const int row = ((comp * g.nxs) + i - blk * g.nxs) * g.nkys + kyl;
+            block_ptr(dst, blk)[static_cast<int64_t>(row) * Dh + kz0 + c] =
+                r2[cidx<ENG>(comp * nc + c, i, D)];
         }
     }
 }
@@ -698,7 +709,7 @@ template <int ENG, bool INV>
 __global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
                                                    int Mt, int nx, int A, int nxs, int nkys,
                                                    int ncol, double2* __restrict__ B,
-                                                   double2* __restrict__ Cb) {
+                                                   double2* __restrict__ Cb, BlockDest dst) {
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
     const double2* tw = stage_twiddles(a, pl, tw_g);
@@ -724,8 +735,12 @@ __global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __
             return n < Mt ? Bp[static_cast<int64_t>(n) * Dh + c] : make_double2(0.0, 0.0);
         });
         __syncthreads();
-        freg::pass2<D1, D2, true, D2>(a, nc, -1, tab,
-                                      [&](int c, int k, double2 v) { Ck[crow(k) + c] = v; });
+        // block k / nkys goes to its ky owner
+        const int rb = (comp * nxs + xl) * nkys;
+        freg::pass2<D1, D2, true, D2>(a, nc, -1, tab, [&](int c, int k, double2 v) {
+            const int blk = static_cast<int>(fdiv(k, fky));
+            block_ptr(dst, blk)[static_cast<int64_t>(rb + k - blk * nkys) * Dh + kz0 + c] = v;
+        });
     } else {
         freg::pass1<D1, D2, true, D1>(a, nc, +1, tw, tab,
                                       [&](int c, int n) { return Ck[crow(n) + c]; });
@@ -741,7 +756,7 @@ template <int ENG, int KIND>
 __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
-                                                    double2* __restrict__ Cb) {
+                                                    double2* __restrict__ Cb, BlockDest dst) {
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
@@ -820,7 +835,10 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
     __syncthreads();
     freg::pass2<D1, D2, true, D2 / 2>(a, NO * nc, +1, tab, [&](int col, int k, double2 v) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
-        *at(comp, k, c) = v;  // k < Mt by NOUT2
+        // k < Mt by NOUT2; x block k / nxs goes back to its slab owner
+        const int blk = static_cast<int>(fdiv(k, fnxs));
+        const int row = (comp * g.nxs + k - blk * g.nxs) * g.nkys + kyl;
+        block_ptr(dst, blk)[static_cast<int64_t>(row) * Dh + kz0 + c] = v;
     });
 }
 
@@ -1145,10 +1163,20 @@ void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw
     ++*L.launches;
 }
 
+// local block table: block b of the exchange buffer C (block = ncomp nxs nkys Dh)
+BlockDest local_blocks(const GridParams& g, int ncomp, double2* C) {
+    BlockDest d{};
+    d.base = C;
+    d.stride = static_cast<int64_t>(ncomp) * g.nxs * g.nkys * g.Dh;
+    d.tab = nullptr;
+    return d;
+}
+
 void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                            const GridParams& g, int ncomp, const double* R, double2* B,
-                           double2* C) {
+                           double2* C, const BlockDest* peers) {
     upload_consts();
+    const BlockDest dst = peers ? *peers : local_blocks(g, ncomp, C);
     const int Mt = g.Mt, nx = g.nx;
     const int D = h.dev.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     if (nx <= 0 || ncomp <= 0) return;  // empty slab
@@ -1187,16 +1215,16 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
                 if (v2_mask_for<EV>() & 2) {
                     allow_smem(k_ypass2<EV, false>, sm);
                     k_ypass2<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
-                                                                   g.nkys, u, B, C);
+                                                                   g.nkys, u, B, C, dst);
                 } else {
                     allow_smem(k_ypass<EV, false>, sm);
                     k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
-                                                                  g.nkys, u, B, C);
+                                                                  g.nkys, u, B, C, dst);
                 }
             } else {
                 allow_smem(k_ypass<EV, false>, sm);
                 k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
-                                                              g.nkys, u, B, C);
+                                                              g.nkys, u, B, C, dst);
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
@@ -1205,9 +1233,12 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
 }
 
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
-                       const GridParams& g, int kind, const double* G, double2* C) {
+                       const GridParams& g, int kind, const double* G, double2* C,
+                       const BlockDest* peers) {
     upload_consts();
     const int A = kind == KIND_SCALAR ? 1 : arity_of(kind);
+    // results (3 comps) go back in place (local) or to the x-slab owners
+    const BlockDest dst = peers ? *peers : local_blocks(g, A, C);
     const int D = h.dev.D, Dh = D / 2 + 1;
     // v2 (register engines) reads G from global memory; v1 stages it
     int xmask = 0;
@@ -1226,31 +1257,31 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
         if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
-                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
             } else if (kind == FSE_STRESSLET) {
                 allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
-                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
             } else if (kind == KIND_SCALAR) {
                 allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
-                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
             } else {
                 allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
-                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
             }
             return;
         }
         if (kind == FSE_STOKESLET) {
             allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
-            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
         } else if (kind == FSE_STRESSLET) {
             allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
-            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
         } else if (kind == KIND_SCALAR) {
             allow_smem(k_xscale<EV, KIND_SCALAR>, sm);
-            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
         } else {
             allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
-            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C);
+            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
         }
     });
     FSE_LAUNCH_CHECK();
@@ -1277,16 +1308,16 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
                 if (v2_mask_for<EV>() & 8) {
                     allow_smem(k_ypass2<EV, true>, sm);
                     k_ypass2<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
-                                                                  u, B, C);
+                                                                  u, B, C, BlockDest{});
                 } else {
                     allow_smem(k_ypass<EV, true>, sm);
                     k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
-                                                                 B, C);
+                                                                 B, C, BlockDest{});
                 }
             } else {
                 allow_smem(k_ypass<EV, true>, sm);
                 k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
-                                                             B, C);
+                                                             B, C, BlockDest{});
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;

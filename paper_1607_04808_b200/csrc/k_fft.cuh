@@ -64,13 +64,18 @@ void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw
 
 // R (a x nx x Mt^2 real, this slab's planes) -> B (a x nx x Mt x Dh) -> C (slab-blocked
 // send layout, see spec_row in k_fft.cu; one GPU: a x Mt x D x Dh)
+// peers: destinations of the spectrum blocks (peer-direct exchange); null =
+// the local exchange buffer C
 void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                            const GridParams& g, int ncomp, const double* R, double2* B,
-                           double2* C);
+                           double2* C, const BlockDest* peers = nullptr);
 // C (receive layout, ky rows [ky_lo, ky_lo + nky)): forward x-FFT, multiply by
 // A_eff(k) G(k) / D^3, inverse x-FFT, in place (3 comps out)
+// peers: where the results of each x block go (peer-direct exchange); null =
+// in place
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
-                       const GridParams& g, int kind, const double* G, double2* C);
+                       const GridParams& g, int kind, const double* G, double2* C,
+                       const BlockDest* peers = nullptr);
 // C (send layout, 3 comps in blocks of A) -> B (j < Mt) -> W (3 x nx x Mt^2 real)
 void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                            const GridParams& g, int A, double2* C, double2* B, double* W,

@@ -16,10 +16,13 @@ share of every target's quadrature.  The exchanges per evaluation are
    self term of target range ``r`` are added by rank ``r`` only).
 
 ``Exchange`` implementations: ``TorchExchange`` (torch.distributed; NCCL over
-NVLink on GPUs, gloo on CPU for the tests) and the single-process
+NVLink on GPUs, gloo on CPU for the tests), ``PeerExchange`` (no all-to-all:
+the y pass and the x pass store their blocks straight into the owning rank's
+buffer, mapped over NVLink with torch symmetric memory, and a barrier orders
+the phases; see ``fse_cuda_slab_forward_peers``) and the single-process
 ``simulate`` driver, which runs ``G`` virtual ranks one after another on one
-device (no kernel ever waits on another rank) to check the decomposition
-against the one-GPU result.
+device (no kernel ever waits on another rank) to check the decomposition --
+both exchanges -- against the one-GPU result.
 """
 from __future__ import annotations
 
@@ -91,6 +94,38 @@ class TorchExchange:
         self._sync(t)
 
 
+class PeerExchange:
+    """Peer-direct exchange buffers: two symmetric-memory allocations per rank
+    (CUDA IPC mappings over NVLink), every rank's buffer addresses known to all.
+
+    ``ptrs[0][s]`` / ``ptrs[1][s]``: rank s's forward (A) / backward (B) buffer.
+    """
+
+    def __init__(self, nelem: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.torch, self.dist = torch, dist
+        self.group = group if group is not None else dist.distributed_c10d._get_default_group()
+        self.rank = dist.get_rank(self.group)
+        self.size = dist.get_world_size(self.group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.tensors, self.handles, self.ptrs = [], [], []
+        for _ in range(2):
+            t = symm_mem.empty(int(nelem), dtype=torch.float64, device=dev)
+            h = symm_mem.rendezvous(t, self.group)
+            self.tensors.append(t)
+            self.handles.append(h)
+            self.ptrs.append([int(q) for q in h.buffer_ptrs])
+
+    def barrier(self):
+        """All ranks' previous phase done (the C-ABI calls return after their
+        kernels completed; the device barrier then orders the ranks)."""
+        self.torch.cuda.synchronize()
+        self.handles[0].barrier()
+        self.torch.cuda.synchronize()
+
+
 class SlabSum:
     """One rank's side of the decomposed ``total_sum`` (device pointers).
 
@@ -124,6 +159,20 @@ class SlabSum:
         self.ctx.slab_inverse(self.cfg, self.kind, d_pos, d_str, n, self.d_send, self.rank,
                               self.nslabs, d_tgt, nt, int(tas), d_u)
 
+    def run_peers(self, px: PeerExchange, ex: TorchExchange, green, d_pos, d_str, n, d_tgt,
+                  nt, tas, d_u):
+        """Full evaluation with the peer-direct exchange (buffers of ``px``; the
+        final sum of the partial velocities still goes through ``ex``)."""
+        fwd, bwd = px.ptrs
+        r, G = self.rank, self.nslabs
+        self.ctx.slab_forward_peers(self.cfg, self.kind, d_pos, d_str, n, r, G, fwd)
+        px.barrier()
+        self.ctx.slab_scale_peers(self.cfg, self.kind, green, r, G, fwd[r], bwd)
+        px.barrier()
+        self.ctx.slab_inverse(self.cfg, self.kind, d_pos, d_str, n, bwd[r], r, G, d_tgt, nt,
+                              int(tas), d_u)
+        ex.all_reduce_sum(torch_view(d_u, 3 * nt))
+
     def run(self, ex: TorchExchange, green, d_pos, d_str, n, d_tgt, nt, tas, d_u):
         """Full evaluation; on return d_u (NT x 3) holds the summed velocities."""
         send = torch_view(self.d_send, self.block_doubles * self.nslabs)
@@ -137,12 +186,14 @@ class SlabSum:
 
 
 def simulate(ctx: Context, cfg: EwaldConfig, kind, positions, strengths, targets, green,
-             nslabs: int, targets_are_sources: bool) -> np.ndarray:
+             nslabs: int, targets_are_sources: bool, peers: bool = False) -> np.ndarray:
     """Run the G-slab pipeline as G virtual ranks on one device, in sequence.
 
-    Host arrays in, host velocities out.  The exchanges are device copies
-    between the virtual ranks' buffers.  Used by the tests to check the
-    decomposition against ``Context.total_sum``.
+    Host arrays in, host velocities out.  ``peers=False``: the exchanges are
+    device copies between the virtual ranks' buffers (what the all-to-all
+    does); ``peers=True``: the peer-direct entry points store every block
+    straight into the owning virtual rank's buffer, as over NVLink.  Used by
+    the tests to check the decomposition against ``Context.total_sum``.
     """
     pos = np.ascontiguousarray(positions, dtype=np.float64)
     st = np.ascontiguousarray(strengths, dtype=np.float64)
@@ -161,16 +212,24 @@ def simulate(ctx: Context, cfg: EwaldConfig, kind, positions, strengths, targets
         ctx.memcpy(d_tgt, tgt.ctypes.data, tgt.nbytes)
         ranks = [SlabSum(ctx, cfg, kind, r, nslabs) for r in range(nslabs)]
         blk = 8 * ranks[0].block_doubles
-        for rk in ranks:
-            rk.forward(d_pos, d_str, n)
-        for r, rk in enumerate(ranks):      # block s of rank r -> block r of rank s
-            for s, dst in enumerate(ranks):
-                ctx.memcpy(dst.d_recv + r * blk, rk.d_send + s * blk, blk)
-        for rk in ranks:
-            rk.scale(green)
-        for s, rk in enumerate(ranks):      # block r of rank s -> block s of rank r
-            for r, dst in enumerate(ranks):
-                ctx.memcpy(dst.d_send + s * blk, rk.d_recv + r * blk, blk)
+        if peers:  # forward buffers = the d_recv's, backward buffers = the d_send's
+            fwd = [rk.d_recv for rk in ranks]
+            bwd = [rk.d_send for rk in ranks]
+            for r in range(nslabs):
+                ctx.slab_forward_peers(cfg, kind, d_pos, d_str, n, r, nslabs, fwd)
+            for r in range(nslabs):
+                ctx.slab_scale_peers(cfg, kind, green, r, nslabs, fwd[r], bwd)
+        else:
+            for rk in ranks:
+                rk.forward(d_pos, d_str, n)
+            for r, rk in enumerate(ranks):      # block s of rank r -> block r of rank s
+                for s, dst in enumerate(ranks):
+                    ctx.memcpy(dst.d_recv + r * blk, rk.d_send + s * blk, blk)
+            for rk in ranks:
+                rk.scale(green)
+            for s, rk in enumerate(ranks):      # block r of rank s -> block s of rank r
+                for r, dst in enumerate(ranks):
+                    ctx.memcpy(dst.d_send + s * blk, rk.d_recv + r * blk, blk)
         u = np.zeros((nt, 3))
         part = np.empty((nt, 3))
         for rk in ranks:

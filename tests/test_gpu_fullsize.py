@@ -104,6 +104,10 @@ def test_cfg2_slab_decomposition_full_size(fse, ctx, cfg2):
         us = slabs.simulate(ctx, cfg, 0, s.positions, s.strengths, s.positions, g, G,
                             targets_are_sources=True)
         assert rel_max(us, u) <= 1e-12
+    # peer-direct exchange at full size: bit-identical to the all-to-all path
+    up = slabs.simulate(ctx, cfg, 0, s.positions, s.strengths, s.positions, g, 3,
+                        targets_are_sources=True, peers=True)
+    assert np.array_equal(up, us)
 
 
 def test_cfg5_full_size(fse, ctx):

@@ -125,3 +125,34 @@ def test_slab_pipeline_uneven(fse, ctx, rng, G):
     got = slabs.simulate(ctx, cfg, 0, s.positions, s.strengths, tgt, g, G,
                          targets_are_sources=True)
     assert rel_max(got, want) <= 1e-12
+    peer = slabs.simulate(ctx, cfg, 0, s.positions, s.strengths, tgt, g, G,
+                          targets_are_sources=True, peers=True)
+    assert np.array_equal(peer, got)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_peer_exchange_equals_all_to_all(fse, ctx, rng, kind, G):
+    """Peer-direct exchange (fse_cuda_slab_forward_peers / _scale_peers: every
+    block stored straight into its owner's buffer) is bit-identical to the
+    all-to-all path: same kernels, same arithmetic, only the destinations of
+    the stores differ."""
+    from paper_1607_04808_b200 import slabs
+    cfg, s, tgt, g = _case(fse, ctx, rng, kind, 2500, (1.0, 15.28, 0.25, 40, 24), True)
+    a2a = slabs.simulate(ctx, cfg, kind, s.positions, s.strengths, tgt, g, G,
+                         targets_are_sources=False)
+    peer = slabs.simulate(ctx, cfg, kind, s.positions, s.strengths, tgt, g, G,
+                          targets_are_sources=False, peers=True)
+    assert np.array_equal(peer, a2a)
+    want = ctx.total_sum(s, kind, cfg, tgt, g)
+    assert rel_max(peer, want) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_peer_exchange_rejects_bad_tables(fse, ctx, rng):
+    cfg, s, tgt, g = _case(fse, ctx, rng, 0, 500, (1.0, 15.28, 0.25, 40, 24), False)
+    with pytest.raises(fse.InvalidArgument):
+        ctx.slab_forward_peers(cfg, 0, 0, 0, 0, 0, 17, [1] * 17)  # > 16 slabs
+    with pytest.raises(fse.InvalidArgument):
+        ctx.slab_forward_peers(cfg, 0, 0, 0, 0, 0, 2, [0, 0])  # null peer buffers
