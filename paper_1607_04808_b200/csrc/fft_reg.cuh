@@ -217,8 +217,10 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
     if (a1) {
         c1 = tid / D2;
         n2 = tid - c1 * D2;
+        // ridx(c, n1 D2 + n2) = ridx(c, n2) + n1 (D2 + 1) for n2 < D2
+        const double2* src = buf + ridx<D1, D2>(c1, n2);
 #pragma unroll
-        for (int n1 = 0; n1 < D1; ++n1) v[n1] = buf[ridx<D1, D2>(c1, n1 * D2 + n2)];
+        for (int n1 = 0; n1 < D1; ++n1) v[n1] = src[n1 * (D2 + 1)];
         rfft<D1>(v, sgn, tab);
         int t = 0;  // n2 * k1 mod D
 #pragma unroll
@@ -234,8 +236,9 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
     }
     __syncthreads();
     if (a1) {
+        double2* dst = buf + ridx<D1, D2>(c1, n2);
 #pragma unroll
-        for (int k1 = 0; k1 < D1; ++k1) buf[ridx<D1, D2>(c1, k1 * D2 + n2)] = v[k1];
+        for (int k1 = 0; k1 < D1; ++k1) dst[k1 * (D2 + 1)] = v[k1];
     }
     __syncthreads();
     // pass 2: item (c, k1)
@@ -245,8 +248,10 @@ __device__ __forceinline__ void fft_cols_2l(double2* buf, int ncol, int sgn,
     if (a2) {
         c2 = tid / D1;
         k1 = tid - c2 * D1;
+        // ridx(c, k1 D2 + j) = ridx(c, 0) + k1 (D2 + 1) + j for j < D2
+        const double2* src = buf + ridx<D1, D2>(c2, 0) + k1 * (D2 + 1);
 #pragma unroll
-        for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c2, k1 * D2 + j)];
+        for (int j = 0; j < D2; ++j) u[j] = src[j];
         rfft<D2>(u, sgn, tab);
     }
     __syncthreads();
@@ -318,8 +323,37 @@ __device__ __forceinline__ void pass1(double2* buf, int ncol, int sgn, const dou
         t += n2;
         if (t >= D) t -= D;
     }
+    double2* dst = buf + ridx<D1, D2>(c, n2);  // + k1 (D2 + 1): ridx(c, k1 D2 + n2)
 #pragma unroll
-    for (int k1 = 0; k1 < D1; ++k1) buf[ridx<D1, D2>(c, k1 * D2 + n2)] = v[k1];
+    for (int k1 = 0; k1 < D1; ++k1) dst[k1 * (D2 + 1)] = v[k1];
+}
+
+// pass 1 in place on buf (loads ridx(c, n1 D2 + n2) of its own item, FFT_D1,
+// twiddle, stores the transpose over them; no barriers inside)
+template <int D1, int D2, bool CF>
+__device__ __forceinline__ void pass1_inplace(double2* buf, int ncol, int sgn, const double2* twD,
+                                              const double2* tab) {
+    constexpr int D = D1 * D2;
+    int c, n2;
+    if (!item1<D1, D2, CF>(ncol, c, n2)) return;
+    double2* col = buf + ridx<D1, D2>(c, n2);
+    double2 v[D1];
+#pragma unroll
+    for (int n1 = 0; n1 < D1; ++n1) v[n1] = col[n1 * (D2 + 1)];
+    rfft<D1>(v, sgn, tab);
+    int t = 0;  // n2 * k1 mod D
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) {
+        if (k1 > 0) {
+            double2 w = twD[t];
+            if (sgn > 0) w.y = -w.y;
+            v[k1] = cmul(v[k1], w);
+        }
+        t += n2;
+        if (t >= D) t -= D;
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) col[k1 * (D2 + 1)] = v[k1];
 }
 
 // pass 2 (after a barrier): u[j] = buf[ridx(c, k1 D2 + j)], FFT_D2, then
@@ -331,8 +365,9 @@ __device__ __forceinline__ void pass2(const double2* buf, int ncol, int sgn, con
     int c, k1;
     if (!item2<D1, D2, CF>(ncol, c, k1)) return;
     double2 u[D2];
+    const double2* src = buf + ridx<D1, D2>(c, 0) + k1 * (D2 + 1);  // ridx(c, k1 D2 + j) - j
 #pragma unroll
-    for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c, k1 * D2 + j)];
+    for (int j = 0; j < D2; ++j) u[j] = src[j];
     rfft<D2>(u, sgn, tab);
 #pragma unroll
     for (int k2 = 0; k2 < NOUT2; ++k2) store(c, k1 + D1 * k2, u[k2]);
@@ -346,8 +381,9 @@ __device__ __forceinline__ void pass2_smem(double2* buf, int ncol, int sgn, cons
     const bool act = item2<D1, D2, CF>(ncol, c, k1);
     double2 u[D2];
     if (act) {
+        const double2* src = buf + ridx<D1, D2>(c, 0) + k1 * (D2 + 1);
 #pragma unroll
-        for (int j = 0; j < D2; ++j) u[j] = buf[ridx<D1, D2>(c, k1 * D2 + j)];
+        for (int j = 0; j < D2; ++j) u[j] = src[j];
         rfft<D2>(u, sgn, tab);
     }
     __syncthreads();

@@ -830,8 +830,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
     __syncthreads();
     // inverse x-FFT of the 3 results (pass 1 in place from shared memory:
     // every item reads and writes only its own (column, n2) elements)
-    freg::pass1<D1, D2, true, D1>(a, NO * nc, +1, tw, tab,
-                                  [&](int col, int n) { return a[freg::ridx<D1, D2>(col, n)]; });
+    freg::pass1_inplace<D1, D2, true>(a, NO * nc, +1, tw, tab);
     __syncthreads();
     freg::pass2<D1, D2, true, D2 / 2>(a, NO * nc, +1, tab, [&](int col, int k, double2 v) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;

@@ -16,10 +16,24 @@ struct FDiv {
 };
 
 inline __host__ __device__ FDiv make_fdiv(uint32_t d) {
+#ifdef __CUDA_ARCH__
+    // kernels build these per CTA: clz instead of the loop, and the 64-bit
+    // quotient from one double division (numerator (2^l - d) 2^32 is exact in
+    // double; the rounded-toward-zero quotient is at most one off) instead of
+    // the ~100-instruction u64 division routine
+    const uint32_t l = d <= 1u ? 0u : 32u - static_cast<uint32_t>(__clz(d - 1u));
+    const uint64_t num = ((1ull << l) - d) << 32;
+    uint64_t q = static_cast<uint64_t>(__ddiv_rz(static_cast<double>(num), static_cast<double>(d)));
+    const int64_t r = static_cast<int64_t>(num - q * d);
+    if (r < 0) --q;
+    else if (r >= static_cast<int64_t>(d)) ++q;
+    return FDiv{d, static_cast<uint32_t>(q + 1), l};
+#else
     uint32_t l = 0;
     while ((1ull << l) < d) ++l;
     const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
     return FDiv{d, static_cast<uint32_t>(m), l};
+#endif
 }
 
 #ifdef __CUDACC__
