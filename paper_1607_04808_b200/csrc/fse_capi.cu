@@ -509,7 +509,8 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
         launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT1], c->s0));
-        launch_fft_xscale(L, fp.host, fp.tw, g, kind, green->d_half, Cs);
+        launch_fft_xscale(L, fp.host, fp.tw, g, kind, green->d_half, Cs,
+                          buf<double>(c, "ex_axis", g.D));
         FSE_CU(cudaEventRecord(c->ev[EV_SCALE], c->s0));
         launch_fft_inverse_yz(L, fp.host, fp.tw, g, a, Cs, Bs, X);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT2], c->s0));
@@ -959,7 +960,8 @@ fse_status fse_cuda_freespace_solve(fse_cuda_ctx* c, const fse_green* green, con
         const FftPlanDev& fp = fft_plan(c, g.D);
         Launch L = L0(c);
         launch_fft_forward_zy(L, fp.host, fp.tw, g, 1, R, Bs, Cs);
-        launch_fft_xscale(L, fp.host, fp.tw, g, KIND_SCALAR_X, green->d_half, Cs);
+        launch_fft_xscale(L, fp.host, fp.tw, g, KIND_SCALAR_X, green->d_half, Cs,
+                          buf<double>(c, "ex_axis", g.D));
         launch_fft_inverse_yz(L, fp.host, fp.tw, g, 1, Cs, Bs, R, 1);
         d2h(c, out, R, vol * sizeof(double));
     });
@@ -1170,7 +1172,8 @@ void slab_scale_impl(fse_cuda_ctx* c, const fse_config* cfg, int kind, const fse
     if (dst_bufs) peers = peer_blocks(c, g, arity_of(kind), rank, nslabs, dst_bufs, "peer_bwd");
     const FftPlanDev& fp = fft_plan(c, g.D);
     launch_fft_xscale(L0(c), fp.host, fp.tw, g, kind, green->d_half,
-                      reinterpret_cast<double2*>(d_spec), dst_bufs ? &peers : nullptr);
+                      reinterpret_cast<double2*>(d_spec), buf<double>(c, "ex_axis", g.D),
+                      dst_bufs ? &peers : nullptr);
     FSE_CU(cudaStreamSynchronize(c->s0));
 }
 

@@ -445,6 +445,16 @@ constexpr int arity_k() { return KIND == FSE_STRESSLET ? 9 : (KIND == KIND_SCALA
 template <int KIND>
 constexpr int nout_k() { return KIND == KIND_SCALAR ? 1 : 3; }
 
+// per-axis factors of the multiplier's exp(-(1 - eta) k^2 / (4 xi^2)):
+// ex[q] = exp(-(1 - eta) kax(q)^2 / (4 xi^2)), q < D (once per call)
+__global__ void k_ex_axis(int D, double dk, double eta, double inv4xi2, double* __restrict__ ex) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < D) {
+        const double kq = dk * (q < D / 2 ? q : q - D);
+        ex[q] = exp(-(1.0 - eta) * (kq * kq) * inv4xi2);
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ void apply(const double k[3], double k2, double gval, double rem,
                                       double inv4xi2, const double2* g, double2* out) {
@@ -504,7 +514,8 @@ template <int ENG, int KIND>
 __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
                                                    GridParams g, int ncol,
                                                    const double* __restrict__ G,
-                                                   double2* __restrict__ Cb, BlockDest dst) {
+                                                   double2* __restrict__ Cb, BlockDest dst,
+                                                   const double* __restrict__ ex_g) {
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
@@ -551,7 +562,8 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
         double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
         const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
                                     __dmul_rn(k[2], k[2]));
-        const double rem = exp(-(1.0 - g.eta) * k2 * g.inv4xi2);
+        // exp(-(1 - eta) k^2 / (4 xi^2)) as the product of its per-axis factors
+        const double rem = __ldg(ex_g + kx) * __ldg(ex_g + ky) * __ldg(ex_g + kz);
         const double gval = Gs[e];
         double2 gh[A];
 #pragma unroll
@@ -756,7 +768,8 @@ template <int ENG, int KIND>
 __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
-                                                    double2* __restrict__ Cb, BlockDest dst) {
+                                                    double2* __restrict__ Cb, BlockDest dst,
+                                                    const double* __restrict__ ex_g) {
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
@@ -780,13 +793,10 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
         const int row = (i + blk * bstep + comp * g.nxs) * g.nkys + kyl;
         return Ck + static_cast<int64_t>(row) * Dh + c;
     };
-    // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (one exp per q per CTA
-    // instead of one per element): rem = ex[kx] * ex[ky] * ex[kz]
+    // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (k_ex_axis, once per
+    // call): rem = ex[kx] * ex[ky] * ex[kz]
     double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
-    for (int q = threadIdx.x; q < D; q += blockDim.x) {
-        const double kq = kax(q, D, g.dk);
-        ex[q] = exp(-(1.0 - g.eta) * (kq * kq) * g.inv4xi2);
-    }
+    for (int q = threadIdx.x; q < D; q += blockDim.x) ex[q] = __ldg(ex_g + q);
     // forward x-FFT of the A components (pass 1 straight from global memory)
     freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
@@ -1233,8 +1243,12 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
 
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                        const GridParams& g, int kind, const double* G, double2* C,
-                       const BlockDest* peers) {
+                       double* d_ex, const BlockDest* peers) {
     upload_consts();
+    if (g.nky <= 0) return;
+    k_ex_axis<<<(h.dev.D + 255) / 256, 256, 0, L.s>>>(h.dev.D, g.dk, g.eta, g.inv4xi2, d_ex);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
     const int A = kind == KIND_SCALAR ? 1 : arity_of(kind);
     // results (3 comps) go back in place (local) or to the x-slab owners
     const BlockDest dst = peers ? *peers : local_blocks(g, A, C);
@@ -1256,31 +1270,31 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
         if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
-                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == FSE_STRESSLET) {
                 allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
-                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == KIND_SCALAR) {
                 allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
-                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else {
                 allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
-                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             }
             return;
         }
         if (kind == FSE_STOKESLET) {
             allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
-            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == FSE_STRESSLET) {
             allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
-            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == KIND_SCALAR) {
             allow_smem(k_xscale<EV, KIND_SCALAR>, sm);
-            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else {
             allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
-            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst);
+            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         }
     });
     FSE_LAUNCH_CHECK();

@@ -87,9 +87,10 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
 // A_eff(k) G(k) / D^3, inverse x-FFT, in place (3 comps out)
 // peers: where the results of each x block go (peer-direct exchange); null =
 // in place
+// d_ex: scratch for the D per-axis exp factors of the multiplier
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                        const GridParams& g, int kind, const double* G, double2* C,
-                       const BlockDest* peers = nullptr);
+                       double* d_ex, const BlockDest* peers = nullptr);
 // C (send layout, 3 comps in blocks of A) -> B (j < Mt) -> W (3 x nx x Mt^2 real)
 void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                            const GridParams& g, int A, double2* C, double2* B, double* W,
