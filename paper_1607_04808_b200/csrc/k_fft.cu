@@ -305,9 +305,17 @@ __device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPl
     return t;
 }
 
+// CTA size per engine.  1200 = 30 x 40 (engine 2): a 40-point register DFT
+// needs more than the 128 registers per thread that 256-thread CTAs at two
+// per SM allow (it spilled ~1 KB per thread), so its CTAs have 128 threads
+// (three columns) and the full 255 registers.
+template <int ENG>
+constexpr int eng_threads() { return ENG == 2 ? 128 : 256; }
+inline int eng_threads_host(int eng) { return eng == 2 ? 128 : 256; }
+
 // ------------------------------------------------------------------ test kernel
 template <int ENG>
-__global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
                                                      double2* data, int ncol_total, int ncol,
                                                      int sgn) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_test(FftPlan pl, const double2* 
 // ------------------------------------------------------------------ z forward
 // column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
 template <int ENG>
-__global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double* __restrict__ R,
                                                  double2* __restrict__ B) {
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(256, 2) k_zfwd(FftPlan pl, const double2* __re
 // forward: columns (comp, i, kz-tile of ncol); input B[comp][i][j][kz], j < Mt
 // inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(256, 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int A, int nxs, int nkys,
                                                   int ncol, double2* __restrict__ B,
                                                   double2* __restrict__ Cb, BlockDest dst) {
@@ -511,7 +519,7 @@ __device__ __forceinline__ double kax(int q, int D, double dk) {
 
 // columns (ky, kz-tile); smem holds a*nc columns: column (comp*nc + c)
 template <int ENG, int KIND>
-__global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
                                                    GridParams g, int ncol,
                                                    const double* __restrict__ G,
                                                    double2* __restrict__ Cb, BlockDest dst,
@@ -602,7 +610,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale(FftPlan pl, const double2* __
 // ------------------------------------------------------------------ z inverse
 // row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
 template <int ENG>
-__global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double2* __restrict__ B,
                                                  double* __restrict__ W) {
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(256, 2) k_zinv(FftPlan pl, const double2* __re
 
 // z forward: column c = row pair (comp, i, jp), rows contiguous -> n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(256, 2) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double* __restrict__ R,
                                                   double2* __restrict__ B) {
@@ -718,7 +726,7 @@ __global__ void __launch_bounds__(256, 2) k_zfwd2(FftPlan pl, const double2* __r
 
 // y passes: column c = (comp, slab plane xl, kz0 + c), columns adjacent in kz -> c-fastest
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
                                                    int Mt, int nx, int A, int nxs, int nkys,
                                                    int ncol, double2* __restrict__ B,
                                                    double2* __restrict__ Cb, BlockDest dst) {
@@ -765,7 +773,7 @@ __global__ void __launch_bounds__(256, 2) k_ypass2(FftPlan pl, const double2* __
 
 // x pass + multiplier: columns (comp, kz0 + c), c-fastest
 template <int ENG, int KIND>
-__global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
                                                     double2* __restrict__ Cb, BlockDest dst,
@@ -853,7 +861,7 @@ __global__ void __launch_bounds__(256, 2) k_xscale2(FftPlan pl, const double2* _
 
 // z inverse: row pairs, Hermitian extension loaded straight from B, n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(256, 2) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double2* __restrict__ B,
                                                   double* __restrict__ W) {
@@ -981,7 +989,9 @@ int v2_mask_for() {
     if (Eng<ENG>::BLUE) return 0;
     const int e = v2_mask_env();
     if (e >= 0) return e;
-    return ENG == 2 ? 0 : (1 | 2 | 4 | 16);
+    // measured per engine on B200: 624 (cfg2) all but the inverse y pass;
+    // 1200 (cfg5) all but the x pass
+    return ENG == 2 ? (1 | 2 | 8 | 16) : (1 | 2 | 4 | 16);
 }
 constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
 
@@ -1103,7 +1113,8 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
         if (smem_bytes(h, cols) > cap) break;
         bool ok = true;
         if (h.eng > 0) {
-            ok = cols * h.D1 <= kThreads && cols * h.D2 <= kThreads;
+            const int T = eng_threads_host(h.eng);
+            ok = cols * h.D1 <= T && cols * h.D2 <= T;
         } else {
             for (int p : h.radices)
                 if (is_reg_radix(p) &&
@@ -1165,7 +1176,7 @@ void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         allow_smem(k_fft_test<EV>, sm);
-        k_fft_test<EV><<<(ncols + u - 1) / u, kThreads, sm, L.s>>>(p, d_tw, data, ncols, u,
+        k_fft_test<EV><<<(ncols + u - 1) / u, eng_threads<EV>(), sm, L.s>>>(p, d_tw, data, ncols, u,
                                                                    inverse ? +1 : -1);
     });
     FSE_LAUNCH_CHECK();
@@ -1201,14 +1212,14 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 1) {
                     allow_smem(k_zfwd2<EV>, sm);
-                    k_zfwd2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                    k_zfwd2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
                 } else {
                     allow_smem(k_zfwd<EV>, sm);
-                    k_zfwd<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                    k_zfwd<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
                 }
             } else {
                 allow_smem(k_zfwd<EV>, sm);
-                k_zfwd<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                k_zfwd<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
@@ -1223,16 +1234,16 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 2) {
                     allow_smem(k_ypass2<EV, false>, sm);
-                    k_ypass2<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                    k_ypass2<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                                    g.nkys, u, B, C, dst);
                 } else {
                     allow_smem(k_ypass<EV, false>, sm);
-                    k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                    k_ypass<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                                   g.nkys, u, B, C, dst);
                 }
             } else {
                 allow_smem(k_ypass<EV, false>, sm);
-                k_ypass<EV, false><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                k_ypass<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                               g.nkys, u, B, C, dst);
             }
             FSE_LAUNCH_CHECK();
@@ -1270,31 +1281,31 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
         if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
-                k_xscale2<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == FSE_STRESSLET) {
                 allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
-                k_xscale2<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == KIND_SCALAR) {
                 allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
-                k_xscale2<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else {
                 allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
-                k_xscale2<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             }
             return;
         }
         if (kind == FSE_STOKESLET) {
             allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
-            k_xscale<EV, FSE_STOKESLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_STOKESLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == FSE_STRESSLET) {
             allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
-            k_xscale<EV, FSE_STRESSLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_STRESSLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == KIND_SCALAR) {
             allow_smem(k_xscale<EV, KIND_SCALAR>, sm);
-            k_xscale<EV, KIND_SCALAR><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, KIND_SCALAR><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else {
             allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
-            k_xscale<EV, FSE_ROTLET><<<blocks, kThreads, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_ROTLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         }
     });
     FSE_LAUNCH_CHECK();
@@ -1320,16 +1331,16 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 8) {
                     allow_smem(k_ypass2<EV, true>, sm);
-                    k_ypass2<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
+                    k_ypass2<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
                                                                   u, B, C, BlockDest{});
                 } else {
                     allow_smem(k_ypass<EV, true>, sm);
-                    k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                    k_ypass<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
                                                                  B, C, BlockDest{});
                 }
             } else {
                 allow_smem(k_ypass<EV, true>, sm);
-                k_ypass<EV, true><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                k_ypass<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
                                                              B, C, BlockDest{});
             }
             FSE_LAUNCH_CHECK();
@@ -1345,14 +1356,14 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE) {
                 if (v2_mask_for<EV>() & 16) {
                     allow_smem(k_zinv2<EV>, sm);
-                    k_zinv2<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                    k_zinv2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
                 } else {
                     allow_smem(k_zinv<EV>, sm);
-                    k_zinv<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                    k_zinv<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
                 }
             } else {
                 allow_smem(k_zinv<EV>, sm);
-                k_zinv<EV><<<nb, kThreads, sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                k_zinv<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
