@@ -467,9 +467,19 @@ class Context:
 
     # -- hot path
     def total_sum(self, system: SourceSystem, kind, cfg: EwaldConfig, targets, green,
-                  timings: StageTimings | None = None, targets_are_sources: int = -1):
+                  timings: StageTimings | None = None, targets_are_sources: int = -1,
+                  out: np.ndarray | None = None):
+        """fse::total_sum (ewald.cpp:394-415).  ``out``: optional (NT, 3) float64
+        C-contiguous array to receive the velocities (e.g. pinned host memory
+        from ``host_alloc``, which the device->host copy reads at full speed)."""
         t = _f64(targets, (-1, 3))
-        u = np.empty((t.shape[0], 3))
+        if out is None:
+            u = np.empty((t.shape[0], 3))
+        else:
+            if (out.shape != (t.shape[0], 3) or out.dtype != np.float64
+                    or not out.flags["C_CONTIGUOUS"]):
+                raise InvalidArgument("total_sum: out must be a C-contiguous (NT, 3) float64 array")
+            u = out
         self._call(_load().fse_cuda_total_sum, C.byref(cfg), int(kind),
                    _p(system.positions), _p(system.strengths), system.size(),
                    float(system.box_side), _p(t), t.shape[0], int(targets_are_sources),

@@ -79,3 +79,19 @@ def test_targets_on_grid_nodes_and_half_nodes(fse, ctx, oracle, rng):
     tgt = np.concatenate([nodes, half])
     pos = rng.uniform(0, 1, (300, 3))
     _check(fse, ctx, oracle, 0, pos, rng.standard_normal((300, 3)), tgt)
+
+
+def test_total_sum_into_pinned_output(fse, ctx, oracle, rng):
+    """total_sum(out=...) writes the same velocities into a caller's (pinned)
+    array; a wrong shape/dtype is rejected before any work."""
+    cfg = fse.make_config(*ARGS)
+    g, _ = _green(fse, ctx, oracle, 0, cfg)
+    pos = rng.random((300, 3))
+    s = fse.SourceSystem(pos, rng.standard_normal((300, 3)), 1.0)
+    want = ctx.total_sum(s, 0, cfg, pos, g)
+    hu = ctx.host_alloc((300, 3))
+    got = ctx.total_sum(s, 0, cfg, pos, g, out=hu)
+    assert got is hu
+    assert np.array_equal(hu, want)
+    with pytest.raises(fse.InvalidArgument):
+        ctx.total_sum(s, 0, cfg, pos, g, out=np.empty((299, 3)))
