@@ -34,7 +34,8 @@ struct Stage {
     double wy[TY][CHP];
     double wz[TZ][CHP];
     double f[3][CHP];
-    int iz[CH];
+    // bit w: the point's z-support meets warp w's 8 z (read 4 points at a time)
+    uint32_t zm4[CH / 4];
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -134,7 +135,9 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         cpa8(&S.f[0][slot], fq, 8);
         cpa8(&S.f[1][slot], fq + 1, 8);
         cpa8(&S.f[2][slot], fq + 2, 8);
-        S.iz[slot] = iz;
+        const uint32_t zb = static_cast<uint32_t>(!(iz > z0n + 7 || iz + P <= z0n)) |
+                            (static_cast<uint32_t>(!(iz > z0n + 15 || iz + P <= z0n + 8)) << 1);
+        reinterpret_cast<uint8_t*>(S.zm4)[slot] = static_cast<uint8_t>(zb);
     };
 
     Cursor cur;
@@ -172,14 +175,11 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         //   A[(x, y)][p] = wx_p[x] wy_p[y]   (m-tile = one x, rows y)
         //   B[p][(c, z)] = f_{c,p} wz_p[z]   (n-tile = one component, 8 z of this warp)
         for (int p0 = 0; p0 < total; p0 += 4) {
-            // warp-uniform skip when no support of the group meets this warp's z range
-            bool hit = false;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int izp = S.iz[min(p0 + j, total - 1)];
-                hit |= !(izp > wz_lo + 7 || izp + P <= wz_lo);
-            }
-            if (!hit) continue;
+            // warp-uniform skip when no support of the group meets this warp's z
+            // range (one byte per point, bytes past `total` are stale: masked)
+            const int left = total - p0;
+            const uint32_t valid = left >= 4 ? 0xffffffffu : (1u << (8 * left)) - 1u;
+            if ((S.zm4[p0 >> 2] & valid & (0x01010101u << warp)) == 0u) continue;
             const int p = p0 + (lane & 3);
             const bool pv = p < total;
             const int pp = pv ? p : p0;
