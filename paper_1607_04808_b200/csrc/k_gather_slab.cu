@@ -25,6 +25,9 @@
 // larger supports use k_gather.cu.
 //
 // Roofline: FP64 tensor (DMMA) -- same ~37 TFLOP/s peak as DFMA on B200.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "fse_internal.cuh"
@@ -246,6 +249,191 @@ __global__ void __launch_bounds__(SW * 32, NST == 2 ? 3 : 2) k_gather_mma(
     }
 }
 
+// ---------------------------------------------------------------- TMA variant
+// Same item, same MMA loop; the slab (all 3 components x P+7 rows y x 34 z)
+// arrives as ONE cp.async.bulk.tensor box per x-plane, issued by one thread
+// and completed on an mbarrier, instead of ~1500 16-byte cp.async per plane
+// issued by all 128 threads (the staging index math was ~2x the MMA loop's
+// instructions).  The box's 34-double rows are exactly the RS = 34 padded
+// layout (two extra z columns are fetched and never read), y rows past the
+// grid edge and z past M~ arrive as zeros (TMA out-of-bounds fill), so the
+// rows are (c, y) with a fixed pitch of P+7 = NYB per component.  Needs an
+// even M~ (16-byte row strides) and KS = 8.
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int z, int y, int x, int c) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(z), "r"(y), "r"(x), "r"(c)
+        : "memory");
+}
+
+template <int MT, int NT, int KS>
+__device__ void gather_item_tma(const GridParams& g, const CUtensorMap* map, double* slab,
+                                uint64_t* bars, const double* b0s, const double* wxs, int x0,
+                                int y0, int z0, int NX, double* red) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows_pad = 8 * MT * SW;
+    const int buf_elems = rows_pad * RS;
+    const unsigned bytes = static_cast<unsigned>(sizeof(double)) * RS * (g.P + 7) * 3;
+    double C[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
+    const int rbase = 8 * MT * warp + (lane >> 2);
+    const int tb = lane >> 2;
+    const int xs0 = max(0, g.x_lo - x0), xs1 = min(NX, g.x_lo + g.nx - x0);
+    auto issue = [&](int xs) {  // one thread: slab xs -> buffer (xs - xs0) & 1
+        const int b = (xs - xs0) & 1;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(bars + b, bytes);
+        tma_load_4d(slab + b * buf_elems, map, bars + b, z0, y0, x0 + xs - g.x_lo, 0);
+    };
+    if (threadIdx.x == 0 && xs0 < xs1) issue(xs0);
+    for (int xs = xs0; xs < xs1; ++xs) {
+        const int i = xs - xs0;
+        if (threadIdx.x == 0 && xs + 1 < xs1) issue(xs + 1);
+        mbar_wait(bars + (i & 1), (i >> 1) & 1);
+        const double* A = slab + (i & 1) * buf_elems + rbase * RS + (lane & 3);
+        double wxt[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) wxt[nt] = wxs[xs * MAXT + 8 * nt + tb];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            double bs[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) bs[nt] = b0s[(ks * 4 + nt) * 32 + lane] * wxt[nt];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const double a = A[8 * mt * RS + 4 * ks];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], a, bs[nt]);
+            }
+        }
+        __syncthreads();  // everyone is done with this buffer before it is refilled
+    }
+    const int tc = 2 * (lane & 3);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int r = rbase + 8 * mt;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            red[r * MAXT + 8 * nt + tc] = C[mt][nt][0];
+            red[r * MAXT + 8 * nt + tc + 1] = C[mt][nt][1];
+        }
+    }
+}
+
+template <int MT, int KS>
+__global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
+    const __grid_constant__ CUtensorMap map, GridParams g, const int32_t* __restrict__ i0s,
+    const double* __restrict__ w, const int32_t* __restrict__ tstart,
+    const int32_t* __restrict__ items, const int32_t* __restrict__ nitems_dev,
+    const uint32_t* __restrict__ perm, double scale, double* __restrict__ u) {
+    extern __shared__ __align__(128) double gsm[];
+    if (static_cast<int>(blockIdx.x) >= *nitems_dev) return;  // CTA-uniform
+    constexpr int ROWS = 8 * MT * SW;
+    double* slab = gsm;                    // [2][ROWS][RS], 128-byte aligned buffers
+    double* wxs = slab + 2 * ROWS * RS;    // [nx][MAXT]
+    double* b0s = wxs + 32 * MAXT;         // [KS][4][32] B fragments (wz)
+    int4* tinfo = reinterpret_cast<int4*>(b0s + KS * 4 * 32);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tinfo + MAXT);
+    const int e = items[2 * blockIdx.x], bi = items[2 * blockIdx.x + 1];
+    const int c = e >> 1, h = e & 1;
+    const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+    const int P = g.P, Mt = g.Mt, NYB = P + 7;
+    const int x0 = cx * 8, y0 = cy * 8, z0 = cz * 16 + 8 * h;
+    const int first = tstart[8 * c + 4 * h] + MAXT * bi;
+    const int n = min(MAXT, tstart[8 * c + 4 * h + 4] - first);
+    const int NX = min(P + 7, Mt - x0), NZ = min(P + 7, Mt - z0);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (tid < MAXT) {
+        int4 ti = make_int4(0, 0, 0, 0);
+        if (tid < n) {
+            const int q = first + tid;
+            ti = make_int4(q, i0s[3 * q], i0s[3 * q + 1], i0s[3 * q + 2]);
+        }
+        tinfo[tid] = ti;
+    }
+    // pad rows (>= 3 NYB) of both buffers stay zero; the boxes never write them
+    for (int idx = tid; idx < 2 * ROWS * RS; idx += SW * 32) {
+        const int r = (idx / RS) % ROWS;
+        if (r >= 3 * NYB) slab[idx] = 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 32 * MAXT; idx += SW * 32) {
+        const int xx = idx / MAXT, t = idx % MAXT;
+        const int4 ti = tinfo[t];
+        const int px = x0 + xx - ti.y;
+        wxs[idx] = (t < n && xx < NX && px >= 0 && px < P)
+                       ? w[static_cast<int64_t>(ti.x) * 3 * P + px]
+                       : 0.0;
+    }
+    for (int idx = tid; idx < KS * 4 * 32; idx += SW * 32) {
+        const int l = idx & 31, nt = (idx >> 5) & 3, ks = idx >> 7;
+        const int t = 8 * nt + (l >> 2), z = 4 * ks + (l & 3);
+        const int4 ti = tinfo[t];
+        const int pz = z0 + z - ti.w;
+        b0s[idx] = (t < n && z < NZ && pz >= 0 && pz < P)
+                       ? w[static_cast<int64_t>(ti.x) * 3 * P + 2 * P + pz]
+                       : 0.0;
+    }
+    __syncthreads();
+    double* red = slab;  // reused after the last slab (ROWS x MAXT <= 2 ROWS RS)
+    const int nt = (n + 7) / 8;
+    if (nt <= 1)
+        gather_item_tma<MT, 1, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+    else if (nt == 2)
+        gather_item_tma<MT, 2, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+    else if (nt == 3)
+        gather_item_tma<MT, 3, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+    else
+        gather_item_tma<MT, 4, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+    __syncthreads();
+    // u_t[c] = h^3 sum_y wy_t[y] red[(c, y)][t]   (rows at the fixed pitch NYB)
+    if (tid < 3 * MAXT) {
+        const int t = tid % MAXT, cc = tid / MAXT;
+        if (t < n) {
+            const int4 ti = tinfo[t];
+            const double* wy = w + static_cast<int64_t>(ti.x) * 3 * P + P;
+            const int yo = ti.z - y0;
+            double s = 0.0;
+            for (int p = 0; p < P; ++p) s = fma(wy[p], red[(cc * NYB + yo + p) * MAXT + t], s);
+            u[3 * static_cast<int64_t>(perm[first + t]) + cc] = scale * s;
+        }
+    }
+}
+
 // items per (coarse tile, z-half): ceil(n / 32)
 __global__ void k_slab_counts(const int32_t* __restrict__ tstart, int64_t nhalf,
                               int32_t* __restrict__ cnt) {
@@ -310,12 +498,62 @@ static void launch_mma(const Launch& L, const GridParams& g, const int32_t* i0s,
         g, i0s, w, tstart, items, nitems_dev, X, perm, scale, u);
 }
 
+// tensor map of the quadrature grid X[c][x][y][z] (3 components of this slab's
+// planes): 4-d, z fastest, box 34 z x (P+7) y x 1 x x 3 c, zero fill outside
+bool encode_grid_map(const GridParams& g, const double* X, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.Mt), static_cast<cuuint64_t>(g.Mt),
+                                static_cast<cuuint64_t>(g.nx), 3};
+    const cuuint64_t strides[3] = {sizeof(double) * static_cast<cuuint64_t>(g.rowp),
+                                   sizeof(double) * static_cast<cuuint64_t>(g.plane),
+                                   sizeof(double) * static_cast<cuuint64_t>(g.comp)};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(RS), static_cast<cuuint32_t>(g.P + 7), 1, 3};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool gather_tma_enabled(const GridParams& g) {
+    static const bool off = [] {
+        const char* e = std::getenv("FSE_GATHER_TMA");
+        return e && std::atoi(e) == 0;
+    }();
+    return !off && g.Mt % 2 == 0 && ks_for(g.P) == 8 && mt_for(g.P) == 3 && g.nx > 0;
+}
+
 void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                         const int32_t* tstart, const int32_t* items, int64_t max_items,
                         const int32_t* nitems_dev, const double* X, const uint32_t* perm,
                         double scale, double* u) {
     if (max_items <= 0) return;
     const int ks = ks_for(g.P), mt = mt_for(g.P);
+    CUtensorMap map;
+    if (gather_tma_enabled(g) && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+        encode_grid_map(g, X, &map)) {
+        constexpr int ROWS = 8 * 3 * SW;
+        const size_t sm = sizeof(double) * (2 * static_cast<size_t>(ROWS) * RS + 32 * MAXT +
+                                            8 * 4 * 32) +
+                          sizeof(int4) * MAXT + 2 * sizeof(uint64_t);
+        FSE_CU(cudaFuncSetAttribute(k_gather_tma<3, 8>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+        k_gather_tma<3, 8><<<static_cast<unsigned>(max_items), SW * 32, sm, L.s>>>(
+            map, g, i0s, w, tstart, items, nitems_dev, perm, scale, u);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+        return;
+    }
 #define FSE_MMA_CASE(M_, K_)                                                                   \
     if (mt == M_ && ks == K_) {                                                                \
         launch_mma<M_, K_>(L, g, i0s, w, tstart, items, max_items, nitems_dev, X, perm, scale, \
