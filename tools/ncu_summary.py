@@ -101,7 +101,8 @@ def full(path):
         print(f"| {short(r[ki])} | " + " | ".join(cells) + " |")
 
 
-STAGE_OF = {"k_spread": "spread", "k_gather_mma": "gather", "k_realspace": "realspace",
+STAGE_OF = {"k_spread": "spread", "k_gather_mma": "gather", "k_gather_tma": "gather",
+            "k_realspace": "realspace",
             "k_xscale": "kscale", "k_xscale2": "kscale"}
 
 
