@@ -529,7 +529,21 @@ bool gather_tma_enabled(const GridParams& g) {
         const char* e = std::getenv("FSE_GATHER_TMA");
         return e && std::atoi(e) == 0;
     }();
-    return !off && g.Mt % 2 == 0 && ks_for(g.P) == 8 && mt_for(g.P) == 3 && g.nx > 0;
+    return !off && g.Mt % 2 == 0 && g.nx > 0;
+}
+
+template <int MT, int KS>
+void launch_tma(const Launch& L, const CUtensorMap& map, const GridParams& g, const int32_t* i0s,
+                const double* w, const int32_t* tstart, const int32_t* items, int64_t max_items,
+                const int32_t* nitems_dev, const uint32_t* perm, double scale, double* u) {
+    constexpr int ROWS = 8 * MT * SW;
+    const size_t sm = sizeof(double) * (2 * static_cast<size_t>(ROWS) * RS + 32 * MAXT +
+                                        KS * 4 * 32) +
+                      sizeof(int4) * MAXT + 2 * sizeof(uint64_t);
+    FSE_CU(cudaFuncSetAttribute(k_gather_tma<MT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+    k_gather_tma<MT, KS><<<static_cast<unsigned>(max_items), SW * 32, sm, L.s>>>(
+        map, g, i0s, w, tstart, items, nitems_dev, perm, scale, u);
 }
 
 void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
@@ -541,18 +555,23 @@ void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s
     CUtensorMap map;
     if (gather_tma_enabled(g) && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
         encode_grid_map(g, X, &map)) {
-        constexpr int ROWS = 8 * 3 * SW;
-        const size_t sm = sizeof(double) * (2 * static_cast<size_t>(ROWS) * RS + 32 * MAXT +
-                                            8 * 4 * 32) +
-                          sizeof(int4) * MAXT + 2 * sizeof(uint64_t);
-        FSE_CU(cudaFuncSetAttribute(k_gather_tma<3, 8>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sm)));
-        k_gather_tma<3, 8><<<static_cast<unsigned>(max_items), SW * 32, sm, L.s>>>(
-            map, g, i0s, w, tstart, items, nitems_dev, perm, scale, u);
-        FSE_LAUNCH_CHECK();
-        ++*L.launches;
-        return;
+#define FSE_TMA_CASE(M_, K_)                                                                   \
+    if (mt == M_ && ks == K_) {                                                                \
+        launch_tma<M_, K_>(L, map, g, i0s, w, tstart, items, max_items, nitems_dev, perm,      \
+                           scale, u);                                                          \
+        FSE_LAUNCH_CHECK();                                                                    \
+        ++*L.launches;                                                                         \
+        return;                                                                                \
+    }
+        FSE_TMA_CASE(3, 8)
+        FSE_TMA_CASE(3, 7)
+        FSE_TMA_CASE(3, 6)
+        FSE_TMA_CASE(2, 7)
+        FSE_TMA_CASE(2, 6)
+        FSE_TMA_CASE(2, 5)
+        FSE_TMA_CASE(2, 4)
+        FSE_TMA_CASE(1, 4)
+#undef FSE_TMA_CASE
     }
 #define FSE_MMA_CASE(M_, K_)                                                                   \
     if (mt == M_ && ks == K_) {                                                                \

@@ -1,5 +1,5 @@
 """The quadrature's two staging paths give bit-identical velocities: the
-TMA box per x-plane (k_gather_tma: even M~, P = 22..25) and the per-thread
+TMA box per x-plane (k_gather_tma: even M~, every tensor-core tile shape) and the per-thread
 cp.async staging (k_gather_mma), selected with FSE_GATHER_TMA in a fresh
 process (the switch is read once per process)."""
 import os
@@ -39,7 +39,9 @@ def _run(tmp_path, args, tma):
     return np.load(out), int(r.stdout.split()[-1])
 
 
-@pytest.mark.parametrize("args", [(1.0, 15.28, 0.25, 40, 24), (1.0, 20.0, 0.2, 62, 22)])
+@pytest.mark.parametrize("args", [(1.0, 15.28, 0.25, 40, 24), (1.0, 20.0, 0.2, 62, 22),
+                                  (1.0, 10.0, 0.25, 32, 16), (1.0, 8.0, 0.3, 31, 12),
+                                  (1.0, 6.0, 0.3, 24, 8)])
 def test_tma_and_cp_async_staging_agree(tmp_path, args):
     a, mt = _run(tmp_path, args, 1)
     b, _ = _run(tmp_path, args, 0)
