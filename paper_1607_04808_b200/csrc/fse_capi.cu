@@ -682,7 +682,11 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
         cufftHandle pi;
         size_t ws = 0;
         FSE_CUFFT(cufftCreate(&pi));
-        FSE_CUFFT(cufftMakePlan3d(pi, sM, sM, sM, CUFFT_Z2D, &ws));
+        // 64-bit plan API: sM^3 exceeds 2^31 elements from sM = 1291 (cfg5: 1640),
+        // where the 32-bit cufftMakePlan3d of CUDA 12.9's cuFFT fails
+        long long nI[3] = {sM, sM, sM};
+        FSE_CUFFT(cufftMakePlanMany64(pi, 3, nI, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1,
+                                      &ws));
         FSE_CUFFT(cufftSetStream(pi, c->s0));
         FSE_CUFFT(cufftExecZ2D(pi, reinterpret_cast<cufftDoubleComplex*>(S), S));
         const double scale = 1.0 / (static_cast<double>(sM) * sM * sM);
@@ -692,7 +696,9 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
         cufftDestroy(pi);
         cufftHandle pf;
         FSE_CUFFT(cufftCreate(&pf));
-        FSE_CUFFT(cufftMakePlan3d(pf, D, D, D, CUFFT_D2Z, &ws));
+        long long nF[3] = {D, D, D};
+        FSE_CUFFT(cufftMakePlanMany64(pf, 3, nF, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1,
+                                      &ws));
         FSE_CUFFT(cufftSetStream(pf, c->s0));
         FSE_CUFFT(cufftExecD2Z(pf, T, reinterpret_cast<cufftDoubleComplex*>(T)));
         launch_green_real(L, reinterpret_cast<const double2*>(T),

@@ -518,8 +518,22 @@ __device__ __forceinline__ double kax(int q, int D, double dk) {
 }
 
 // columns (ky, kz-tile); smem holds a*nc columns: column (comp*nc + c)
+// x-pass CTA size: the stresslet's nine input columns of one kz need
+// 9 max(D1, D2) threads, more than the engine's default CTA for 1200 = 30 x 40,
+// 704 = 22 x 32 and the 1024-point Bluestein engine: those launch 384-thread
+// CTAs (one per SM).
 template <int ENG, int KIND>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
+constexpr int xs_threads() {
+    return (KIND == FSE_STRESSLET && ENG > 0 &&
+            9 * (Eng<ENG>::D1 > Eng<ENG>::D2 ? Eng<ENG>::D1 : Eng<ENG>::D2) > eng_threads<ENG>())
+               ? 384
+               : eng_threads<ENG>();
+}
+template <int ENG, int KIND>
+constexpr int xs_minb() { return xs_threads<ENG, KIND>() > 256 ? 1 : 2; }
+
+template <int ENG, int KIND>
+__global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>()) k_xscale(FftPlan pl, const double2* __restrict__ tw_g,
                                                    GridParams g, int ncol,
                                                    const double* __restrict__ G,
                                                    double2* __restrict__ Cb, BlockDest dst,
@@ -773,7 +787,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass2(FftPlan pl, co
 
 // x pass + multiplier: columns (comp, kz0 + c), c-fastest
 template <int ENG, int KIND>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>()) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
                                                     double2* __restrict__ Cb, BlockDest dst,
@@ -1105,7 +1119,7 @@ size_t smem_bytes(const HostFftPlan& h, int cols) {
 
 // largest number of units (each `cols_per_unit` columns) that fits the
 // shared-memory cap and the engine's per-thread work limits
-int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
+int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap, int threads) {
     const int D = h.dev.D;
     int best = 0;
     for (int u = 1; u <= 64; ++u) {
@@ -1113,7 +1127,7 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
         if (smem_bytes(h, cols) > cap) break;
         bool ok = true;
         if (h.eng > 0) {
-            const int T = eng_threads_host(h.eng);
+            const int T = threads > 0 ? threads : eng_threads_host(h.eng);
             ok = cols * h.D1 <= T && cols * h.D2 <= T;
         } else {
             for (int p : h.radices)
@@ -1128,9 +1142,9 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap) {
 }
 
 // two CTAs per SM when possible, otherwise one CTA with up to ~220 KB
-int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit) {
+int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit, int threads = 0) {
     for (size_t cap : {kSmemCap, static_cast<size_t>(220 * 1024)}) {
-        int u = units_per_cta(h, cols_per_unit, cap);
+        int u = units_per_cta(h, cols_per_unit, cap, threads);
         while (u > 0 && smem_bytes(h, u * cols_per_unit) + extra_per_unit * u > cap) --u;
         if (u > 0) return u;
     }
@@ -1268,7 +1282,12 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     int xmask = 0;
     with_engine(h.eng, [&](auto E) { xmask = v2_mask_for<decltype(E)::value>(); });
     const size_t gcol = (h.eng > 0 && (xmask & 4)) ? 0 : sizeof(double) * static_cast<size_t>(D);
-    const int u = std::min(units_fit(h, A, gcol), Dh);
+    // the stresslet's 9 columns may need a larger CTA (xs_threads)
+    const int mx = std::max(h.D1, h.D2);
+    const int xthr = (A == 9 && h.eng > 0 && 9 * mx > eng_threads_host(h.eng))
+                         ? 384
+                         : eng_threads_host(h.eng);
+    const int u = std::min(units_fit(h, A, gcol, xthr), Dh);
     FftPlan p = h.dev;
     set_buf(p, h, A * u);
     // v2: exp factor table (D doubles) after the twiddles
@@ -1281,31 +1300,31 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
         if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
-                k_xscale2<EV, FSE_STOKESLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, xs_threads<EV, FSE_STOKESLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == FSE_STRESSLET) {
                 allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
-                k_xscale2<EV, FSE_STRESSLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, xs_threads<EV, FSE_STRESSLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else if (kind == KIND_SCALAR) {
                 allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
-                k_xscale2<EV, KIND_SCALAR><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, xs_threads<EV, KIND_SCALAR>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             } else {
                 allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
-                k_xscale2<EV, FSE_ROTLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, xs_threads<EV, FSE_ROTLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
             }
             return;
         }
         if (kind == FSE_STOKESLET) {
             allow_smem(k_xscale<EV, FSE_STOKESLET>, sm);
-            k_xscale<EV, FSE_STOKESLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_STOKESLET><<<blocks, xs_threads<EV, FSE_STOKESLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == FSE_STRESSLET) {
             allow_smem(k_xscale<EV, FSE_STRESSLET>, sm);
-            k_xscale<EV, FSE_STRESSLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_STRESSLET><<<blocks, xs_threads<EV, FSE_STRESSLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else if (kind == KIND_SCALAR) {
             allow_smem(k_xscale<EV, KIND_SCALAR>, sm);
-            k_xscale<EV, KIND_SCALAR><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, KIND_SCALAR><<<blocks, xs_threads<EV, KIND_SCALAR>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         } else {
             allow_smem(k_xscale<EV, FSE_ROTLET>, sm);
-            k_xscale<EV, FSE_ROTLET><<<blocks, eng_threads<EV>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            k_xscale<EV, FSE_ROTLET><<<blocks, xs_threads<EV, FSE_ROTLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
         }
     });
     FSE_LAUNCH_CHECK();
