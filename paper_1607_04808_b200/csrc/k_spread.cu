@@ -17,6 +17,8 @@
 //
 // Roofline: FP64 FMA (2 a P^3 flops per point, ~100 flop/B); HBM traffic is
 // the weights (3P doubles per point) plus one write of the grid.
+#include <type_traits>
+
 #include "fse_internal.cuh"
 
 namespace fsecu {
@@ -174,14 +176,17 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         // groups of 4 points = one k-step of m8n8k4:
         //   A[(x, y)][p] = wx_p[x] wy_p[y]   (m-tile = one x, rows y)
         //   B[p][(c, z)] = f_{c,p} wz_p[z]   (n-tile = one component, 8 z of this warp)
-        for (int p0 = 0; p0 < total; p0 += 4) {
+        // one k-step of 4 points; FULL: all 4 slots hold points of this chunk
+        // (every group but possibly the last), so no tail masking/selects
+        auto group = [&](int p0, auto full) {
+            constexpr bool FULL = decltype(full)::value;
             // warp-uniform skip when no support of the group meets this warp's z
-            // range (one byte per point, bytes past `total` are stale: masked)
-            const int left = total - p0;
-            const uint32_t valid = left >= 4 ? 0xffffffffu : (1u << (8 * left)) - 1u;
-            if ((S.zm4[p0 >> 2] & valid & (0x01010101u << warp)) == 0u) continue;
+            // range (one byte per point; bytes past `total` are stale: masked)
+            uint32_t zm = S.zm4[p0 >> 2] & (0x01010101u << warp);
+            if (!FULL) zm &= (1u << (8 * (total - p0))) - 1u;
+            if (zm == 0u) return;
             const int p = p0 + (lane & 3);
-            const bool pv = p < total;
+            const bool pv = FULL || p < total;
             const int pp = pv ? p : p0;
             const double wyv = pv ? S.wy[lane >> 2][pp] : 0.0;
             const double wzv = pv ? S.wz[wz_off + (lane >> 2)][pp] : 0.0;
@@ -192,7 +197,10 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dmma(C[r][c][0], C[r][c][1], ar, bf[c]);
             }
-        }
+        };
+        int p0 = 0;
+        for (; p0 + 4 <= total; p0 += 4) group(p0, std::true_type{});
+        if (p0 < total) group(p0, std::false_type{});
         cur = nxt;
         k = kn;
         b ^= 1;
