@@ -522,7 +522,7 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
             const int64_t nhalf = g.nkeys / 4;  // (coarse tile, z-half) pairs
             int32_t* scnt = buf<int32_t>(c, "scnt", nhalf + 1);
             int32_t* soff = buf<int32_t>(c, "soff", nhalf + 1);
-            launch_slab_counts(L, tg.tstart, nhalf, scnt);
+            launch_slab_counts(L, g, tg.tstart, nhalf, scnt);
             exclusive_scan(c, c->s0, "s0", scnt, soff, nhalf + 1);
             const int64_t max_items = std::min<int64_t>(nhalf, nt) + (nt + 31) / 32;
             int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
@@ -1249,11 +1249,15 @@ fse_status fse_cuda_slab_inverse(fse_cuda_ctx* c, const fse_config* cfg, int kin
         const int64_t nhalf = g.nkeys / 4;
         int32_t* scnt = buf<int32_t>(c, "scnt", nhalf + 1);
         int32_t* soff = buf<int32_t>(c, "soff", nhalf + 1);
-        launch_slab_counts(L, tg.tstart, nhalf, scnt);
+        launch_slab_counts(L, g, tg.tstart, nhalf, scnt);
         exclusive_scan(c, c->s0, "s0", scnt, soff, nhalf + 1);
         const int64_t max_items = std::min<int64_t>(nhalf, nt) + (nt + 31) / 32;
         int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
         launch_slab_fill(L, soff, nhalf, sitems);
+        // tiles whose union box misses this slab get no items: their targets'
+        // partial velocities are zero
+        if (nslabs > 1 && nt > 0)
+            FSE_CU(cudaMemsetAsync(d_u, 0, sizeof(double) * 3 * nt, c->s0));
         if (nt > 0)
             launch_gather_slab(L, g, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff + nhalf, W,
                                tg.perm, g.h * g.h * g.h, d_u);

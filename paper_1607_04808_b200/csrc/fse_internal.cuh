@@ -159,7 +159,8 @@ int gather_group_size();
 // slab-staged gather (k_gather.cu): items = (coarse tile, z-half, batch of 32)
 bool gather_slab_enabled(const GridParams& g);
 size_t slab_smem_bytes(const GridParams& g);
-void launch_slab_counts(const Launch& L, const int32_t* tstart, int64_t nhalf, int32_t* cnt);
+void launch_slab_counts(const Launch& L, const GridParams& g, const int32_t* tstart,
+                        int64_t nhalf, int32_t* cnt);
 void launch_slab_fill(const Launch& L, const int32_t* off, int64_t nhalf, int32_t* items);
 void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                         const int32_t* tstart, const int32_t* items, int64_t max_items,

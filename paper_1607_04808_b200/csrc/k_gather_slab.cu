@@ -435,12 +435,19 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
 }
 
 // items per (coarse tile, z-half): ceil(n / 32)
-__global__ void k_slab_counts(const int32_t* __restrict__ tstart, int64_t nhalf,
-                              int32_t* __restrict__ cnt) {
+// A (coarse tile, z-half) whose union box [x0, x0 + P + 7) misses this
+// slab's planes [x_lo, x_lo + nx) gets no items: with several slabs each rank
+// only visits the tiles that reach its planes (their targets' partial
+// velocities are zero here, the caller clears u first).
+__global__ void k_slab_counts(const int32_t* __restrict__ tstart, int64_t nhalf, int ncz,
+                              int ncy, int x_lo, int nx, int span, int32_t* __restrict__ cnt) {
     const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (e < nhalf) {
         const int n = tstart[4 * e + 4] - tstart[4 * e];
-        cnt[e] = (n + MAXT - 1) / MAXT;
+        const int64_t c = e >> 1;
+        const int x0 = static_cast<int>(c / (static_cast<int64_t>(ncz) * ncy)) * 8;
+        const bool meets = x0 < x_lo + nx && x0 + span > x_lo;
+        cnt[e] = meets ? (n + MAXT - 1) / MAXT : 0;
     }
     if (e == nhalf) cnt[e] = 0;
 }
@@ -474,8 +481,10 @@ bool gather_slab_enabled(const GridParams& g) {
     return !off && g.P + 7 <= 32 && ks >= 4 && ks <= 8 && mt >= 1 && mt <= 3;
 }
 
-void launch_slab_counts(const Launch& L, const int32_t* tstart, int64_t nhalf, int32_t* cnt) {
-    k_slab_counts<<<static_cast<unsigned>((nhalf + 256) / 256), 256, 0, L.s>>>(tstart, nhalf, cnt);
+void launch_slab_counts(const Launch& L, const GridParams& g, const int32_t* tstart,
+                        int64_t nhalf, int32_t* cnt) {
+    k_slab_counts<<<static_cast<unsigned>((nhalf + 256) / 256), 256, 0, L.s>>>(
+        tstart, nhalf, g.ncz, g.ncy, g.x_lo, g.nx, g.P + 7, cnt);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
