@@ -392,9 +392,11 @@ Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, con
 // real-space pair sum on s1 into d_uR (caller order).  No host sync: the
 // pair kernel is launched over an upper bound of work items and reads the
 // true count from device memory.
+// part / nparts > 1: only the targets in x-slice `part` of the cell grid
+// (whole cells, so work items stay full); the others' d_uR entries are zero
 void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_str, int64_t n,
                double box_side, double xi, double rc, const double* d_tgt, int64_t nt, bool tas,
-               double* d_uR) {
+               double* d_uR, int part = 0, int nparts = 1) {
     if (!(xi > 0) || !(rc > 0)) invalid("real_space_sum: xi and rc must be positive");
     const int a = arity_of(kind);
     const CellGrid cg = cell_grid(n, box_side, rc, 0.0);
@@ -404,7 +406,14 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     int32_t* icnt = buf<int32_t>(c, "rs_icnt", cg.ncell + 1);
     int32_t* ioff = buf<int32_t>(c, "rs_ioff", cg.ncell + 1);
     const int per = realspace_item_size();
-    launch_item_counts(L, tgt.start, cg.ncell, per, icnt);
+    int64_t c_lo = 0, c_hi = -1;
+    if (nparts > 1) {  // cells are (i dim + j) dim + k: x-slices are contiguous
+        const int64_t plane = static_cast<int64_t>(cg.dim) * cg.dim;
+        c_lo = plane * (static_cast<int64_t>(cg.dim) * part / nparts);
+        c_hi = plane * (static_cast<int64_t>(cg.dim) * (part + 1) / nparts);
+        if (nt > 0) FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
+    }
+    launch_item_counts(L, tgt.start, cg.ncell, per, icnt, c_lo, c_hi);
     exclusive_scan(c, c->s1, "s1", icnt, ioff, cg.ncell + 1);
     const int64_t max_items = std::min<int64_t>(cg.ncell, nt) + (nt + per - 1) / per;
     int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(max_items));
@@ -1229,14 +1238,14 @@ fse_status fse_cuda_slab_inverse(fse_cuda_ctx* c, const fse_config* cfg, int kin
         const GridParams g = slab_params(cfg, rank, nslabs);
         FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
         Launch L = L0(c);
-        // real space + self term for this rank's share of the targets (stream s1)
-        const int64_t t_lo = nt * rank / nslabs, t_hi = nt * (rank + 1) / nslabs;
-        double* uR = buf<double>(c, "uR", 3 * std::max<int64_t>(t_hi - t_lo, 1));
+        // real space for the targets in this rank's x-slice of the cell grid
+        // (stream s1); rank 0 adds the self term
+        double* uR = buf<double>(c, "uR", 3 * std::max<int64_t>(nt, 1));
         FSE_CU(cudaEventRecord(c->ev[EV_START], c->s0));
         FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_START], 0));
-        if (t_hi > t_lo)
-            real_part(c, kind, d_pos, d_str, n, cfg->L, cfg->xi, cfg->rc, d_tgt + 3 * t_lo,
-                      t_hi - t_lo, false, uR);
+        if (nt > 0)
+            real_part(c, kind, d_pos, d_str, n, cfg->L, cfg->xi, cfg->rc, d_tgt, nt, tas != 0, uR,
+                      rank, nslabs);
         FSE_CU(cudaEventRecord(c->ev[EV_JOIN], c->s1));
         // inverse y/z passes of this slab, then its planes' share of the quadrature
         double* qtab = buf<double>(c, "qtab", g.P);
@@ -1262,10 +1271,10 @@ fse_status fse_cuda_slab_inverse(fse_cuda_ctx* c, const fse_config* cfg, int kin
             launch_gather_slab(L, g, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff + nhalf, W,
                                tg.perm, g.h * g.h * g.h, d_u);
         FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_JOIN], 0));
-        if (t_hi > t_lo) {
-            const bool self = tas && kind == FSE_STOKESLET;
-            launch_epilogue(L, t_hi - t_lo, d_u + 3 * t_lo, uR, self ? d_str + 3 * t_lo : nullptr,
-                            self ? -4.0 * cfg->xi / std::sqrt(M_PI) : 0.0, d_u + 3 * t_lo);
+        if (nt > 0) {
+            const bool self = tas && kind == FSE_STOKESLET && rank == 0;
+            launch_epilogue(L, nt, d_u, uR, self ? d_str : nullptr,
+                            self ? -4.0 * cfg->xi / std::sqrt(M_PI) : 0.0, d_u);
         }
         raise_flags(c);
     });

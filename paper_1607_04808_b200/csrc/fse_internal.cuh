@@ -182,8 +182,9 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
                       double xi, double rc, unsigned long long* counts, double* uR);
 int realspace_item_size();  // targets per work item
+// items per cell; only cells in [c_lo, c_hi) get any (c_hi < 0: all cells)
 void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
-                        int32_t* cnt);
+                        int32_t* cnt, int64_t c_lo = 0, int64_t c_hi = -1);
 void launch_fill_items(const Launch& L, const int32_t* start, const int32_t* off, int64_t ncell,
                        int per, int32_t* items);
 

@@ -422,10 +422,14 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     }
 }
 
+// items of cell c: ceil(targets / per) for cells in [c_lo, c_hi), else none
+// (a slab rank's share of the real-space work: whole x-slices of cells, so
+// every item keeps its full warp of targets)
 __global__ void k_item_counts(const int32_t* __restrict__ start, int64_t ncell, int per,
-                              int32_t* __restrict__ cnt) {
+                              int64_t c_lo, int64_t c_hi, int32_t* __restrict__ cnt) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (c < ncell) cnt[c] = (start[c + 1] - start[c] + per - 1) / per;
+    if (c < ncell)
+        cnt[c] = (c >= c_lo && c < c_hi) ? (start[c + 1] - start[c] + per - 1) / per : 0;
     if (c == ncell) cnt[c] = 0;
 }
 
@@ -496,9 +500,9 @@ void ensure_tables() {
 int realspace_item_size() { return 32; }
 
 void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
-                        int32_t* cnt) {
-    k_item_counts<<<static_cast<unsigned>((ncell + 256) / 256), 256, 0, L.s>>>(start, ncell, per,
-                                                                             cnt);
+                        int32_t* cnt, int64_t c_lo, int64_t c_hi) {
+    k_item_counts<<<static_cast<unsigned>((ncell + 256) / 256), 256, 0, L.s>>>(
+        start, ncell, per, c_lo, c_hi < 0 ? ncell : c_hi, cnt);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
