@@ -338,7 +338,9 @@ Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
     launch_histogram(L, keys2, n, counts);
     exclusive_scan(c, c->s0, "s0", counts, s.tstart, g.nkeys + 1);
     if (d_str && c->str_pending) FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_H2D], 0));
-    launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true);
+    // sources of one z-slab: only points whose support reaches its planes need weights
+    launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true,
+                          d_str != nullptr && g.nx < g.Mt);
     return s;
 }
 

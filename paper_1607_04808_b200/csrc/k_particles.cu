@@ -71,42 +71,56 @@ __global__ void k_quad_table(GridParams g, double* q) {
 __global__ void k_payload(GridParams g, const double* __restrict__ pos,
                           const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
                           int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
-                          double* __restrict__ w, double* __restrict__ fs, bool fold_prefac) {
+                          double* __restrict__ w, double* __restrict__ fs, bool fold_prefac,
+                          bool slab_only) {
     extern __shared__ double stage[];
+    __shared__ bool keep_row[128];
     const int P = g.P, W3 = 3 * P, RS = W3 + 1;
     const int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x);
     const int64_t q = q0 + threadIdx.x;
+    bool keep = false;
     if (q < n) {
         const int64_t idx = perm[q];
-        double* row = stage + threadIdx.x * RS;
-#pragma unroll 1
+        double s[3];
+        int first[3];
+#pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-            const double x = pos[3 * idx + ax];
-            const double s = __ddiv_rn(__dsub_rn(x, g.origin), g.h);
-            int first = static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
-            const double x0 = (first - s) * g.h;
-            const double e0 = exp(-g.alpha * x0 * x0);
-            const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
-            const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
-            double r = 1.0;
-            for (int p = 0; p < P; ++p) {
-                row[ax * P + p] = scale * (e0 * r * qtab[p]);
-                r *= ratio;
-            }
-            if (first < 0) first = 0;
-            if (first + P > g.Mt) first = g.Mt - P;
-            i0s[3 * q + ax] = first;
+            s[ax] = __ddiv_rn(__dsub_rn(pos[3 * idx + ax], g.origin), g.h);
+            first[ax] = static_cast<int>(ceil(__dsub_rn(s[ax], 0.5 * P)));
+            int f = first[ax] < 0 ? 0 : first[ax];
+            if (f + P > g.Mt) f = g.Mt - P;
+            i0s[3 * q + ax] = f;
         }
-        if (fs)
-            for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
+        // slab_only: a point whose x support misses this slab's planes is never
+        // read by its spread tiles, so its weights are not computed or written
+        const int fx = i0s[3 * q];
+        keep = !slab_only || (fx + P > g.x_lo && fx < g.x_lo + g.nx);
+        if (keep) {
+            double* row = stage + threadIdx.x * RS;
+#pragma unroll 1
+            for (int ax = 0; ax < 3; ++ax) {
+                const double x0 = (first[ax] - s[ax]) * g.h;
+                const double e0 = exp(-g.alpha * x0 * x0);
+                const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
+                const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
+                double r = 1.0;
+                for (int p = 0; p < P; ++p) {
+                    row[ax * P + p] = scale * (e0 * r * qtab[p]);
+                    r *= ratio;
+                }
+            }
+            if (fs)
+                for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
+        }
     }
+    keep_row[threadIdx.x] = keep;
     __syncthreads();
     const int64_t left = n - q0;
     const int cnt = static_cast<int>(left < blockDim.x ? left : blockDim.x);
     double* out = w + q0 * W3;
     for (int e = threadIdx.x; e < cnt * W3; e += blockDim.x) {
         const int t = e / W3;
-        out[e] = stage[t * RS + (e - t * W3)];
+        if (keep_row[t]) out[e] = stage[t * RS + (e - t * W3)];
     }
 }
 
@@ -176,7 +190,7 @@ void launch_quad_table(const Launch& L, const GridParams& g, double* q) {
 void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
                            const double* str, int a, const uint32_t* perm, int64_t n,
                            const double* qtab, int32_t* i0s, double* w, double* fs,
-                           bool fold_prefac) {
+                           bool fold_prefac, bool slab_only) {
     if (n <= 0) return;
     // block size: as many warps (<= 4) as fit 48 KB of staged weight rows;
     // wider supports take one warp and opt-in shared memory
@@ -190,7 +204,8 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
                                     static_cast<int>(row_bytes * tpb)));
     }
     k_payload<<<blocks_for(n, tpb), tpb, row_bytes * tpb, L.s>>>(g, pos, str, a, perm, n, qtab,
-                                                                  i0s, w, fs, fold_prefac);
+                                                                  i0s, w, fs, fold_prefac,
+                                                                  slab_only);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
