@@ -338,9 +338,10 @@ Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
     launch_histogram(L, keys2, n, counts);
     exclusive_scan(c, c->s0, "s0", counts, s.tstart, g.nkeys + 1);
     if (d_str && c->str_pending) FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_H2D], 0));
-    // sources of one z-slab: only points whose support reaches its planes need weights
+    // one z-slab: weights only for the sources whose support reaches its planes
+    // and the targets of the quadrature items that do (k_slab_counts)
     launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true,
-                          d_str != nullptr && g.nx < g.Mt);
+                          g.nx < g.Mt ? (d_str != nullptr ? 1 : 2) : 0);
     return s;
 }
 

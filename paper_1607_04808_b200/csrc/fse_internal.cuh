@@ -113,7 +113,7 @@ void launch_quad_table(const Launch& L, const GridParams& g, double* q);
 void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
                            const double* str, int a, const uint32_t* perm, int64_t n,
                            const double* qtab, int32_t* i0s, double* w, double* fs,
-                           bool fold_prefac, bool slab_only = false);
+                           bool fold_prefac, int slab_only = 0);
 // histogram of keys into counts (size nkeys, zeroed by caller)
 void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts);
 // cell ids of points for the reference cell list (realspace.cpp:60-63,80)

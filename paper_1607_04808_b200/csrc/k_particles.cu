@@ -72,7 +72,7 @@ __global__ void k_payload(GridParams g, const double* __restrict__ pos,
                           const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
                           int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
                           double* __restrict__ w, double* __restrict__ fs, bool fold_prefac,
-                          bool slab_only) {
+                          int slab_only) {
     extern __shared__ double stage[];
     __shared__ bool keep_row[128];
     const int P = g.P, W3 = 3 * P, RS = W3 + 1;
@@ -91,10 +91,15 @@ __global__ void k_payload(GridParams g, const double* __restrict__ pos,
             if (f + P > g.Mt) f = g.Mt - P;
             i0s[3 * q + ax] = f;
         }
-        // slab_only: a point whose x support misses this slab's planes is never
-        // read by its spread tiles, so its weights are not computed or written
+        // slab_only 1 (sources): a point whose x support misses this slab's
+        // planes is never read by its spread tiles; 2 (targets): a target whose
+        // coarse tile's union box misses them is in no quadrature item
+        // (k_slab_counts).  Such points get no weights.
         const int fx = i0s[3 * q];
-        keep = !slab_only || (fx + P > g.x_lo && fx < g.x_lo + g.nx);
+        const int x0 = (fx >> 3) * 8;
+        keep = slab_only == 0 ||
+               (slab_only == 1 ? (fx + P > g.x_lo && fx < g.x_lo + g.nx)
+                               : (x0 < g.x_lo + g.nx && x0 + P + 7 > g.x_lo));
         if (keep) {
             double* row = stage + threadIdx.x * RS;
 #pragma unroll 1
@@ -190,7 +195,7 @@ void launch_quad_table(const Launch& L, const GridParams& g, double* q) {
 void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
                            const double* str, int a, const uint32_t* perm, int64_t n,
                            const double* qtab, int32_t* i0s, double* w, double* fs,
-                           bool fold_prefac, bool slab_only) {
+                           bool fold_prefac, int slab_only) {
     if (n <= 0) return;
     // block size: as many warps (<= 4) as fit 48 KB of staged weight rows;
     // wider supports take one warp and opt-in shared memory
