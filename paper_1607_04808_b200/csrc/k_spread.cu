@@ -32,10 +32,13 @@ constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = 2;
 // fragment reads (4 points x 8 rows) spread over all banks
 constexpr int CHP = CH + 4;
 struct Stage {
-    double wx[TX][CHP];
+    // wx and f are read 4 consecutive points of one row at a time (no
+    // conflicts unpadded); wy and wz rows are read 8 at a time (padded).
+    // Unpadded they bring the CTA to 37.5 KB: six CTAs per SM instead of five.
+    double wx[TX][CH];
     double wy[TY][CHP];
     double wz[TZ][CHP];
-    double f[3][CHP];
+    double f[3][CH];
     // bit w: the point's z-support meets warp w's 8 z (read 4 points at a time)
     uint32_t zm4[CH / 4];
 };
