@@ -687,13 +687,32 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
     const int D = 2 * Mt;
     Launch L = L0(c);
     fse_green* g = new_green(c, gkind, Ltilde, Mt, h, R);
+    // cuFFT plans and the sM^3 scratch (tens of GB at cfg5) are released on
+    // every exit, including a failed plan or allocation
+    struct Scratch {
+        fse_cuda_ctx* c;
+        cufftHandle plans[2] = {0, 0};
+        bool live[2] = {false, false};
+        ~Scratch() {
+            for (int i = 0; i < 2; ++i)
+                if (live[i]) cufftDestroy(plans[i]);
+            for (const char* nm : {"green_S", "green_T"}) {
+                auto it = c->bufs.find(nm);
+                if (it != c->bufs.end() && it->second.p) {
+                    cudaFree(it->second.p);
+                    it->second = DevBuf{};
+                }
+            }
+        }
+    } scratch{c};
     try {
         const int64_t sMp = sM + 2;
         double* S = buf<double>(c, "green_S", static_cast<size_t>(sM) * sM * sMp);
         launch_green_fill(L, gkind, sM, dk, R, reinterpret_cast<double2*>(S));
-        cufftHandle pi;
+        cufftHandle& pi = scratch.plans[0];
         size_t ws = 0;
         FSE_CUFFT(cufftCreate(&pi));
+        scratch.live[0] = true;
         // 64-bit plan API: sM^3 exceeds 2^31 elements from sM = 1291 (cfg5: 1640),
         // where the 32-bit cufftMakePlan3d of CUDA 12.9's cuFFT fails
         long long nI[3] = {sM, sM, sM};
@@ -705,9 +724,9 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
         double* T = buf<double>(c, "green_T", static_cast<size_t>(D) * D * (D + 2));
         launch_green_window(L, sM, sMp, Mt, S, scale, T);
         FSE_CU(cudaStreamSynchronize(c->s0));
-        cufftDestroy(pi);
-        cufftHandle pf;
+        cufftHandle& pf = scratch.plans[1];
         FSE_CUFFT(cufftCreate(&pf));
+        scratch.live[1] = true;
         long long nF[3] = {D, D, D};
         FSE_CUFFT(cufftMakePlanMany64(pf, 3, nF, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1,
                                       &ws));
@@ -716,13 +735,6 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
         launch_green_real(L, reinterpret_cast<const double2*>(T),
                           static_cast<int64_t>(D) * D * (D / 2 + 1), g->d_half);
         FSE_CU(cudaStreamSynchronize(c->s0));
-        cufftDestroy(pf);
-        // the scratch is large (sM^3): give it back
-        for (const char* nm : {"green_S", "green_T"}) {
-            DevBuf& b = c->bufs[nm];
-            if (b.p) FSE_CU(cudaFree(b.p));
-            b = DevBuf{};
-        }
     } catch (...) {
         cudaFree(g->d_half);
         delete g;
