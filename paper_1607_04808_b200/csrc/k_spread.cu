@@ -1,19 +1,21 @@
 // k_spread.cu -- Gaussian spreading (ewald.cpp:136-214), atomics-free.
 //
 // Ownership instead of atomics: one CTA owns an 8 x 8 x 16 tile of grid
-// nodes and is the only writer of it.  Each of its 2 warps owns the z-half
-// (8 z) of all 8 x 8 (x, y) rows, and accumulates it on the FP64 tensor
-// cores: for every group of 4 points (one k-step of mma.m8n8k4.f64)
+// nodes and is the only writer of it.  Each of its 4 warps owns one
+// (x-half, z-half) of the tile -- 4 x-rows x 8 y x 8 z -- and accumulates it
+// on the FP64 tensor cores: for every group of 4 points (one k-step of
+// mma.m8n8k4.f64)
 //     G_c[(x, y)][z] += sum_p (wx_p[x] wy_p[y]) (f_{c,p} wz_p[z]),
-// 8 x-m-tiles x 3 component-n-tiles = 24 MMAs per group from 12 fragment
-// products (1 DMUL each).  The CTA streams, in tile-key order, every
-// point whose P^3 support meets the tile (points are pre-sorted by the tile
-// of their support start i0, so those points sit in 4 x 4 contiguous
-// key ranges), stages the slices of their separable weights that fall on the
-// tile in shared memory (wx[8], wy[8], wz[16], f[3] per point; cp.async,
-// double-buffered so the next chunk's copies overlap this chunk's FMAs), and every lane
-// accumulates in registers: no shared-memory read-modify-write, no global
-// atomics; fixed order (deterministic).
+// 4 x-m-tiles x 3 component-n-tiles = 12 MMAs per group from 7 fragment
+// products (1 DMUL each); a group none of whose supports meets the warp's
+// domain is skipped (one staged byte per point).  The CTA streams, in
+// tile-key order, every point whose P^3 support meets the tile (points are
+// pre-sorted by the tile of their support start i0, so those points sit in
+// 4 x 4 contiguous key ranges), stages the slices of their separable weights
+// that fall on the tile in shared memory (wx[8], wy[8], wz[16], f[3] per
+// point; cp.async, double-buffered so the next chunk's copies overlap this
+// chunk's MMAs), and every lane accumulates in registers: no shared-memory
+// read-modify-write, no global atomics; fixed order (deterministic).
 //
 // Roofline: FP64 FMA (2 a P^3 flops per point, ~100 flop/B); HBM traffic is
 // the weights (3P doubles per point) plus one write of the grid.
@@ -25,7 +27,19 @@ namespace fsecu {
 
 namespace {
 
-constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = 2;
+#ifndef FSE_SPREAD_NWARP
+#define FSE_SPREAD_NWARP 4
+#endif
+// NWARP = 2: warp w owns z [8w, 8w + 8) of all 8 x-rows; NWARP = 4: warp w
+// owns x-rows [4 (w % 2), +4) and z [8 (w / 2), +8).  CH = 64 points per chunk
+// (staged by the first 64 threads).
+constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = FSE_SPREAD_NWARP;
+constexpr int XS = NWARP / 2, XW = TX / XS;  // x splits, x-rows per warp
+// 4 warps: (x-half, z-half) domains, 96 registers for five CTAs per SM
+// (cfg2 spread 7.28 -> 6.60 ms against 2 warps with all 8 x-rows each)
+#ifndef FSE_SPREAD_MINB
+#define FSE_SPREAD_MINB 5
+#endif
 
 // element-major staging ([element][point], point stride CHP = CH + 4): the
 // per-thread staging writes of a warp are consecutive doubles and the MMA
@@ -61,7 +75,7 @@ struct Cursor {
     int kx, ky, base, qend;
 };
 
-__global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32_t* __restrict__ i0s,
+__global__ void __launch_bounds__(NWARP * 32, FSE_SPREAD_MINB) k_spread(GridParams g, const int32_t* __restrict__ i0s,
                                                        const double* __restrict__ w,
                                                        const double* __restrict__ fs, int a, int c0,
                                                        const int32_t* __restrict__ tstart,
@@ -75,14 +89,15 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
     const int tx = g.x_lo / TX + tile / (g.ncz * g.ncy);  // this slab's x tiles
     const int x0n = tx * TX, y0n = ty * TY, z0n = tz * TZ;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // warp w owns z in [z0n + 8w, +8) of all 8 x 8 (x, y) rows of the tile
-    const int wz_off = warp * 8;
+    // warp w owns x-rows [wx_off, +XW) and z [wz_lo, +8) of the tile
+    const int wx_off = (warp % XS) * XW;
+    const int wz_off = (warp / XS) * 8;
     const int wz_lo = z0n + wz_off;
 
-    // MMA accumulators: C[x][c] holds G_c[x0n + x][y0n + lane/4][wz_lo + 2 (lane%4) + {0,1}]
-    double C[TX][3][2];
+    // MMA accumulators: C[x][c] holds G_c[x0n + wx_off + x][y0n + lane/4][wz_lo + 2 (lane%4) + {0,1}]
+    double C[XW][3][2];
 #pragma unroll
-    for (int r = 0; r < TX; ++r)
+    for (int r = 0; r < XW; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) C[r][c][0] = C[r][c][1] = 0.0;
 
@@ -108,7 +123,7 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
     // per-chunk metadata: which of this thread's point is kept (support meets the tile)
     auto meta = [&](const Cursor& c, int& q, int& ix, int& iy, int& iz) -> bool {
         q = c.base + tid;
-        if (q >= c.qend) return false;
+        if (tid >= CH || q >= c.qend) return false;
         ix = i0s[3 * q];
         iy = i0s[3 * q + 1];
         iz = i0s[3 * q + 2];
@@ -140,8 +155,13 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
         cpa8(&S.f[0][slot], fq, 8);
         cpa8(&S.f[1][slot], fq + 1, 8);
         cpa8(&S.f[2][slot], fq + 2, 8);
-        const uint32_t zb = static_cast<uint32_t>(!(iz > z0n + 7 || iz + P <= z0n)) |
-                            (static_cast<uint32_t>(!(iz > z0n + 15 || iz + P <= z0n + 8)) << 1);
+        uint32_t zb = 0;  // bit w: the support meets warp w's x-rows and z range
+#pragma unroll
+        for (int ww = 0; ww < NWARP; ++ww) {
+            const int xa = x0n + (ww % XS) * XW, za = z0n + (ww / XS) * 8;
+            const bool in = !(ix > xa + XW - 1 || ix + P <= xa) && !(iz > za + 7 || iz + P <= za);
+            zb |= static_cast<uint32_t>(in) << ww;
+        }
         reinterpret_cast<uint8_t*>(S.zm4)[slot] = static_cast<uint8_t>(zb);
     };
 
@@ -195,8 +215,8 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
             const double wzv = pv ? S.wz[wz_off + (lane >> 2)][pp] : 0.0;
             const double bf[3] = {S.f[0][pp] * wzv, S.f[1][pp] * wzv, S.f[2][pp] * wzv};
 #pragma unroll
-            for (int r = 0; r < TX; ++r) {
-                const double ar = S.wx[r][pp] * wyv;
+            for (int r = 0; r < XW; ++r) {
+                const double ar = S.wx[wx_off + r][pp] * wyv;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dmma(C[r][c][0], C[r][c][1], ar, bf[c]);
             }
@@ -214,8 +234,8 @@ __global__ void __launch_bounds__(NWARP * 32) k_spread(GridParams g, const int32
     const bool z1 = z + 1 < g.Mt;
     const bool vec = z1 && (g.Mt % 2 == 0);  // 16-byte aligned pairs
 #pragma unroll
-    for (int r = 0; r < TX; ++r) {
-        const int x = x0n + r;
+    for (int r = 0; r < XW; ++r) {
+        const int x = x0n + wx_off + r;
         if (x >= g.x_lo + g.nx) break;
         const int64_t off = (x - g.x_lo) * g.plane + y * g.rowp + z;  // slab-local plane
 #pragma unroll
