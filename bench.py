@@ -17,11 +17,17 @@ e2e   : targets/s through the reference-facing C-ABI call with HOST buffers
         of the velocities inside the timed region, wall clock;
 roofline : the dominant kernel of the step, achieved = algorithmic bytes or
         flops per launch (DESIGN.md) / its CUDA-event duration;
-cpu_baseline : the reference compiled from its own sources (oracle/_ref) on a
-        bounded same-density sample, rank 0, N=1 only.
+cpu_baseline : the reference compiled from its own sources (oracle/_ref) timed
+        on this host at the SAME workload: one full fse::total_sum call (its
+        Green's precompute excluded, as harness.hpp:50 does), rank 0, N=1 only;
+--impl reference : the same reference call, warm-up + timed steps until K or a
+        time budget (--ref-budget-s) is reached (reported as "steps"); inputs
+        from the reference-side generator (oracle/ref_capi.cpp), so the arm
+        never loads the product library.
 
-N > 1 (torchrun): every rank runs the full workload on its own GPU (replicas,
-weak scaling; the z-slab decomposition is the next multi-GPU step).
+N > 1 (torchrun, or `--gpus N` which relaunches itself under torchrun): one
+evaluation decomposed into N z-slabs (slabs.py, DESIGN.md section 6);
+--replicas runs N independent full evaluations instead.
 """
 from __future__ import annotations
 
@@ -365,7 +371,7 @@ def run_slabs(args, dist: Dist):
                    "exchange_note": why,
                    "slab": {"x_lo": ss.info.x_lo, "nx": ss.info.nx, "ky_lo": ss.info.ky_lo,
                             "nky": ss.info.nky},
-                   "l2": "working set >> 126 MB L2; no flush needed"},
+                   "l2": working_set_note(w, cfg)},
         "e2e": {"value": nt * max(1, args.steps) / e2e_s, "unit": "targets/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * 3 * nt),
                 "api": "slabs.SlabSum.run_peers (fse_cuda_slab_*_peers + symmetric memory)"
@@ -500,11 +506,11 @@ def run_ours(args, dist: Dist):
     roof["ms"] = stage_ms[dom]
     roof["peak_src"] = pk["hbm_src"] if roof["bound"] == "hbm" else \
         "measured in this run (DFMA loop, fse_cuda_fp64_peak)"
-    roof["traffic"] = traffic_for(dom)
+    roof["traffic"] = traffic_for(args.workload, dom)
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(w, frac=8, threads=None)
+        cpu = cpu_baseline_line(w)
 
     value = dist.world * nt * args.steps / (max_ms * 1e-3)
     line = {
@@ -516,8 +522,7 @@ def run_ours(args, dist: Dist):
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
                    "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
                    "eta": round(cfg.eta, 4), "parallelism": f"replicas x{dist.world}",
-                   "l2": "working set (3 x 1.95 GB spectrum + 0.6 GB weights) >> 126 MB L2; "
-                         "no flush needed",
+                   "l2": working_set_note(w, cfg),
                    "green_precompute_s": round(precompute_s, 3)},
         "e2e": {"value": nt * e2e_steps * dist.world / e2e_s, "unit": "targets/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -539,14 +544,29 @@ def run_ours(args, dist: Dist):
         ctx.dev_free(p)
 
 
-def traffic_for(kernel: str):
-    """dram bytes per launch from the committed ncu capture, if any."""
+def traffic_for(workload: str, kernel: str):
+    """dram read+write bytes per launch of `kernel` at `workload` from the committed
+    ncu --set full capture (profiles/traffic.json, keyed by workload), else None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         t = json.load(f)
-    return t.get(kernel)
+    return (t.get(workload) or {}).get(kernel)
+
+
+def working_set_note(w, cfg):
+    """Bytes the Fourier part streams per step vs the 126 MB L2."""
+    a = 9 if w["kind"] == 1 else 3
+    D, Mt = cfg.D, cfg.Mtilde
+    Dh = D // 2 + 1
+    ws = a * (8 * Mt ** 3 + 16 * Mt * Mt * Dh + 16 * Mt * D * Dh) + 8 * D * D * Dh
+    ws += w["n"] * (24 + 8 * a + 24 * cfg.P)
+    gb = ws / 1e9
+    if ws > 8 * 126e6:
+        return f"working set ~{gb:.2f} GB >> 126 MB L2 (inputs larger than L2): no flush needed"
+    return (f"working set ~{gb:.2f} GB, not >> 126 MB L2: part of it may stay L2-resident "
+            "between steps (no explicit flush)")
 
 
 # ------------------------------------------------------------------ reference CPU
@@ -558,92 +578,141 @@ def _avail_bytes():
         return 16 << 30
 
 
-def cpu_reference_sample(w, frac: int, threads):
-    """Time the reference (oracle/_ref: its own sources, OpenMP) on a same-density
-    sub-box of the workload: N/frac points in a box of side L/frac^(1/3) with the same
-    h, xi, rc, P (so spreading, quadrature and real-space work per point are those of
-    the full run) and extrapolate each StageTimings field: per-point stages x frac,
-    FFT x (D^3 log D^3 ratio), scale x (D^3 ratio)."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_full(w, steps: int, warmup: int, budget_s: float):
+    """Time the UNMODIFIED reference fse::total_sum (oracle/_ref: /root/reference
+    sources compiled by oracle/Makefile, OpenMP) on this host at the full workload.
+    Inputs from the reference-side generator (oracle/ref_capi.cpp), the Green's
+    table from the reference's own precompute_mollified_green (excluded from the
+    timing, as harness.hpp:50 does).  `warmup` untimed calls, then timed calls
+    until `steps` are done or `budget_s` of timed calls has elapsed (>= 1).
+    Threads: every host thread, capped so the reference's memory (a private
+    Mtilde^3 spread grid per thread, ewald.cpp:166-176, plus the C2C spectra)
+    fits in 85 % of available RAM.  Returns (result dict, None) or (None, why)."""
     from oracle import refimpl as R
     if not R.available():
-        return {"value": None, "unit": "targets/s", "cores": 0, "kind": "reference",
-                "sample": "oracle/_ref not built"}
-    side = frac ** (-1.0 / 3.0)
-    Ms = int(round(w["M"] * side))
-    side = Ms / w["M"]  # keep h identical
-    kind = w["kind"]
-    import paper_1607_04808_b200 as fse
-    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED)
-    pos = system.positions
-    inside = np.all(pos < side, axis=1)
-    pos = pos[inside]
-    st = system.strengths[inside]
-    nts = pos.shape[0]
-    cfg_s = R.make_config(side, w["xi"], w["rc"], Ms, w["P"])
-    cfg_f = R.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+        return None, "oracle/_ref (the reference built from its sources) is missing"
+    cfg = R.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    a = 9 if w["kind"] == 1 else 3
+    D, Mt = cfg.D, cfg.Mtilde
+    fixed = a * 8 * Mt ** 3 + (a + 3) * 16 * D ** 3 + 8 * D ** 3 + w["n"] * (48 + 8 * a) * 3
+    per_thread = a * 8 * Mt ** 3
+    avail = 0.85 * _avail_bytes()
     cores = os.cpu_count() or 1
-    grid_bytes = 8 * (9 if kind == 1 else 3) * cfg_s.Mtilde ** 3
-    cap = max(1, int(0.4 * _avail_bytes() / max(grid_bytes, 1)))
-    nthr = threads or min(cores, cap)
-    R.set_threads(nthr)
-    green = np.zeros((cfg_s.D,) * 3)
-    green[0, 0, 0] = 1.0  # timing only: the table's values do not change the work
-    tsum = {}
-    tgt_s = pos if tgt is None else np.ascontiguousarray(tgt[np.all(tgt < side, axis=1)])
-    R.total_sum(cfg_s, kind, pos, st, tgt_s, green, timings=tsum)
-    Ds, Df = cfg_s.D, cfg_f.D
-    fft_scale = (Df ** 3 * math.log(Df ** 3)) / (Ds ** 3 * math.log(Ds ** 3))
-    n_full = w["n"]
-    per_pt = n_full / nts
-    est = (tsum["spread"] * per_pt + tsum["quadrature"] * (n_full / tgt_s.shape[0]) +
-           tsum["realspace"] * (n_full / tgt_s.shape[0]) + tsum["fft"] * fft_scale +
-           tsum["scale"] * (Df / Ds) ** 3)
-    return {"value": n_full / est, "unit": "targets/s", "cores": nthr, "kind": "reference",
-            "sample": (f"reference total_sum on a same-density sub-box: N={nts} points, "
-                       f"L={side:.4f}, M={Ms} (Mtilde={cfg_s.Mtilde}, D={Ds}), same h/xi/rc/P; "
-                       f"stages extrapolated to N={n_full}, D={Df}: per-point x{per_pt:.2f}, "
-                       f"fft x{fft_scale:.2f} (n log n), scale x{(Df / Ds) ** 3:.2f}; "
-                       "FFT single-threaded as the reference is written (FFTW-API shim)"),
-            "sample_seconds": tsum["total"],
-            "stages_s_extrapolated": {"spread": tsum["spread"] * per_pt,
-                                      "fft": tsum["fft"] * fft_scale,
-                                      "scale": tsum["scale"] * (Df / Ds) ** 3,
-                                      "quadrature": tsum["quadrature"] * per_pt,
-                                      "realspace": tsum["realspace"] * per_pt},
-            "est_total_s": est}
+    thr = min(cores, int((avail - fixed) // per_thread)) if avail > fixed else 0
+    if thr < 1:
+        return None, (f"reference total_sum needs ~{(fixed + per_thread) / 1e9:.0f} GB of host "
+                      f"RAM; {avail / 0.85 / 1e9:.0f} GB available")
+    R.set_threads(thr)
+    pos, st, tgt = R.generate_workload(w["wl"], w["n"], SEED)
+    targets = pos if tgt is None else tgt
+    t0 = time.perf_counter()
+    green = R.precompute_green(R.green_kind_for(w["kind"]), cfg.Ltilde, cfg.Mtilde, cfg.sf)
+    pre_s = time.perf_counter() - t0
+    times, stages = [], []
+    i = 0
+    while True:
+        tm = {}
+        t0 = time.perf_counter()
+        R.total_sum(cfg, w["kind"], pos, st, targets, green, timings=tm)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+            stages.append(tm)
+        i += 1
+        if i >= warmup + steps or (times and sum(times) >= budget_s):
+            break
+    med = float(np.median(times))
+    keys = ("spread", "fft", "scale", "quadrature", "realspace", "total")
+    st_med = {k: float(np.median([s[k] for s in stages])) for k in keys}
+    return {"seconds": times, "median_s": med, "threads": thr, "cores": cores,
+            "cpu": _cpu_model(), "precompute_s": pre_s, "stages_s": st_med,
+            "warmup": min(warmup, i), "nt": targets.shape[0]}, None
 
 
-def run_reference(args, dist: Dist):
-    if dist.rank != 0:
+REF_NOTE = ("the reference's own sources (oracle/_ref, g++ -O2 -fopenmp), FFTs through "
+            "oracle/fftw_shim (FFTW3 is absent; the shim is OpenMP-parallel over 1D lines, "
+            "i.e. faster than the reference's single-threaded FFTW as written, fft.cpp)")
+
+
+def cpu_baseline_line(w):
+    r, why = reference_full(w, steps=1, warmup=0, budget_s=0.0)
+    if r is None:
+        return {"value": None, "unit": "targets/s", "cores": 0, "kind": "reference",
+                "sample": f"not run: {why}"}
+    return {"value": r["nt"] / r["median_s"], "unit": "targets/s", "cores": r["threads"],
+            "kind": "reference",
+            "sample": (f"one full fse::total_sum call at the bench workload ({w['desc']}), "
+                       f"no sub-sampling or extrapolation; {REF_NOTE}; {r['threads']} OpenMP "
+                       f"threads of {r['cores']} ({r['cpu']}); Green's precompute "
+                       f"({r['precompute_s']:.1f} s) excluded as harness.hpp:50 does"),
+            "seconds": r["median_s"], "stages_s": r["stages_s"]}
+
+
+def run_reference(args):
+    """--impl reference: rank 0 only (other torchrun ranks exit 0 without work)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     w = WORKLOADS[args.workload]
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(w, frac=args.ref_frac, threads=None)
-        if r["value"] is None:
-            emit({"impl": "reference", "unavailable": r["sample"]})
-            return
-        if i >= args.warmup:
-            vals.append(r["est_total_s"])
-        info = r
-    t = float(np.mean(vals))
-    v = w["n"] / t
-    info = dict(info)
-    info["value"] = v
+    r, why = reference_full(w, steps=max(1, args.steps), warmup=min(args.warmup, 1),
+                            budget_s=args.ref_budget_s)
+    if r is None:
+        emit({"impl": "reference", "unavailable": why})
+        return
+    v = r["nt"] / r["median_s"]
     line = {
         "impl": "reference", "metric": metric_name(w), "value": v, "unit": "targets/s",
-        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (seed {SEED})",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(r["seconds"]),
+        "warmup": r["warmup"], "ms_per_step": r["median_s"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (seed {SEED}), reference-side "
+                "generator (oracle/ref_capi.cpp), no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
-                   "parallelism": "host CPU (OpenMP), rank 0 only"},
-        "cpu_baseline": info,
+                   "N": w["n"], "NT": r["nt"], "parallelism": "host CPU (OpenMP), rank 0 only",
+                   "steps_requested": args.steps, "warmup_requested": args.warmup,
+                   "step_note": (f"timed calls stop at {args.steps} or once {args.ref_budget_s:.0f} s "
+                                 "of timed calls have elapsed; ms_per_step = median of the "
+                                 "timed calls, each a full-size call (no extrapolation)"),
+                   "seconds_per_call": [round(x, 3) for x in r["seconds"]],
+                   "product_library_loaded": _product_loaded()},
+        "cpu_baseline": {"value": v, "unit": "targets/s", "cores": r["threads"],
+                         "kind": "reference",
+                         "sample": (f"full fse::total_sum calls at the bench workload; {REF_NOTE}; "
+                                    f"{r['threads']} OpenMP threads of {r['cores']} ({r['cpu']}); "
+                                    f"Green's precompute ({r['precompute_s']:.1f} s) excluded"),
+                         "stages_s": r["stages_s"]},
         "e2e": {"value": v, "unit": "targets/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     emit(line)
+
+
+def _product_loaded() -> bool:
+    """Whether this process mapped libfse_b200.so (the reference arm must not)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return "libfse_b200" in f.read()
+    except OSError:
+        return False
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: run N ranks on this node."""
+    port = os.environ.get("MASTER_PORT", "29533")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -661,19 +730,25 @@ def main():
                          "with a verified fallback to NCCL (auto, N > 1)")
     ap.add_argument("--slabs", action="store_true",
                     help="use the z-slab path also at N = 1 (one slab, NCCL group of one)")
-    ap.add_argument("--ref-frac", type=int, default=64,
-                    help="--impl reference: sample = 1/ref_frac of the points per step")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: stop timing full-size calls after this many seconds")
     ap.add_argument("--fp64-peak", type=float, default=None,
                     help="TFLOP/s; default: measured in-run with a DFMA loop")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     _stdout_to_stderr()
+    if args.impl == "reference":
+        run_reference(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     dist = Dist(force_group=args.slabs and args.impl == "ours")
     try:
-        if args.impl == "reference":
-            run_reference(args, dist)
-        elif (dist.world > 1 and not args.replicas) or args.slabs:
+        if (dist.world > 1 and not args.replicas) or args.slabs:
             run_slabs(args, dist)
         else:
             run_ours(args, dist)

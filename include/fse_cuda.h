@@ -215,6 +215,12 @@ fse_status fse_cuda_real_space_sum(fse_cuda_ctx* ctx, int kind, const double* po
 fse_status fse_cuda_spread(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
                            const double* pos, const double* str, int64_t n, double box_side,
                            double* grid);
+/* spread(..., use_fgg) (ewald.hpp:45-46): use_fgg = 0 builds the per-axis weights with
+ * one exp per node (axis_weights_naive, ewald.cpp:53-66) instead of the FGG
+ * recurrence (ewald.cpp:33-51) */
+fse_status fse_cuda_spread_ex(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                              const double* pos, const double* str, int64_t n, double box_side,
+                              int use_fgg, double* grid);
 /* replaces fse::kspace_scale (ewald.cpp:216-293) on full D^3 interleaved complex
  * planes: ghat a planes in, 3 planes out (D = 2 Mtilde) */
 fse_status fse_cuda_kspace_scale(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
@@ -237,6 +243,16 @@ fse_status fse_cuda_direct_sum(fse_cuda_ctx* ctx, int kind, const double* pos,
 /* the FFT seam (fft.hpp:11,14): in-place 3D C2C on interleaved complex host data;
  * inverse scales by 1/(n0 n1 n2) */
 fse_status fse_cuda_fft3d(fse_cuda_ctx* ctx, double* data, int n0, int n1, int n2, int inverse);
+/* diagnostics: the fused x pass of the hot path (forward x-FFT, k-space multiplier
+ * with the Nyquist-exact Hermitian average and 1/D^3, inverse x-FFT, window x < Mtilde;
+ * the kspace_scale of ewald.cpp:216-293 on the pruned layout) applied to a pseudo-random
+ * spectrum C[c][x][ky][kz] = splitmix64-derived values (seed), with the Green's table of
+ * `green`, or (green == NULL) a pseudo-random half table.  Returns out = nprobe x 3 x
+ * Mtilde complex (interleaved) results at the columns (ky[p], kz[p]) and gcol = nprobe x D
+ * the table values G[kx][ky[p]][kz[p]] used there. */
+fse_status fse_cuda_xscale_probe(fse_cuda_ctx* ctx, const fse_config* cfg, int kind,
+                                 const fse_green* green, uint64_t seed, int nprobe,
+                                 const int* ky, const int* kz, double* out, double* gcol);
 /* diagnostics: the hand-written fp64 FFT engine of the hot path on `ncols` contiguous
  * interleaved-complex columns of length D, in place, unnormalised (sign -1 / +1) */
 fse_status fse_cuda_fft_columns(fse_cuda_ctx* ctx, int D, int ncols, double* data, int inverse);

@@ -247,48 +247,166 @@ void fc_exec1d(fc_plan1d* p, double* data) {
     if (src != data) memcpy(data, src, sizeof(double) * 2 * (size_t)n);
 }
 
-/* Transform `count` lines of length n, line b starting at data + b*1 (complex
- * units) with element stride `stride`; lines are gathered in blocks. */
-static void lines_strided(double* data, size_t nlines_outer, size_t outer_stride, int n,
-                          size_t stride, size_t count, fc_plan1d* plan) {
-    enum { B = 16 };
-    double* buf = (double*)malloc(sizeof(double) * 2 * (size_t)n * B);
-    for (size_t o = 0; o < nlines_outer; ++o) {
-        double* base = data + 2 * o * outer_stride;
-        for (size_t c0 = 0; c0 < count; c0 += B) {
-            const size_t nb = count - c0 < B ? count - c0 : B;
-            for (int j = 0; j < n; ++j) {
-                const double* src = base + 2 * ((size_t)j * stride + c0);
-                for (size_t b = 0; b < nb; ++b) {
-                    buf[2 * (b * n + j)] = src[2 * b];
-                    buf[2 * (b * n + j) + 1] = src[2 * b + 1];
-                }
-            }
-            for (size_t b = 0; b < nb; ++b) fc_exec1d(plan, buf + 2 * b * n);
-            for (int j = 0; j < n; ++j) {
-                double* dst = base + 2 * ((size_t)j * stride + c0);
-                for (size_t b = 0; b < nb; ++b) {
-                    dst[2 * b] = buf[2 * (b * n + j)];
-                    dst[2 * b + 1] = buf[2 * (b * n + j) + 1];
+/* ---- batched path: LB lines at once, layout buf[j][b] (line index fastest),
+ * so every butterfly's inner loop runs over LB independent lines with the
+ * same twiddle (vectorisable).  Same per-element arithmetic as run_stage. */
+enum { LB = 16 };
+
+static void run_stage_batch(const fc_stage* st, int n, int sign, const double* in,
+                            double* out) {
+    const int p = st->p, Ns = st->Ns, stride = n / p;
+    double v[2 * FC_GENERIC_MAX * LB];
+    for (int j = 0; j < stride; ++j) {
+        const int k = j % Ns;
+        for (int r = 0; r < p; ++r)
+            memcpy(&v[2 * r * LB], &in[2 * (size_t)(j + r * stride) * LB], sizeof(double) * 2 * LB);
+        if (k != 0) {
+            const double* tw = &st->tw[2 * (size_t)k * (p - 1)];
+            for (int r = 1; r < p; ++r) {
+                const double c = tw[2 * (r - 1)], d = tw[2 * (r - 1) + 1];
+                double* x = &v[2 * r * LB];
+                for (int b = 0; b < LB; ++b) {
+                    const double a = x[2 * b], e = x[2 * b + 1];
+                    x[2 * b] = a * c - e * d;
+                    x[2 * b + 1] = a * d + e * c;
                 }
             }
         }
+        const int base = (j / Ns) * Ns * p + k;
+        double* o[FC_GENERIC_MAX];
+        for (int r = 0; r < p; ++r) o[r] = &out[2 * (size_t)(base + r * Ns) * LB];
+        if (p == 2) {
+            for (int b = 0; b < LB; ++b) {
+                const double* x0 = &v[2 * b];
+                const double* x1 = &v[2 * (LB + b)];
+                o[0][2 * b] = x0[0] + x1[0]; o[0][2 * b + 1] = x0[1] + x1[1];
+                o[1][2 * b] = x0[0] - x1[0]; o[1][2 * b + 1] = x0[1] - x1[1];
+            }
+        } else if (p == 4) {
+            for (int b = 0; b < LB; ++b) {
+                const double* x0 = &v[2 * b];
+                const double* x1 = &v[2 * (LB + b)];
+                const double* x2 = &v[2 * (2 * LB + b)];
+                const double* x3 = &v[2 * (3 * LB + b)];
+                double s0r = x0[0] + x2[0], s0i = x0[1] + x2[1];
+                double d0r = x0[0] - x2[0], d0i = x0[1] - x2[1];
+                double s1r = x1[0] + x3[0], s1i = x1[1] + x3[1];
+                double d1r = x1[0] - x3[0], d1i = x1[1] - x3[1];
+                double jr = -sign * d1i, ji = sign * d1r;
+                o[0][2 * b] = s0r + s1r; o[0][2 * b + 1] = s0i + s1i;
+                o[1][2 * b] = d0r + jr;  o[1][2 * b + 1] = d0i + ji;
+                o[2][2 * b] = s0r - s1r; o[2][2 * b + 1] = s0i - s1i;
+                o[3][2 * b] = d0r - jr;  o[3][2 * b + 1] = d0i - ji;
+            }
+        } else if (p == 3) {
+            const double h = 0.86602540378443864676372317075293618 * sign;
+            for (int b = 0; b < LB; ++b) {
+                const double* x0 = &v[2 * b];
+                const double* x1 = &v[2 * (LB + b)];
+                const double* x2 = &v[2 * (2 * LB + b)];
+                double t1r = x1[0] + x2[0], t1i = x1[1] + x2[1];
+                double t2r = x0[0] - 0.5 * t1r, t2i = x0[1] - 0.5 * t1i;
+                double t3r = h * (x1[0] - x2[0]), t3i = h * (x1[1] - x2[1]);
+                o[0][2 * b] = x0[0] + t1r; o[0][2 * b + 1] = x0[1] + t1i;
+                o[1][2 * b] = t2r - t3i;   o[1][2 * b + 1] = t2i + t3r;
+                o[2][2 * b] = t2r + t3i;   o[2][2 * b + 1] = t2i - t3r;
+            }
+        } else {
+            const double* w = st->w;
+            for (int q = 0; q < p; ++q) {
+                double acc[2 * LB];
+                memset(acc, 0, sizeof acc);
+                int t = 0;
+                for (int r = 0; r < p; ++r) {
+                    const double c = w[2 * t], d = w[2 * t + 1];
+                    const double* x = &v[2 * r * LB];
+                    for (int b = 0; b < LB; ++b) {
+                        acc[2 * b] += x[2 * b] * c - x[2 * b + 1] * d;
+                        acc[2 * b + 1] += x[2 * b] * d + x[2 * b + 1] * c;
+                    }
+                    t += q;
+                    if (t >= p) t -= p;
+                }
+                memcpy(o[q], acc, sizeof acc);
+            }
+        }
     }
-    free(buf);
+}
+
+/* In-place transform of LB lines stored as buf[j][b]; work holds 2*n*LB doubles. */
+static void exec_batch(fc_plan1d* p, double* buf, double* work, double* line) {
+    const int n = p->n;
+    if (p->blue || p->nstages == 0) {
+        if (p->nstages == 0 && !p->blue) return;
+        for (int b = 0; b < LB; ++b) {
+            for (int j = 0; j < n; ++j) {
+                line[2 * j] = buf[2 * ((size_t)j * LB + b)];
+                line[2 * j + 1] = buf[2 * ((size_t)j * LB + b) + 1];
+            }
+            fc_exec1d(p, line);
+            for (int j = 0; j < n; ++j) {
+                buf[2 * ((size_t)j * LB + b)] = line[2 * j];
+                buf[2 * ((size_t)j * LB + b) + 1] = line[2 * j + 1];
+            }
+        }
+        return;
+    }
+    double* src = buf;
+    double* dst = work;
+    for (int s = 0; s < p->nstages; ++s) {
+        run_stage_batch(&p->st[s], n, p->sign, src, dst);
+        double* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != buf) memcpy(buf, src, sizeof(double) * 2 * (size_t)n * LB);
+}
+
+/* Transform lines of length n with element stride `stride` (complex units):
+ * line (o, c) starts at data + o*outer_stride + c*cstride.  LB lines are
+ * gathered into buf[j][b]; the (outer, block) items are independent and split
+ * over OpenMP threads, each with its own plan and buffers. */
+static void lines_strided(double* data, size_t nlines_outer, size_t outer_stride, int n,
+                          size_t stride, size_t count, size_t cstride, int sign) {
+    const size_t nblk = (count + LB - 1) / LB;
+    const long long items = (long long)(nlines_outer * nblk);
+#pragma omp parallel
+    {
+        fc_plan1d* plan = fc_plan1d_create(n, sign);
+        double* buf = (double*)calloc(2 * (size_t)n * LB, sizeof(double));
+        double* work = (double*)malloc(sizeof(double) * 2 * (size_t)n * LB);
+        double* line = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+#pragma omp for schedule(static)
+        for (long long it = 0; it < items; ++it) {
+            const size_t o = (size_t)it / nblk, c0 = ((size_t)it % nblk) * LB;
+            double* base = data + 2 * o * outer_stride;
+            const size_t nb = count - c0 < LB ? count - c0 : LB;
+            for (int j = 0; j < n; ++j)
+                for (size_t b = 0; b < nb; ++b) {
+                    const double* src = base + 2 * ((size_t)j * stride + (c0 + b) * cstride);
+                    buf[2 * ((size_t)j * LB + b)] = src[0];
+                    buf[2 * ((size_t)j * LB + b) + 1] = src[1];
+                }
+            exec_batch(plan, buf, work, line);
+            for (int j = 0; j < n; ++j)
+                for (size_t b = 0; b < nb; ++b) {
+                    double* dst = base + 2 * ((size_t)j * stride + (c0 + b) * cstride);
+                    dst[0] = buf[2 * ((size_t)j * LB + b)];
+                    dst[1] = buf[2 * ((size_t)j * LB + b) + 1];
+                }
+        }
+        free(line);
+        free(work);
+        free(buf);
+        fc_plan1d_destroy(plan);
+    }
 }
 
 void fc_fft3d(double* data, int n0, int n1, int n2, int sign) {
-    /* axis 2: contiguous rows */
-    fc_plan1d* p2 = fc_plan1d_create(n2, sign);
-    const size_t rows = (size_t)n0 * n1;
-    for (size_t r = 0; r < rows; ++r) fc_exec1d(p2, data + 2 * r * n2);
-    fc_plan1d_destroy(p2);
+    /* axis 2: contiguous rows (element stride 1, rows n2 apart) */
+    lines_strided(data, 1, 0, n2, 1, (size_t)n0 * n1, (size_t)n2, sign);
     /* axis 1: stride n2, n0 outer blocks */
-    fc_plan1d* p1 = fc_plan1d_create(n1, sign);
-    lines_strided(data, (size_t)n0, (size_t)n1 * n2, n1, (size_t)n2, (size_t)n2, p1);
-    fc_plan1d_destroy(p1);
+    lines_strided(data, (size_t)n0, (size_t)n1 * n2, n1, (size_t)n2, (size_t)n2, 1, sign);
     /* axis 0: stride n1*n2 */
-    fc_plan1d* p0 = fc_plan1d_create(n0, sign);
-    lines_strided(data, 1, 0, n0, (size_t)n1 * n2, (size_t)n1 * n2, p0);
-    fc_plan1d_destroy(p0);
+    lines_strided(data, 1, 0, n0, (size_t)n1 * n2, (size_t)n1 * n2, 1, sign);
 }

@@ -13,7 +13,13 @@
  * per axis; that is what is implemented here (validated against numpy.fft in
  * tests/test_oracle_fft.py to <= 1e-14 relative).
  *
- * Single-threaded on purpose: the reference never enables FFTW threads.
+ * The 3D transform is OpenMP-parallel over independent 1D lines (it uses
+ * omp_get_max_threads(), i.e. the reference's own thread setting).  The
+ * reference as written runs FFTW single-threaded (fft.cpp never calls
+ * fftw_plan_with_nthreads), so this shim makes the reference's FFT stage
+ * FASTER than it would be with FFTW as built upstream: a conservative CPU
+ * baseline.  Results do not depend on the thread count (each line is
+ * transformed by the same sequential code).
  */
 #ifndef FSE_ORACLE_FFT_CORE_H
 #define FSE_ORACLE_FFT_CORE_H

@@ -14,7 +14,10 @@
 
 #include <omp.h>
 
+#include <algorithm>
+#include <cmath>
 #include <complex>
+#include <random>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -325,6 +328,75 @@ int ref_generate_system(int kind, int64_t n, double L, uint64_t seed, double* po
         for (int64_t i = 0; i < n; ++i) {
             for (int d = 0; d < 3; ++d) pos[3 * i + d] = s.positions[i][d];
             for (int c = 0; c < a; ++c) str[a * i + c] = s.strengths[i].c[c];
+        }
+    });
+}
+
+// SURVEY.md 8(d) workload generators (BASELINE.json configs), restated here so
+// that bench.py's reference arm and the golden-vector script build their inputs
+// without loading the product library.  The stream conventions follow the
+// reference harness (harness.cpp:32-34: u = (rng() >> 11) * 2^-53 from
+// std::mt19937_64) plus SURVEY 8(d)'s Box-Muller normal (u1 = ((rng() >> 11) + 1)
+// * 2^-53, one normal per pair).  Draw order: positions, strengths, targets.
+// which: 1 uniform (cfg1/2), 3 sphere (cfg3), 4 clustered (cfg4), 5 uniform +
+// distinct targets (cfg5).  tests/test_oracle_generators.py checks the product's
+// fse_generate_workload reproduces these streams bit for bit.
+namespace {
+struct Stream {
+    std::mt19937_64 g;
+    explicit Stream(uint64_t seed) : g(seed) {}
+    double u() { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+    double z() {
+        const double u1 = (static_cast<double>(g() >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = u();
+        return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+    }
+};
+}  // namespace
+
+int ref_generate_workload(int which, int64_t n, uint64_t seed, double* pos, double* str,
+                          double* tgt) {
+    return guarded([&] {
+        Stream s(seed);
+        if (which == 1 || which == 5) {
+            for (int64_t i = 0; i < 3 * n; ++i) pos[i] = s.u();
+            for (int64_t i = 0; i < 3 * n; ++i) str[i] = s.z();
+            if (which == 5)
+                for (int64_t i = 0; i < 3 * n; ++i) tgt[i] = s.u();
+        } else if (which == 3) {
+            std::vector<double> nrm(3 * n);
+            for (int64_t i = 0; i < n; ++i) {
+                double d0, d1, d2, r2;
+                do {
+                    d0 = s.z();
+                    d1 = s.z();
+                    d2 = s.z();
+                    r2 = d0 * d0 + d1 * d1 + d2 * d2;
+                } while (r2 == 0);
+                const double inv = 1.0 / std::sqrt(r2);
+                const double d[3] = {d0 * inv, d1 * inv, d2 * inv};
+                for (int c = 0; c < 3; ++c) {
+                    nrm[3 * i + c] = d[c];
+                    pos[3 * i + c] = std::min(1.0, std::max(0.0, 0.5 + 0.5 * d[c]));
+                }
+            }
+            for (int64_t i = 0; i < n; ++i) {
+                const double q[3] = {s.z(), s.z(), s.z()};
+                // Strength::pair(q, n): f_lm = n_l q_m (kernels.hpp:39-45)
+                for (int l = 0; l < 3; ++l)
+                    for (int m = 0; m < 3; ++m) str[9 * i + 3 * l + m] = nrm[3 * i + l] * q[m];
+            }
+        } else if (which == 4) {
+            double ctr[32][3];
+            for (int b = 0; b < 32; ++b)
+                for (int c = 0; c < 3; ++c) ctr[b][c] = 0.2 + 0.6 * s.u();
+            const double hi = std::nextafter(1.0, 0.0);
+            for (int64_t i = 0; i < n; ++i)
+                for (int c = 0; c < 3; ++c)
+                    pos[3 * i + c] = std::min(hi, std::max(0.0, ctr[i % 32][c] + 0.03 * s.z()));
+            for (int64_t i = 0; i < 3 * n; ++i) str[i] = s.z();
+        } else {
+            throw std::invalid_argument("ref_generate_workload: unknown workload");
         }
     });
 }

@@ -254,6 +254,21 @@ def save_green(gkind, Ltilde, Mtilde, sf, path):
     _check(f(gkind, Ltilde, Mtilde, sf, path.encode()))
 
 
+def load_green(path):
+    """load_mollified_green (greens.cpp:173-203): (kind, Ltilde, h, R, Mtilde, table)."""
+    f = lib().ref_load_green
+    gk, Mt = C.c_int(), C.c_int()
+    Lt, h, R = C.c_double(), C.c_double(), C.c_double()
+    f.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                  C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]
+    _check(f(path.encode(), C.byref(gk), C.byref(Lt), C.byref(h), C.byref(R), C.byref(Mt), None))
+    D = 2 * Mt.value
+    out = np.zeros((D, D, D))
+    _check(f(path.encode(), C.byref(gk), C.byref(Lt), C.byref(h), C.byref(R), C.byref(Mt),
+             out.ctypes.data_as(C.c_void_p)))
+    return gk.value, Lt.value, h.value, R.value, Mt.value, out
+
+
 def direct_sum(kind, pos, strengths, L, targets, exclude_self):
     pos, strengths, targets = _a(pos), _a(strengths), _a(targets)
     u = np.zeros((targets.shape[0], 3))
@@ -290,6 +305,19 @@ def generate_system(kind, n, L, seed):
     f.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_uint64, _dp, _dp]
     _check(f(kind, n, L, seed, pos, st))
     return pos, st
+
+
+def generate_workload(which, n, seed):
+    """SURVEY 8(d) workload streams (ref_capi.cpp ref_generate_workload):
+    returns (positions, strengths, targets or None)."""
+    a = 9 if which == 3 else 3
+    pos = np.zeros((n, 3))
+    st = np.zeros((n, a))
+    tgt = np.zeros((n, 3)) if which == 5 else np.zeros((1, 3))
+    f = lib().ref_generate_workload
+    f.argtypes = [C.c_int, C.c_int64, C.c_uint64, _dp, _dp, _dp]
+    _check(f(which, n, seed, pos, st, tgt))
+    return pos, st, (tgt if which == 5 else None)
 
 
 def fft3d(data, inverse=False):

@@ -27,6 +27,7 @@ import ctypes as C
 import enum
 import os
 import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -259,6 +260,8 @@ def _load():
                                                 C.c_double, C.c_double, _dp, i64, _dp]
         lib.fse_cuda_spread.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
                                         C.c_double, _dp]
+        lib.fse_cuda_spread_ex.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
+                                           C.c_double, C.c_int, _dp]
         lib.fse_cuda_kspace_scale.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, _dp, _dp]
         lib.fse_cuda_build_cell_list.argtypes = [vp, _dp, i64, C.c_double, C.c_double,
                                                  C.c_double, C.POINTER(C.c_int), _dp, _dp,
@@ -268,6 +271,9 @@ def _load():
         lib.fse_cuda_direct_sum.argtypes = [vp, C.c_int, _dp, _dp, i64, _dp, i64, C.c_int, _dp]
         lib.fse_cuda_fft3d.argtypes = [vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int]
         lib.fse_cuda_fft_columns.argtypes = [vp, C.c_int, C.c_int, _dp, C.c_int]
+        lib.fse_cuda_xscale_probe.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp,
+                                              C.c_uint64, C.c_int, C.POINTER(C.c_int),
+                                              C.POINTER(C.c_int), _dp, _dp]
         lib.fse_cuda_host_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
         lib.fse_cuda_host_free.argtypes = [vp]
         lib.fse_cuda_dev_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
@@ -548,12 +554,15 @@ class Context:
                    float(rc), _p(t), t.shape[0], _p(u))
         return u
 
-    def spread(self, system: SourceSystem, cfg: EwaldConfig, kind):
+    def spread(self, system: SourceSystem, cfg: EwaldConfig, kind, use_fgg: bool = True):
+        """fse::spread (ewald.cpp:136-214); use_fgg=False: one exp per node
+        (axis_weights_naive, ewald.cpp:53-66)."""
         a = strength_arity(kind)
         Mt = cfg.Mtilde
         grid = np.empty((a, Mt, Mt, Mt))
-        self._call(_load().fse_cuda_spread, C.byref(cfg), int(kind), _p(system.positions),
-                   _p(system.strengths), system.size(), float(system.box_side), _p(grid))
+        self._call(_load().fse_cuda_spread_ex, C.byref(cfg), int(kind), _p(system.positions),
+                   _p(system.strengths), system.size(), float(system.box_side),
+                   int(bool(use_fgg)), _p(grid))
         return grid
 
     def kspace_scale(self, ghat, cfg: EwaldConfig, kind, green):
@@ -606,6 +615,20 @@ class Context:
                    int(inverse))
         return d
 
+    def xscale_probe(self, cfg, kind, green, seed, ky, kz):
+        """Diagnostics (fse_cuda_xscale_probe): the hot path's fused x pass on a
+        pseudo-random spectrum; returns (out (np, 3, Mt) complex, gcol (np, D))."""
+        ky = np.ascontiguousarray(ky, dtype=np.int32)
+        kz = np.ascontiguousarray(kz, dtype=np.int32)
+        npb = ky.shape[0]
+        out = np.empty((npb, 3, cfg.Mtilde), np.complex128)
+        gcol = np.empty((npb, cfg.D))
+        ip = C.POINTER(C.c_int)
+        self._call(_load().fse_cuda_xscale_probe, C.byref(cfg), int(kind),
+                   green.handle if green is not None else None, int(seed), npb,
+                   ky.ctypes.data_as(ip), kz.ctypes.data_as(ip), out.ctypes.data_as(_dp), _p(gcol))
+        return out, gcol
+
     def fft3d(self, data, inverse=False):
         d = np.ascontiguousarray(data, dtype=np.complex128).copy()
         n0, n1, n2 = d.shape
@@ -622,13 +645,14 @@ class Context:
         _load().fse_cuda_dev_free(self._h, C.c_void_p(ptr))
 
     def host_alloc(self, shape, dtype=np.float64) -> np.ndarray:
-        """Pinned host array (kept alive by the returned object)."""
+        """Pinned host array; the pinned block is released (fse_cuda_host_free) when
+        the array and every view of it are garbage collected."""
         n = int(np.prod(shape)) * np.dtype(dtype).itemsize
         p = C.c_void_p()
         self._call(_load().fse_cuda_host_alloc, n, C.byref(p))
         buf = (C.c_char * max(n, 1)).from_address(p.value)
         arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
-        _PINNED[id(arr)] = (p.value, buf)
+        weakref.finalize(buf, _load().fse_cuda_host_free, C.c_void_p(p.value))
         return arr
 
     def memcpy(self, dst: int, src: int, nbytes: int):
@@ -642,8 +666,6 @@ class Context:
         self._call(_load().fse_cuda_elapsed_ms, C.byref(v))
         return v.value
 
-
-_PINNED: dict = {}
 
 # ---------------------------------------------------------- default context
 _default = None
@@ -662,8 +684,8 @@ def precompute_mollified_green(kind, Ltilde, Mtilde, sf) -> MollifiedGreen:
     return default_context().precompute_mollified_green(kind, Ltilde, Mtilde, sf)
 
 
-def spread(system, cfg, kind):
-    return default_context().spread(system, cfg, kind)
+def spread(system, cfg, kind, use_fgg=True):
+    return default_context().spread(system, cfg, kind, use_fgg)
 
 
 def kspace_scale(ghat, cfg, kind, green):

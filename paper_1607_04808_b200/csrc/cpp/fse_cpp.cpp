@@ -310,14 +310,14 @@ MollifiedGreen load_mollified_green(const std::string& path) {
 // ------------------------------------------------------------------ ewald.hpp
 GriddedSources spread(const SourceSystem& system, const EwaldConfig& cfg, KernelKind kind,
                       bool use_fgg) {
-    (void)use_fgg;  // FGG and naive weights agree to 1e-13 (test_spectral.cpp:102-122)
     const int a = strength_arity(kind);
     const size_t vol = static_cast<size_t>(cfg.Mtilde) * cfg.Mtilde * cfg.Mtilde;
     std::vector<double> flat(vol * a);
     const auto str = detail::pack_strengths(system, kind);
-    check(fse_cuda_spread(ctx(), detail::cfg_of(cfg), static_cast<int>(kind),
-                          detail::pts(system.positions), str.data(),
-                          static_cast<int64_t>(system.size()), system.box_side, flat.data()));
+    check(fse_cuda_spread_ex(ctx(), detail::cfg_of(cfg), static_cast<int>(kind),
+                             detail::pts(system.positions), str.data(),
+                             static_cast<int64_t>(system.size()), system.box_side,
+                             use_fgg ? 1 : 0, flat.data()));
     GriddedSources g;
     g.extents[0] = g.extents[1] = g.extents[2] = cfg.Mtilde;
     g.h = cfg.h;

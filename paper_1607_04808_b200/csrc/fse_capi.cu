@@ -4,22 +4,25 @@
 //
 //   stream s0 (Fourier part, ewald.cpp:295-392)
 //     support starts + tile keys -> stable radix sort -> tile starts
-//     -> FGG weights in sorted order -> memset spectrum buffer
-//     -> k_spread (tile-owned, register accumulation)           [spread]
-//     -> cuFFT 2D D2Z over the Mtilde non-zero x-planes
-//     -> cuFFT 1D Z2Z along x (the 7/8 zero padding is never transformed
-//        along y/z: pruned R2C of the D = 2 Mtilde grid)          [fft]
-//     -> k_kscale_half (Nyquist-exact multiplier, 1/D^3 folded)   [scale]
-//     -> cuFFT 1D Z2Z inverse along x -> 2D Z2D over Mtilde planes [fft]
+//     -> FGG weights in sorted order (prefac folded)              [prep]
+//     -> k_spread: tile-owned DMMA spreading, no atomics            [spread]
+//     -> k_zfwd (R2C along z, two real rows per complex FFT) and
+//        k_ypass (y), pruned: zero planes x >= Mtilde are never stored [fft]
+//     -> k_xscale*: forward x-FFT, Nyquist-exact multiplier A_eff G / D^3,
+//        inverse x-FFT, in shared memory / registers                [scale]
+//     -> k_ypass<inverse>, k_zinv (C2R): only the Mtilde^3 window   [fft]
 //     -> target prep (reuses the source sort when targets == sources)
-//     -> k_gather (warp groups of 8 targets)                     [quadrature]
+//     -> k_gather_tma: TMA-staged x-planes, DMMA z-contraction        [quadrature]
 //   stream s1 (real part, realspace.cpp:86-149), concurrent with s0
 //     cell ids -> stable radix sort -> bucket starts (the reference CellList)
 //     -> SoA permute -> k_realspace                               [realspace]
 //   s0 waits for s1 -> k_epilogue: u = (uF + uR) + self term
 //
-// Device buffers are cached per context and grow on demand; cuFFT plans are
-// cached per (D, Mtilde) and share one work area.
+// All FFTs of the hot path are the hand-written engines of k_fft.cu (no cuFFT);
+// the Green's precompute uses cuBLAS DGEMMs for its cosine passes and the
+// fse::fft3d drop-in uses cuFFT.  Device buffers are cached per context and grow
+// on demand.
+#include <cublas_v2.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -144,8 +147,6 @@ struct fse_cuda_ctx {
     uint64_t launches = 0;
     double kms[NKMS] = {};  // per-kernel device ms of the last evaluation
     std::map<std::string, DevBuf> bufs;
-    std::map<std::tuple<int, int, int>, cufftHandle> plans;
-    DevBuf work;
     int* d_flags = nullptr;  // [0] s0 flags, [1] s1 flags, [2] equality flag
     int* h_flags = nullptr;  // pinned
     bool overlap = std::getenv("FSE_SERIAL") == nullptr;  // real space on s1 alongside s0
@@ -201,8 +202,6 @@ T* buf(fse_cuda_ctx* c, const std::string& name, size_t count) {
 }
 
 void release_plans(fse_cuda_ctx* c) {
-    for (auto& kv : c->plans) cufftDestroy(kv.second);
-    c->plans.clear();
     for (auto& kv : c->fft_plans)
         if (kv.second.tw) cudaFree(kv.second.tw);
     c->fft_plans.clear();
@@ -222,41 +221,6 @@ const FftPlanDev& fft_plan(fse_cuda_ctx* c, int D) {
 
 Launch L0(fse_cuda_ctx* c) { return Launch{c->s0, &c->launches}; }
 Launch L1(fse_cuda_ctx* c) { return Launch{c->s1, &c->launches}; }
-
-// which: 0 = 2D D2Z batch Mt, 1 = 2D Z2D batch Mt, 2 = 1D Z2Z along x
-cufftHandle plan(fse_cuda_ctx* c, int which, int D, int Mt) {
-    const auto key = std::make_tuple(which, D, which == 2 ? 0 : Mt);
-    auto it = c->plans.find(key);
-    if (it != c->plans.end()) return it->second;
-    cufftHandle h;
-    FSE_CUFFT(cufftCreate(&h));
-    FSE_CUFFT(cufftSetAutoAllocation(h, 0));
-    size_t ws = 0;
-    const long long Dh = D / 2 + 1;
-    if (which == 0 || which == 1) {
-        long long n[2] = {D, D};
-        FSE_CUFFT(cufftMakePlanMany64(h, 2, n, nullptr, 1, 0, nullptr, 1, 0,
-                                      which == 0 ? CUFFT_D2Z : CUFFT_Z2D, Mt, &ws));
-    } else {
-        long long n[1] = {D};
-        long long emb[1] = {D};
-        const long long stride = static_cast<long long>(D) * Dh;
-        FSE_CUFFT(cufftMakePlanMany64(h, 1, n, emb, stride, 1, emb, stride, 1, CUFFT_Z2Z,
-                                      stride, &ws));
-    }
-    if (ws > c->work.bytes) {
-        sync_all(c);
-        if (c->work.p) FSE_CU(cudaFree(c->work.p));
-        c->work.p = nullptr;
-        FSE_CU(cudaMalloc(&c->work.p, ws));
-        c->work.bytes = ws;
-        for (auto& kv : c->plans) FSE_CUFFT(cufftSetWorkArea(kv.second, c->work.p));
-    }
-    FSE_CUFFT(cufftSetWorkArea(h, c->work.p));
-    FSE_CUFFT(cufftSetStream(h, c->s0));
-    c->plans[key] = h;
-    return h;
-}
 
 void check_cfg(const fse_config* cfg) {
     if (!cfg) invalid("null config");
@@ -319,7 +283,7 @@ struct Sorted {
 
 Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
                    const double* d_pos, const double* d_str, int a, int64_t n, int check_box,
-                   const double* qtab) {
+                   const double* qtab, bool naive = false) {
     Launch L = L0(c);
     Sorted s;
     uint32_t* keys = buf<uint32_t>(c, tag + "keys", n);
@@ -341,7 +305,7 @@ Sorted prep_points(fse_cuda_ctx* c, const GridParams& g, const std::string& tag,
     // one z-slab: weights only for the sources whose support reaches its planes
     // and the targets of the quadrature items that do (k_slab_counts)
     launch_gather_payload(L, g, d_pos, d_str, a, s.perm, n, qtab, s.i0s, s.w, s.fs, true,
-                          g.nx < g.Mt ? (d_str != nullptr ? 1 : 2) : 0);
+                          g.nx < g.Mt ? (d_str != nullptr ? 1 : 2) : 0, naive);
     return s;
 }
 
@@ -671,9 +635,80 @@ fse_green* new_green(fse_cuda_ctx* c, int kind, double Ltilde, int Mt, double h,
     return g;
 }
 
-// greens.cpp:48-113 on the GPU: Ghat on the sM^3 wavenumber grid (half
-// spectrum, the grid is real and even) -> Z2D -> scale 1/sM^3 and window to
-// the (2 Mt)^3 offsets in [-Mt, Mt) -> D2Z -> real part.
+// One device buffer owned for the duration of a call (one-off scratch that must
+// not stay cached in the context).
+struct DevScratch {
+    void* p = nullptr;
+    DevScratch() = default;
+    DevScratch(const DevScratch&) = delete;
+    DevScratch& operator=(const DevScratch&) = delete;
+    ~DevScratch() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        if (p) FSE_CU(cudaFree(p));
+        p = nullptr;
+        FSE_CU(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        return static_cast<T*>(p);
+    }
+};
+
+struct Cublas {
+    cublasHandle_t h = nullptr;
+    ~Cublas() {
+        if (h) cublasDestroy(h);
+    }
+};
+
+#define FSE_CUBLAS(x)                                                                  \
+    do {                                                                               \
+        cublasStatus_t st_ = (x);                                                      \
+        if (st_ != CUBLAS_STATUS_SUCCESS) {                                            \
+            char b_[256];                                                              \
+            std::snprintf(b_, sizeof b_, "cuBLAS error %d in %s", static_cast<int>(st_), #x); \
+            throw Error(st_ == CUBLAS_STATUS_ALLOC_FAILED ? FSE_ENOMEM : FSE_ECUDA, b_);    \
+        }                                                                              \
+    } while (0)
+
+// even-sequence cosine matrix, row-major [nout][nin]:
+//   C[n][q] = w_q cos(2 pi q n / len) * scale, w_q = 1 at q = 0 and q = len/2, else 2
+// (the length-len DFT of a real sequence even in q, evaluated at n, folded onto
+// q in [0, len/2]); angles reduced exactly in integers, cosl in long double.
+std::vector<double> cos_matrix(int nout, int nin, int len, long double scale) {
+    std::vector<double> m(static_cast<size_t>(nout) * nin);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int n = 0; n < nout; ++n)
+        for (int q = 0; q < nin; ++q) {
+            const int64_t r = (static_cast<int64_t>(q) * n) % len;
+            const long double w = (q == 0 || 2 * q == len) ? 1.0L : 2.0L;
+            m[static_cast<size_t>(n) * nin + q] =
+                static_cast<double>(w * scale * cosl(two_pi * static_cast<long double>(r) / len));
+        }
+    return m;
+}
+
+// One separable pass: out[n][ab] = sum_q Cm[n][q] in[ab][q] (row-major); the
+// summed axis is the fastest of `in` and becomes the slowest of `out`, so three
+// passes rotate the axes back to their original order.  A plain DGEMM (cuBLAS).
+void cos_pass(cublasHandle_t hb, const double* in, int64_t AB, int K, const double* Cm, int N,
+              double* out) {
+    const double one = 1.0, zero = 0.0;
+    FSE_CUBLAS(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(AB), N, K, &one, in,
+                           K, Cm, K, &zero, out, static_cast<int>(AB)));
+}
+
+// greens.cpp:48-113 on the GPU, pruned and symmetry-aware.
+// The reference fills Ghat(|k|) on the sM^3 wavenumber grid, inverse-FFTs it,
+// keeps the real (2 Mt)^3 window of offsets [-Mt, Mt) and forward-FFTs that.
+// Ghat is real and even in every axis, so the inverse DFT is a product of
+// cosine sums over q in [0, sM/2] and is only needed at |offset| <= Mt; the
+// windowed grid is again real and even, so the forward DFT is a product of
+// cosine sums over n in [0, Mt] evaluated at k in [0, D/2]:
+//   octant Ghat (sM/2+1)^3 -> 3 cosine passes -> g (Mt+1)^3 -> 3 cosine passes
+//   -> T (D/2+1)^3 -> unfolded to the D x D x (D/2+1) half table.
+// Six DGEMMs on arrays of at most (sM/2+1)^3 doubles instead of an sM^3 grid
+// (cfg5: 4.4 GB instead of 35 GB; cfg5t: 13 GB instead of 105 GB).
 fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, double sf) {
     const double sf_min = 1.0 + std::sqrt(3.0);
     if (!(Ltilde > 0) || Mt < 1) invalid("precompute_mollified_green: bad domain");
@@ -685,55 +720,37 @@ fse_green* green_precompute(fse_cuda_ctx* c, int gkind, double Ltilde, int Mt, d
     if (sM % 2 != 0) ++sM;
     const double dk = 2.0 * M_PI / (sM * h);
     const int D = 2 * Mt;
+    const int nq = sM / 2 + 1, nm = Mt + 1;  // D/2 + 1 == Mt + 1
     Launch L = L0(c);
     fse_green* g = new_green(c, gkind, Ltilde, Mt, h, R);
-    // cuFFT plans and the sM^3 scratch (tens of GB at cfg5) are released on
-    // every exit, including a failed plan or allocation
-    struct Scratch {
-        fse_cuda_ctx* c;
-        cufftHandle plans[2] = {0, 0};
-        bool live[2] = {false, false};
-        ~Scratch() {
-            for (int i = 0; i < 2; ++i)
-                if (live[i]) cufftDestroy(plans[i]);
-            for (const char* nm : {"green_S", "green_T"}) {
-                auto it = c->bufs.find(nm);
-                if (it != c->bufs.end() && it->second.p) {
-                    cudaFree(it->second.p);
-                    it->second = DevBuf{};
-                }
-            }
-        }
-    } scratch{c};
     try {
-        const int64_t sMp = sM + 2;
-        double* S = buf<double>(c, "green_S", static_cast<size_t>(sM) * sM * sMp);
-        launch_green_fill(L, gkind, sM, dk, R, reinterpret_cast<double2*>(S));
-        cufftHandle& pi = scratch.plans[0];
-        size_t ws = 0;
-        FSE_CUFFT(cufftCreate(&pi));
-        scratch.live[0] = true;
-        // 64-bit plan API: sM^3 exceeds 2^31 elements from sM = 1291 (cfg5: 1640),
-        // where the 32-bit cufftMakePlan3d of CUDA 12.9's cuFFT fails
-        long long nI[3] = {sM, sM, sM};
-        FSE_CUFFT(cufftMakePlanMany64(pi, 3, nI, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1,
-                                      &ws));
-        FSE_CUFFT(cufftSetStream(pi, c->s0));
-        FSE_CUFFT(cufftExecZ2D(pi, reinterpret_cast<cufftDoubleComplex*>(S), S));
-        const double scale = 1.0 / (static_cast<double>(sM) * sM * sM);
-        double* T = buf<double>(c, "green_T", static_cast<size_t>(D) * D * (D + 2));
-        launch_green_window(L, sM, sMp, Mt, S, scale, T);
-        FSE_CU(cudaStreamSynchronize(c->s0));
-        cufftHandle& pf = scratch.plans[1];
-        FSE_CUFFT(cufftCreate(&pf));
-        scratch.live[1] = true;
-        long long nF[3] = {D, D, D};
-        FSE_CUFFT(cufftMakePlanMany64(pf, 3, nF, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1,
-                                      &ws));
-        FSE_CUFFT(cufftSetStream(pf, c->s0));
-        FSE_CUFFT(cufftExecD2Z(pf, T, reinterpret_cast<cufftDoubleComplex*>(T)));
-        launch_green_real(L, reinterpret_cast<const double2*>(T),
-                          static_cast<int64_t>(D) * D * (D / 2 + 1), g->d_half);
+        Cublas cb;
+        FSE_CUBLAS(cublasCreate(&cb.h));
+        FSE_CUBLAS(cublasSetStream(cb.h, c->s0));
+        FSE_CUBLAS(cublasSetMathMode(cb.h, CUBLAS_DEFAULT_MATH));
+        // inverse transform matrix [n][q] (1/sM per axis = the 1/sM^3 of fft3d_inverse)
+        // and forward matrix [k][n] over the D-periodic windowed grid
+        const std::vector<double> ci = cos_matrix(nm, nq, sM, 1.0L / sM);
+        const std::vector<double> cf = cos_matrix(nm, nm, D, 1.0L);
+        DevScratch sci, scf, sa, sb;
+        double* dci = sci.alloc<double>(ci.size());
+        double* dcf = scf.alloc<double>(cf.size());
+        FSE_CU(cudaMemcpyAsync(dci, ci.data(), ci.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, c->s0));
+        FSE_CU(cudaMemcpyAsync(dcf, cf.data(), cf.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, c->s0));
+        const int64_t q3 = static_cast<int64_t>(nq) * nq * nq;
+        const int64_t big = std::max<int64_t>(q3, static_cast<int64_t>(nm) * nm * nq);
+        double* A = sa.alloc<double>(static_cast<size_t>(big));
+        double* B = sb.alloc<double>(static_cast<size_t>(static_cast<int64_t>(nm) * nq * nq));
+        launch_green_octant(L, gkind, sM, dk, R, A);                                  // [qx][qy][qz]
+        cos_pass(cb.h, A, static_cast<int64_t>(nq) * nq, nq, dci, nm, B);           // [nz][qx][qy]
+        cos_pass(cb.h, B, static_cast<int64_t>(nm) * nq, nq, dci, nm, A);           // [ny][nz][qx]
+        cos_pass(cb.h, A, static_cast<int64_t>(nm) * nm, nq, dci, nm, B);           // [nx][ny][nz]
+        cos_pass(cb.h, B, static_cast<int64_t>(nm) * nm, nm, dcf, nm, A);           // [kz][nx][ny]
+        cos_pass(cb.h, A, static_cast<int64_t>(nm) * nm, nm, dcf, nm, B);           // [ky][kz][nx]
+        cos_pass(cb.h, B, static_cast<int64_t>(nm) * nm, nm, dcf, nm, A);           // [kx][ky][kz]
+        launch_green_unfold(L, Mt, A, g->d_half);
         FSE_CU(cudaStreamSynchronize(c->s0));
     } catch (...) {
         cudaFree(g->d_half);
@@ -782,7 +799,6 @@ void fse_cuda_destroy(fse_cuda_ctx* c) {
     release_plans(c);
     for (auto& kv : c->bufs)
         if (kv.second.p) cudaFree(kv.second.p);
-    if (c->work.p) cudaFree(c->work.p);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->mark)
@@ -804,8 +820,6 @@ fse_status fse_cuda_trim(fse_cuda_ctx* c) {
         for (auto& kv : c->bufs)
             if (kv.second.p) FSE_CU(cudaFree(kv.second.p));
         c->bufs.clear();
-        if (c->work.p) FSE_CU(cudaFree(c->work.p));
-        c->work = DevBuf{};
     });
 }
 
@@ -933,7 +947,8 @@ fse_status fse_cuda_green_upload(fse_cuda_ctx* c, int green_kind, double Ltilde,
         try {
             const int D = 2 * Mtilde;
             const size_t n = static_cast<size_t>(D) * D * D;
-            double* tmp = buf<double>(c, "green_full", n);
+            DevScratch scratch;
+            double* tmp = scratch.alloc<double>(n);
             h2d(c, tmp, full, n * sizeof(double));
             launch_green_full_to_half(L0(c), D, tmp, g->d_half);
             FSE_CU(cudaStreamSynchronize(c->s0));
@@ -951,7 +966,8 @@ fse_status fse_cuda_green_download(fse_cuda_ctx* c, const fse_green* g, double* 
         if (!g || !full) invalid("null pointer");
         const int D = 2 * g->Mtilde;
         const size_t n = static_cast<size_t>(D) * D * D;
-        double* tmp = buf<double>(c, "green_full", n);
+        DevScratch scratch;
+        double* tmp = scratch.alloc<double>(n);
         launch_green_half_to_full(L0(c), D, g->d_half, tmp);
         d2h(c, full, tmp, n * sizeof(double));
     });
@@ -1024,7 +1040,8 @@ fse_status fse_cuda_green_save(fse_cuda_ctx* c, const fse_green* g, const char* 
         if (!g || !path) invalid("null pointer");
         const uint64_t D = 2 * static_cast<uint64_t>(g->Mtilde);
         std::vector<double> full(D * D * D);
-        double* tmp = buf<double>(c, "green_full", full.size());
+        DevScratch scratch;  // one-off D^3 staging, not cached in the context
+        double* tmp = scratch.alloc<double>(full.size());
         launch_green_half_to_full(L0(c), static_cast<int>(D), g->d_half, tmp);
         d2h(c, full.data(), tmp, full.size() * sizeof(double));
         std::ofstream os(path, std::ios::binary);
@@ -1067,13 +1084,18 @@ fse_status fse_cuda_green_load(fse_cuda_ctx* c, const char* path, fse_green** ou
         is.read(reinterpret_cast<char*>(d), 24);
         if (!is || d[0] != d[1] || d[0] != d[2] || d[0] == 0 || d[0] % 2 != 0)
             throw Error(FSE_ERUNTIME, "load_mollified_green: bad extents");
+        // the reference stores whatever byte it finds (greens.cpp:189); a table of
+        // an unknown kind could never pass check_green, so reject it here
+        if (kind != FSE_HARMONIC && kind != FSE_BIHARMONIC)
+            throw Error(FSE_ERUNTIME, "load_mollified_green: unknown green kind");
         std::vector<double> full(d[0] * d[1] * d[2]);
         is.read(reinterpret_cast<char*>(full.data()),
                 static_cast<std::streamsize>(full.size() * sizeof(double)));
         if (!is) throw Error(FSE_ERUNTIME, "load_mollified_green: truncated payload");
         const int Mt = static_cast<int>(d[0] / 2);
         fse_green* g = new_green(c, kind, Lt, Mt, h, R);
-        double* tmp = buf<double>(c, "green_full", full.size());
+        DevScratch scratch;
+        double* tmp = scratch.alloc<double>(full.size());
         h2d(c, tmp, full.data(), full.size() * sizeof(double));
         launch_green_full_to_half(L0(c), static_cast<int>(d[0]), tmp, g->d_half);
         FSE_CU(cudaStreamSynchronize(c->s0));
@@ -1321,6 +1343,12 @@ fse_status fse_cuda_real_space_sum(fse_cuda_ctx* c, int kind, const double* pos,
 
 fse_status fse_cuda_spread(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* pos,
                            const double* str, int64_t n, double box_side, double* grid) {
+    return fse_cuda_spread_ex(c, cfg, kind, pos, str, n, box_side, 1, grid);
+}
+
+fse_status fse_cuda_spread_ex(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* pos,
+                              const double* str, int64_t n, double box_side, int use_fgg,
+                              double* grid) {
     return api(c, [&] {
         check_kind(kind);
         check_cfg(cfg);
@@ -1336,7 +1364,7 @@ fse_status fse_cuda_spread(fse_cuda_ctx* c, const fse_config* cfg, int kind, con
         FSE_CU(cudaMemsetAsync(c->d_flags, 0, 3 * sizeof(int), c->s0));
         double* qtab = buf<double>(c, "qtab", g.P);
         launch_quad_table(L0(c), g, qtab);
-        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab);
+        Sorted src = prep_points(c, g, "fs_", d_pos, d_str, a, n, 0, qtab, use_fgg == 0);
         double* X = buf<double>(c, "R", static_cast<size_t>(a) * g.comp);
         for (int c0 = 0; c0 < a; c0 += 3)
             launch_spread(L0(c), g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
@@ -1443,6 +1471,48 @@ fse_status fse_cuda_fft_columns(fse_cuda_ctx* c, int D, int ncols, double* data,
         h2d(c, d, data, n * sizeof(double2));
         fft_test_columns(L0(c), fp.host, fp.tw, d, ncols, inverse);
         d2h(c, data, d, n * sizeof(double2));
+    });
+}
+
+// diagnostics: the fused x pass (k_xscale*: FFT_x -> multiplier -> IFFT_x) of the
+// hot path on a pseudo-random spectrum, probed at chosen (ky, kz) columns
+fse_status fse_cuda_xscale_probe(fse_cuda_ctx* c, const fse_config* cfg, int kind,
+                                 const fse_green* green, uint64_t seed, int nprobe,
+                                 const int* ky, const int* kz, double* out, double* gcol) {
+    return api(c, [&] {
+        check_cfg(cfg);
+        check_kind(kind);
+        if (green) check_green(cfg, kind, green);
+        if (nprobe < 1 || !ky || !kz || !out || !gcol) invalid("xscale_probe: bad arguments");
+        const GridParams g = make_grid_params(*cfg);
+        for (int p = 0; p < nprobe; ++p)
+            if (ky[p] < 0 || ky[p] >= g.D || kz[p] < 0 || kz[p] >= g.Dh)
+                invalid("xscale_probe: column out of range");
+        const int a = arity_of(kind);
+        const Launch L = L0(c);
+        const int64_t nC = static_cast<int64_t>(a) * g.Mt * g.D * g.Dh;
+        double2* C = buf<double2>(c, "C", static_cast<size_t>(nC));
+        launch_probe_fill(L, C, nC, seed);
+        const double* G = nullptr;
+        if (green) {
+            G = green->d_half;
+        } else {
+            const int64_t nG = static_cast<int64_t>(g.D) * g.D * g.Dh;
+            double* Gs = buf<double>(c, "probe_G", static_cast<size_t>(nG));
+            launch_probe_green(L, Gs, nG, seed ^ 0x5DEECE66Dull);
+            G = Gs;
+        }
+        const FftPlanDev& fp = fft_plan(c, g.D);
+        launch_fft_xscale(L, fp.host, fp.tw, g, kind, G, C, buf<double>(c, "ex_axis", g.D));
+        int* dk = buf<int>(c, "probe_k", 2 * static_cast<size_t>(nprobe));
+        h2d(c, dk, ky, sizeof(int) * nprobe);
+        h2d(c, dk + nprobe, kz, sizeof(int) * nprobe);
+        const size_t no = static_cast<size_t>(nprobe) * 3 * g.Mt;
+        double2* dout = buf<double2>(c, "probe_out", no);
+        double* dg = buf<double>(c, "probe_gcol", static_cast<size_t>(nprobe) * g.D);
+        launch_probe_extract(L, C, G, g.Mt, g.D, nprobe, dk, dk + nprobe, dout, dg);
+        d2h(c, out, dout, no * sizeof(double2));
+        d2h(c, gcol, dg, sizeof(double) * nprobe * g.D);
     });
 }
 

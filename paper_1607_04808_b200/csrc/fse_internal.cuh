@@ -109,11 +109,12 @@ void launch_support_keys(const Launch& L, const GridParams& g, const double* pos
 // q[p] table
 void launch_quad_table(const Launch& L, const GridParams& g, double* q);
 // sorted payload: i0s (n x 3), weights (n x 3P, prefac folded into x when
-// fold_prefac), strengths (a x n SoA), from perm
+// fold_prefac), strengths (a x n SoA), from perm; naive: one exp per node
+// (axis_weights_naive, ewald.cpp:53-66) instead of the FGG recurrence
 void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
                            const double* str, int a, const uint32_t* perm, int64_t n,
                            const double* qtab, int32_t* i0s, double* w, double* fs,
-                           bool fold_prefac, int slab_only = 0);
+                           bool fold_prefac, int slab_only = 0, bool naive = false);
 // histogram of keys into counts (size nkeys, zeroed by caller)
 void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts);
 // cell ids of points for the reference cell list (realspace.cpp:60-63,80)
@@ -139,10 +140,6 @@ void launch_extract_grid(const Launch& L, const GridParams& g, const double* X, 
                          double* out);
 
 // k_kscale.cu ---------------------------------------------------------------
-// half-spectrum, Hermitian-exact (Nyquist-averaged) multiplier, 1/D^3 folded;
-// in place on X (a components in, 3 out)
-void launch_kscale_half(const Launch& L, const GridParams& g, int kind, const double* G,
-                        double2* X, int64_t comp_c);
 // full D^3 C2C, reference multiplier verbatim (ewald.cpp:216-293)
 void launch_kscale_full(const Launch& L, const GridParams& g, int kind, const double* Gfull,
                         const double2* ghat, double2* out);
@@ -194,13 +191,11 @@ void launch_epilogue(const Launch& L, int64_t nt, const double* uF, const double
                      const double* str_self, double self_coef, double* u);
 
 // k_green.cu ----------------------------------------------------------------
-// fill the half spectrum (sM x sM x (sM/2+1)) of Hhat^R / Bhat^R (greens.cpp:62-79)
-void launch_green_fill(const Launch& L, int gkind, int sM, double dk, double R, double2* half);
-// window the (scaled) real sM^3 grid into the D^3 real view (pitch D+2) (greens.cpp:84-104)
-void launch_green_window(const Launch& L, int sM, int64_t sMpitch, int Mt, const double* grid,
-                         double scale, double* trunc);
-// keep the real part of the half spectrum
-void launch_green_real(const Launch& L, const double2* spec, int64_t n, double* G);
+// Hhat^R / Bhat^R (greens.cpp:62-79) on the octant q in [0, sM/2]^3 of the sM^3
+// wavenumber grid, [qx][qy][qz] (the grid is even in every axis)
+void launch_green_octant(const Launch& L, int gkind, int sM, double dk, double R, double* oct);
+// T[kx][ky][kz] (k in [0, Mt]^3, even table) -> D x D x (D/2+1) half table
+void launch_green_unfold(const Launch& L, int Mt, const double* T, double* half);
 // full <-> half conversions of the reference layout
 void launch_green_full_to_half(const Launch& L, int D, const double* full, double* half);
 void launch_green_half_to_full(const Launch& L, int D, const double* half, double* full);
@@ -209,5 +204,11 @@ void launch_green_half_to_full(const Launch& L, int D, const double* half, doubl
 double measure_dfma_tflops(const Launch& L, double* scratch);
 void launch_direct(const Launch& L, int kind, const double* pos, const double* str, int64_t n,
                    const double* tgt, int64_t nt, int exclude_self, double* u, int* flags);
+
+// x-pass probe (fse_cuda_xscale_probe, diagnostics) ------------------------------
+void launch_probe_fill(const Launch& L, double2* C, int64_t n, uint64_t seed);
+void launch_probe_green(const Launch& L, double* G, int64_t n, uint64_t seed);
+void launch_probe_extract(const Launch& L, const double2* C, const double* G, int Mt, int D,
+                          int nprobe, const int* ky, const int* kz, double2* out, double* gcol);
 
 }  // namespace fsecu

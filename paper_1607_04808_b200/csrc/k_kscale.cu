@@ -1,20 +1,14 @@
 // k_kscale.cu -- pointwise k-space scaling (ewald.cpp:216-293).
 //
-// Half-spectrum kernel (the hot path): the reference multiplies the FULL C2C
-// spectrum by A(k) and keeps Re(IFFT) (ewald.cpp:343).  Re(IFFT(X)) is the
-// C2R inverse of the Hermitian part of X, and because ghat is the transform
-// of real data the Hermitian part of A(k) ghat(idx) is A_eff(k) ghat(idx) with
+// The fse::kspace_scale drop-in: the reference multiplier verbatim on D^3
+// C2C planes.  The hot path does not use it: there the multiplier is fused
+// into the x pass (k_fft.cu k_xscale*) in its Nyquist-exact half-spectrum form
 //     A_eff(k) = (A(k) + A(k~)) / 2,
-// k~ = k with every component sitting on the Nyquist index (D/2, assigned
-// -dk D/2 by the reference, ewald.cpp:235) negated.  Off the Nyquist planes
-// k~ = k.  So R2C/C2R with this multiplier reproduces the reference exactly
-// (a plain half-spectrum port is off by 7.8e-7).  The
-// inverse-FFT normalisation 1/D^3 (fft.cpp:32-37) is folded in.
-//
-// Full kernel: the reference multiplier verbatim on D^3 C2C planes, for the
-// fse::kspace_scale drop-in.
-//
-// Roofline: HBM (H (16 a + 8 + 48) bytes per call, H = D^2 (D/2+1)).
+// k~ = k with every component on the Nyquist index (D/2, assigned -dk D/2 by
+// the reference, ewald.cpp:235) negated.  The reference keeps Re(IFFT) of the
+// full spectrum (ewald.cpp:343), which is the C2R inverse of the Hermitian part
+// of A(k) ghat(idx) = A_eff(k) ghat(idx) for the transform of real data
+// (SURVEY.md 8a A7).
 #include "fse_internal.cuh"
 
 namespace fsecu {
@@ -85,51 +79,6 @@ __device__ __forceinline__ double kax(int q, int D, double dk) {
     return dk * (q < D / 2 ? q : q - D);
 }
 
-// X: component c at X + c*comp_c (double2 units), layout [i][j][l], l < Dh
-template <int KIND>
-__global__ void __launch_bounds__(256) k_kscale_half(GridParams g, const double* __restrict__ G,
-                                                     double2* __restrict__ X, int64_t comp_c) {
-    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
-    const int64_t H = static_cast<int64_t>(g.D) * g.D * g.Dh;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < H;
-         idx += stride) {
-        const int l = static_cast<int>(idx % g.Dh);
-        const int64_t ij = idx / g.Dh;
-        const int j = static_cast<int>(ij % g.D);
-        const int i = static_cast<int>(ij / g.D);
-        double k[3] = {kax(i, g.D, g.dk), kax(j, g.D, g.dk), kax(l, g.D, g.dk)};
-        const double k2 = k[0] * k[0] + k[1] * k[1] + k[2] * k[2];
-        const double rem = exp(-(1.0 - g.eta) * k2 * g.inv4xi2);
-        const double gval = G[idx];
-        C2 gh[A];
-#pragma unroll
-        for (int c = 0; c < A; ++c) {
-            const double2 v = X[c * comp_c + idx];
-            gh[c].re = v.x;
-            gh[c].im = v.y;
-        }
-        C2 out[3];
-        apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
-        const int half = g.D / 2;
-        if (i == half || j == half || l == half) {
-            if (i == half) k[0] = -k[0];
-            if (j == half) k[1] = -k[1];
-            if (l == half) k[2] = -k[2];
-            C2 o2[3];
-            apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, o2);
-#pragma unroll
-            for (int p = 0; p < 3; ++p) {
-                out[p].re = 0.5 * (out[p].re + o2[p].re);
-                out[p].im = 0.5 * (out[p].im + o2[p].im);
-            }
-        }
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-            X[p * comp_c + idx] = make_double2(out[p].re * g.invD3, out[p].im * g.invD3);
-    }
-}
-
 template <int KIND>
 __global__ void __launch_bounds__(256) k_kscale_full(GridParams g, const double* __restrict__ G,
                                                      const double2* __restrict__ gh_in,
@@ -175,20 +124,6 @@ unsigned grid_for(int64_t n) {
 }
 
 }  // namespace
-
-void launch_kscale_half(const Launch& L, const GridParams& g, int kind, const double* G,
-                        double2* X, int64_t comp_c) {
-    const int64_t H = static_cast<int64_t>(g.D) * g.D * g.Dh;
-    const unsigned b = grid_for(H);
-    if (kind == FSE_STOKESLET)
-        k_kscale_half<FSE_STOKESLET><<<b, 256, 0, L.s>>>(g, G, X, comp_c);
-    else if (kind == FSE_STRESSLET)
-        k_kscale_half<FSE_STRESSLET><<<b, 256, 0, L.s>>>(g, G, X, comp_c);
-    else
-        k_kscale_half<FSE_ROTLET><<<b, 256, 0, L.s>>>(g, G, X, comp_c);
-    FSE_LAUNCH_CHECK();
-    ++*L.launches;
-}
 
 void launch_kscale_full(const Launch& L, const GridParams& g, int kind, const double* Gfull,
                         const double2* ghat, double2* out) {

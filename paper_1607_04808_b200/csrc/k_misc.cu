@@ -161,52 +161,39 @@ __device__ double d_bhat(double k, double R) {
     return 4.0 * M_PI * num / t4 * (R * R * R * R);
 }
 
-// half spectrum of the sM^3 grid, (greens.cpp:62-79): k2(a) = (dk n_a)^2,
-// k = sqrt((k2(i) + k2(j)) + k2(l))
-__global__ void k_green_fill(int gkind, int sM, double dk, double R, double2* __restrict__ half) {
-    const int sh = sM / 2 + 1;
-    const int64_t tot = static_cast<int64_t>(sM) * sM * sh;
+// octant of the sM^3 wavenumber grid (greens.cpp:62-79): index q <= sM/2 has
+// n_a = q (q = sM/2 is n = -sM/2, same k2), k = sqrt((k2(i) + k2(j)) + k2(l)) in
+// the reference's summation order
+__global__ void k_green_octant(int gkind, int sM, double dk, double R, double* __restrict__ oct) {
+    const int nq = sM / 2 + 1;
+    const int64_t tot = static_cast<int64_t>(nq) * nq * nq;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
          q += stride) {
-        const int l = static_cast<int>(q % sh);
-        const int j = static_cast<int>((q / sh) % sM);
-        const int i = static_cast<int>(q / (static_cast<int64_t>(sh) * sM));
-        const int ni = i < sM / 2 ? i : i - sM, nj = j < sM / 2 ? j : j - sM,
-                  nl = l < sM / 2 ? l : l - sM;
-        const double ki = dk * ni, kj = dk * nj, kl = dk * nl;
+        const int l = static_cast<int>(q % nq);
+        const int j = static_cast<int>((q / nq) % nq);
+        const int i = static_cast<int>(q / (static_cast<int64_t>(nq) * nq));
+        auto sgn = [&](int a) { return a < sM / 2 ? a : a - sM; };
+        const double ki = dk * sgn(i), kj = dk * sgn(j), kl = dk * sgn(l);
         const double k2ij = ki * ki + kj * kj;
         const double k = sqrt(k2ij + kl * kl);
-        half[q] = make_double2(gkind == FSE_HARMONIC ? d_hhat(k, R) : d_bhat(k, R), 0.0);
+        oct[q] = gkind == FSE_HARMONIC ? d_hhat(k, R) : d_bhat(k, R);
     }
 }
 
-// (greens.cpp:94-104): doubled-grid index p -> signed offset (p < Mt ? p : p - D)
-// -> oversampled index; real sM^3 grid has row pitch sMpitch
-__global__ void k_green_window(int sM, int64_t sMpitch, int Mt, const double* __restrict__ grid,
-                               double scale, double* __restrict__ trunc) {
-    const int D = 2 * Mt;
-    const int64_t tot = static_cast<int64_t>(D) * D * D;
+// half[kx][ky][kz] = T[fold(kx)][fold(ky)][kz], fold(k) = min(k, D - k)
+__global__ void k_green_unfold(int Mt, const double* __restrict__ T, double* __restrict__ half) {
+    const int D = 2 * Mt, Dh = Mt + 1;
+    const int64_t tot = static_cast<int64_t>(D) * D * Dh;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < tot;
          q += stride) {
-        const int l = static_cast<int>(q % D);
-        const int j = static_cast<int>((q / D) % D);
-        const int i = static_cast<int>(q / (static_cast<int64_t>(D) * D));
-        auto src = [&](int p) {
-            const int off = p < Mt ? p : p - D;
-            return off >= 0 ? off : off + sM;
-        };
-        const double v = grid[(static_cast<int64_t>(src(i)) * sM + src(j)) * sMpitch + src(l)];
-        trunc[(static_cast<int64_t>(i) * D + j) * (D + 2) + l] = v * scale;
+        const int l = static_cast<int>(q % Dh);
+        const int j = static_cast<int>((q / Dh) % D);
+        const int i = static_cast<int>(q / (static_cast<int64_t>(Dh) * D));
+        const int fi = i <= Mt ? i : D - i, fj = j <= Mt ? j : D - j;
+        half[q] = T[(static_cast<int64_t>(fi) * Dh + fj) * Dh + l];
     }
-}
-
-__global__ void k_green_real(const double2* __restrict__ spec, int64_t n, double* __restrict__ G) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
-         q += stride)
-        G[q] = spec[q].x;
 }
 
 __global__ void k_full_to_half(int D, const double* __restrict__ full, double* __restrict__ half) {
@@ -313,24 +300,16 @@ void launch_direct(const Launch& L, int kind, const double* pos, const double* s
     ++*L.launches;
 }
 
-void launch_green_fill(const Launch& L, int gkind, int sM, double dk, double R, double2* half) {
-    const int64_t tot = static_cast<int64_t>(sM) * sM * (sM / 2 + 1);
-    k_green_fill<<<grid_stride_blocks(tot), TPB, 0, L.s>>>(gkind, sM, dk, R, half);
+void launch_green_octant(const Launch& L, int gkind, int sM, double dk, double R, double* oct) {
+    const int64_t nq = sM / 2 + 1;
+    k_green_octant<<<grid_stride_blocks(nq * nq * nq), TPB, 0, L.s>>>(gkind, sM, dk, R, oct);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
 
-void launch_green_window(const Launch& L, int sM, int64_t sMpitch, int Mt, const double* grid,
-                         double scale, double* trunc) {
+void launch_green_unfold(const Launch& L, int Mt, const double* T, double* half) {
     const int64_t D = 2 * Mt;
-    k_green_window<<<grid_stride_blocks(D * D * D), TPB, 0, L.s>>>(sM, sMpitch, Mt, grid, scale,
-                                                                   trunc);
-    FSE_LAUNCH_CHECK();
-    ++*L.launches;
-}
-
-void launch_green_real(const Launch& L, const double2* spec, int64_t n, double* G) {
-    k_green_real<<<grid_stride_blocks(n), TPB, 0, L.s>>>(spec, n, G);
+    k_green_unfold<<<grid_stride_blocks(D * D * (Mt + 1)), TPB, 0, L.s>>>(Mt, T, half);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
@@ -345,6 +324,71 @@ void launch_green_full_to_half(const Launch& L, int D, const double* full, doubl
 void launch_green_half_to_full(const Launch& L, int D, const double* half, double* full) {
     const int64_t n = static_cast<int64_t>(D) * D * D;
     k_half_to_full<<<grid_stride_blocks(n), TPB, 0, L.s>>>(D, half, full);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+// ---------------------------------------------------------------- x-pass probe
+// Diagnostics for fse_cuda_xscale_probe: deterministic pseudo-random spectra
+// and Green's tables from splitmix64(seed + index), u = (z >> 11) 2^-53
+// (tests/test_gpu_xpass_oracle.py regenerates the same values in numpy).
+__device__ __forceinline__ double probe_u(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return static_cast<double>(x >> 11) * 0x1.0p-53;
+}
+
+__global__ void k_probe_fill(double2* C, int64_t n, uint64_t seed) {
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        C[q] = make_double2(probe_u(seed + 2 * q) - 0.5, probe_u(seed + 2 * q + 1) - 0.5);
+}
+
+__global__ void k_probe_green(double* G, int64_t n, uint64_t seed) {
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        G[q] = 0.5 + probe_u(seed + q);
+}
+
+// out[p][c][x] = C[c][x][ky_p][kz_p] (c < 3, x < Mt); gcol[p][kx] = G[kx][ky_p][kz_p]
+__global__ void k_probe_extract(const double2* C, const double* G, int Mt, int D, int nprobe,
+                                const int* ky, const int* kz, double2* out, double* gcol) {
+    const int Dh = D / 2 + 1;
+    const int64_t n = static_cast<int64_t>(nprobe) * 3 * Mt;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(q / (3 * Mt));
+        const int r = static_cast<int>(q - static_cast<int64_t>(p) * 3 * Mt);
+        const int c = r / Mt, x = r - c * Mt;
+        out[q] = C[((static_cast<int64_t>(c) * Mt + x) * D + ky[p]) * Dh + kz[p]];
+    }
+    const int64_t m = static_cast<int64_t>(nprobe) * D;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < m;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(q / D), kx = static_cast<int>(q - static_cast<int64_t>(p) * D);
+        gcol[q] = G[(static_cast<int64_t>(kx) * D + ky[p]) * Dh + kz[p]];
+    }
+}
+
+void launch_probe_fill(const Launch& L, double2* C, int64_t n, uint64_t seed) {
+    k_probe_fill<<<grid_stride_blocks(n), TPB, 0, L.s>>>(C, n, seed);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_probe_green(const Launch& L, double* G, int64_t n, uint64_t seed) {
+    k_probe_green<<<grid_stride_blocks(n), TPB, 0, L.s>>>(G, n, seed);
+    FSE_LAUNCH_CHECK();
+    ++*L.launches;
+}
+
+void launch_probe_extract(const Launch& L, const double2* C, const double* G, int Mt, int D,
+                          int nprobe, const int* ky, const int* kz, double2* out, double* gcol) {
+    const int64_t n = static_cast<int64_t>(nprobe) * (3 * Mt > D ? 3 * Mt : D);
+    k_probe_extract<<<grid_stride_blocks(n), TPB, 0, L.s>>>(C, G, Mt, D, nprobe, ky, kz, out,
+                                                            gcol);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }

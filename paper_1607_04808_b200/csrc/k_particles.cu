@@ -72,7 +72,7 @@ __global__ void k_payload(GridParams g, const double* __restrict__ pos,
                           const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
                           int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
                           double* __restrict__ w, double* __restrict__ fs, bool fold_prefac,
-                          int slab_only) {
+                          int slab_only, bool naive) {
     extern __shared__ double stage[];
     __shared__ bool keep_row[128];
     const int P = g.P, W3 = 3 * P, RS = W3 + 1;
@@ -103,7 +103,16 @@ __global__ void k_payload(GridParams g, const double* __restrict__ pos,
         if (keep) {
             double* row = stage + threadIdx.x * RS;
 #pragma unroll 1
-            for (int ax = 0; ax < 3; ++ax) {
+            for (int ax = 0; ax < 3 && naive; ++ax) {
+                // axis_weights_naive (ewald.cpp:53-66): one exp per node
+                const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
+                for (int p = 0; p < P; ++p) {
+                    const double dx = (static_cast<double>(first[ax] + p) - s[ax]) * g.h;
+                    row[ax * P + p] = scale * exp(-g.alpha * dx * dx);
+                }
+            }
+#pragma unroll 1
+            for (int ax = 0; ax < 3 && !naive; ++ax) {
                 const double x0 = (first[ax] - s[ax]) * g.h;
                 const double e0 = exp(-g.alpha * x0 * x0);
                 const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
@@ -195,7 +204,7 @@ void launch_quad_table(const Launch& L, const GridParams& g, double* q) {
 void launch_gather_payload(const Launch& L, const GridParams& g, const double* pos,
                            const double* str, int a, const uint32_t* perm, int64_t n,
                            const double* qtab, int32_t* i0s, double* w, double* fs,
-                           bool fold_prefac, int slab_only) {
+                           bool fold_prefac, int slab_only, bool naive) {
     if (n <= 0) return;
     // block size: as many warps (<= 4) as fit 48 KB of staged weight rows;
     // wider supports take one warp and opt-in shared memory
@@ -210,7 +219,7 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
     }
     k_payload<<<blocks_for(n, tpb), tpb, row_bytes * tpb, L.s>>>(g, pos, str, a, perm, n, qtab,
                                                                   i0s, w, fs, fold_prefac,
-                                                                  slab_only);
+                                                                  slab_only, naive);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }

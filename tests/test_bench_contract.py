@@ -13,8 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_reference_arm_prints_one_json_line():
-    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "cfg2",
-                        "--steps", "1", "--warmup", "0", "--ref-frac", "512"],
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "cfg1",
+                        "--steps", "2", "--warmup", "1"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip()]
@@ -30,6 +30,19 @@ def test_reference_arm_prints_one_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
     assert d["cpu_baseline"]["cores"] >= 1
+    # the full workload, timed (no sub-box, no extrapolation), without the product library
+    assert d["config"]["N"] == 10_000 and d["config"]["NT"] == 10_000
+    assert d["steps"] == 2 and d["warmup"] == 1 and len(d["config"]["seconds_per_call"]) == 2
+    assert d["config"]["product_library_loaded"] is False
+    assert abs(d["ms_per_step"] - 1e3 * sorted(d["config"]["seconds_per_call"])[0]) <= \
+        1e3 * abs(d["config"]["seconds_per_call"][1] - d["config"]["seconds_per_call"][0]) + 1e-6
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
 
 
 @pytest.mark.gpu

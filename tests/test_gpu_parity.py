@@ -198,3 +198,28 @@ def test_total_sum_large_support(fse, ctx, oracle, rng, kind, n):
         ref = oracle.direct_sum(kind, s.positions, s.strengths, s.positions, True)
         e_gpu, e_or = fse.rms_error(got, ref, True), fse.rms_error(want, ref, True)
         assert e_gpu < max(1e-12, 2 * e_or)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_spread_naive_weights_vs_reference(fse, ctx, ref, rng, kind):
+    """spread(..., use_fgg=false) (ewald.cpp:53-66) against the reference's own
+    naive-weight spread (deterministic), and FGG = naive to 1e-13
+    (test_spectral.cpp:102-122)."""
+    args = (1.0, 8.0, 0.3, 24, 16)
+    cfg = fse.make_config(*args)
+    s = system(fse, rng, kind, 500)
+    got = ctx.spread(s, cfg, kind, use_fgg=False)
+    want = ref.spread(ref.make_config(*args), kind, s.positions, s.strengths, use_fgg=False,
+                      deterministic=True)
+    assert rel_max(got, want) <= 1e-13
+    assert rel_max(ctx.spread(s, cfg, kind, use_fgg=True), got) <= 1e-13
+
+
+@pytest.mark.parametrize("gkind", [0, 1])
+def test_green_precompute_vs_reference_larger(fse, ctx, ref, gkind):
+    """The pruned cosine-pass precompute against the reference's sM^3 FFT
+    precompute (greens.cpp:48-113) at Mtilde = 60 (sM = 164)."""
+    sf = 1.0 + np.sqrt(3.0)
+    g = ctx.precompute_mollified_green(gkind, 1.1, 60, sf)
+    want = ref.precompute_green(gkind, 1.1, 60, sf)
+    assert rel_max(g.fourier, want) <= 1e-13
