@@ -293,6 +293,19 @@ int or_support(const or_cfg* c, const double* x, int use_fgg, int* i0, double* w
     return 0;
 }
 
+/* or_support over many points (test convenience, ewald.cpp:33-51 index rule) */
+int64_t or_support_index(const or_cfg* c, const double* pts, int64_t n, int* i0) {
+    int64_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+    for (int64_t q = 0; q < n; ++q) {
+        double w[3 * 64];
+        double* wa = c->P <= 64 ? w : (double*)malloc(sizeof(double) * 3 * c->P);
+        if (or_support(c, pts + 3 * q, 1, i0 + 3 * q, wa)) ++bad;
+        if (wa != w) free(wa);
+    }
+    return bad;
+}
+
 /* ewald.cpp:70-85: block key, stable order within a block */
 static int64_t* spatial_order(const double* pts, int64_t n, double block, double L) {
     int nb = (int)(L / block);

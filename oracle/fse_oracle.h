@@ -46,6 +46,8 @@ int or_real_space_sum(int kind, const double* pos, const double* str, int64_t n,
 
 /* per-point support: first index per axis and the 3P FGG axis weights */
 int or_support(const or_cfg* cfg, const double* x, int use_fgg, int* i0, double* w);
+/* i0 of n points (n x 3 ints), or_support's index rule; returns #points out of the grid */
+int64_t or_support_index(const or_cfg* cfg, const double* pts, int64_t n, int* i0);
 
 int or_spread(const or_cfg* cfg, int kind, const double* pos, const double* str, int64_t n,
               double box_side, int use_fgg, double* grid);

@@ -144,6 +144,18 @@ def support(cfg: Cfg, x, use_fgg=True):
     return i0, w.reshape(3, cfg.P), rc == 0
 
 
+def support_index(cfg: Cfg, pts):
+    """i0 of every point (n, 3) int32 (or_support_index)."""
+    pts = _a(pts).reshape(-1, 3)
+    i0 = np.zeros((pts.shape[0], 3), np.int32)
+    f = lib().or_support_index
+    f.restype = C.c_int64
+    f.argtypes = [C.POINTER(_OrCfg), _dp, C.c_int64, _i32p]
+    c = _c(cfg)
+    f(C.byref(c), pts, pts.shape[0], i0)
+    return i0
+
+
 def spread(cfg: Cfg, kind, pos, strengths, use_fgg=True, box_side=None):
     pos, strengths = _a(pos), _a(strengths)
     Mt = cfg.Mtilde

@@ -282,6 +282,11 @@ extern __shared__ __align__(16) unsigned char fse_smem[];
 // Asynchronous global -> shared copies (LDGSTS): every load of a pass is in
 // flight at once instead of one register round trip per element, which is
 // what bounds these strided column gathers.  src_bytes = 0 zero-fills.
+// L2 prefetch (no register, no completion wait): data a kernel reads later
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
@@ -815,6 +820,14 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
         const int row = (i + blk * bstep + comp * g.nxs) * g.nkys + kyl;
         return Ck + static_cast<int64_t>(row) * Dh + c;
     };
+    // the multiplier's Green's column G[kx][ky][kz0 .. kz0 + nc) is read ~10 us
+    // later, one dependent load per element: prefetch it into L2 now (24 B of
+    // each 32 B sector, ~15 KB per CTA) so those loads hit L2 instead of HBM
+    for (int kx = threadIdx.x; kx < D; kx += blockDim.x) {
+        const double* gp = G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0;
+        prefetch_l2(gp);
+        prefetch_l2(gp + nc - 1);
+    }
     // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (k_ex_axis, once per
     // call): rem = ex[kx] * ex[ky] * ex[kz]
     double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
