@@ -157,6 +157,43 @@ fse_status fse_cuda_slab_scale_peers(fse_cuda_ctx* ctx, const fse_config* cfg, i
                                      const fse_green* green, int rank, int nslabs,
                                      double* d_spec, double* const* dst_bufs);
 
+/* ---- partitioned multi-GPU evaluation (no reference counterpart).
+ * Each rank (one GPU, one process or thread) holds only the points it OWNS: a point
+ * at x belongs to the slab whose x-planes hold its support centre ceil((x - origin)/h)
+ * (fse_dist_owner).  One call of fse_cuda_dist_total_sum on every rank exchanges, over
+ * NCCL (grouped ncclSend / ncclRecv on the context's stream):
+ *   the ghost sources each neighbour needs (supports crossing into its planes,
+ *   real-space neighbours within rc of its owned targets) and the targets whose
+ *   support crosses into its planes; the two spectrum transposes of the distributed
+ *   FFT; and the ghost targets' partial quadrature sums back to their owners.
+ * u receives the velocities of this rank's owned targets, in their input order
+ * (n_total: the global source count, which fixes the cell-list geometry).
+ * fse_cuda_nccl_unique_id fills the 128-byte ncclUniqueId that rank 0 creates and the
+ * caller broadcasts (any channel) before fse_cuda_dist_create. */
+typedef struct fse_dist fse_dist;
+fse_status fse_cuda_nccl_unique_id(void* id128);
+fse_status fse_cuda_dist_create(fse_cuda_ctx* ctx, int rank, int nranks, const void* id128,
+                                fse_dist** out);
+void fse_cuda_dist_destroy(fse_dist* d);
+fse_status fse_cuda_dist_total_sum(fse_dist* d, const fse_config* cfg, int kind,
+                                   const double* d_pos, const double* d_str, int64_t n_own,
+                                   int64_t n_total, const double* d_tgt, int64_t nt_own, int tas,
+                                   const fse_green* green, double* d_u);
+/* owner rank of each of n host points (x = pos[3 i]) for nranks slabs (host, no GPU) */
+fse_status fse_dist_owner(const fse_config* cfg, int nranks, const double* pos, int64_t n,
+                          int32_t* owner);
+/* bit masks of the ranks that need each host point as a source (ghost rule) or as a
+ * target (quadrature share); the owner's bit is always set (host, no GPU) */
+fse_status fse_dist_masks(const fse_config* cfg, int nranks, const double* pos, int64_t n,
+                          int targets, uint32_t* mask);
+/* the whole partitioned algorithm with nranks VIRTUAL ranks on this context's device
+ * (exchanges as device copies): partitions all n points by the ownership rule, runs
+ * every step of every rank, returns u for all targets in caller order (tests) */
+fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* ctx, int nranks, const fse_config* cfg,
+                                           int kind, const double* d_pos, const double* d_str,
+                                           int64_t n, const double* d_tgt, int64_t nt, int tas,
+                                           const fse_green* green, double* d_u);
+
 /* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
 fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);
 /* overlap the real-space sum (second stream) with the Fourier part of total sums

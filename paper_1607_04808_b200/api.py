@@ -271,6 +271,18 @@ def _load():
         lib.fse_cuda_direct_sum.argtypes = [vp, C.c_int, _dp, _dp, i64, _dp, i64, C.c_int, _dp]
         lib.fse_cuda_fft3d.argtypes = [vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int]
         lib.fse_cuda_fft_columns.argtypes = [vp, C.c_int, C.c_int, _dp, C.c_int]
+        lib.fse_cuda_nccl_unique_id.argtypes = [vp]
+        lib.fse_cuda_dist_create.argtypes = [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]
+        lib.fse_cuda_dist_destroy.argtypes = [vp]
+        lib.fse_cuda_dist_total_sum.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp, vp, i64,
+                                                i64, vp, i64, C.c_int, vp, vp]
+        lib.fse_cuda_dist_virtual_total_sum.argtypes = [vp, C.c_int, C.POINTER(EwaldConfig),
+                                                        C.c_int, vp, vp, i64, vp, i64, C.c_int,
+                                                        vp, vp]
+        lib.fse_dist_owner.argtypes = [C.POINTER(EwaldConfig), C.c_int, _dp, i64,
+                                       C.POINTER(C.c_int32)]
+        lib.fse_dist_masks.argtypes = [C.POINTER(EwaldConfig), C.c_int, _dp, i64, C.c_int,
+                                       C.POINTER(C.c_uint32)]
         lib.fse_cuda_xscale_probe.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, vp,
                                               C.c_uint64, C.c_int, C.POINTER(C.c_int),
                                               C.POINTER(C.c_int), _dp, _dp]
@@ -629,6 +641,54 @@ class Context:
                    ky.ctypes.data_as(ip), kz.ctypes.data_as(ip), out.ctypes.data_as(_dp), _p(gcol))
         return out, gcol
 
+    # -- partitioned multi-GPU evaluation (fse_dist)
+    def dist_virtual_total_sum(self, system: SourceSystem, kind, cfg, targets, green, nranks,
+                               targets_are_sources=False):
+        """The partitioned algorithm (ownership, ghost exchange, distributed FFT,
+        partial-sum return) with `nranks` virtual ranks on this device; u in
+        caller order."""
+        t = system.positions if targets_are_sources else _f64(targets, (-1, 3))
+        n, nt = system.size(), t.shape[0]
+        ptrs = []
+        try:
+            def up(a):
+                p = self.dev_alloc(max(a.nbytes, 8))
+                ptrs.append(p)
+                if a.nbytes:
+                    self.memcpy(p, a.ctypes.data, a.nbytes)
+                return p
+            dp, ds = up(system.positions), up(system.strengths)
+            dt = dp if targets_are_sources else up(t)
+            du = self.dev_alloc(max(24 * nt, 8))
+            ptrs.append(du)
+            self._call(_load().fse_cuda_dist_virtual_total_sum, int(nranks), C.byref(cfg),
+                       int(kind), C.c_void_p(dp), C.c_void_p(ds), n, C.c_void_p(dt), nt,
+                       int(bool(targets_are_sources)), green.handle, C.c_void_p(du))
+            u = np.empty((nt, 3))
+            if nt:
+                self.memcpy(u.ctypes.data, du, u.nbytes)
+            return u
+        finally:
+            for p in ptrs:
+                self.dev_free(p)
+
+    def dist_create(self, rank: int, nranks: int, unique_id: bytes):
+        """NCCL rank of the partitioned evaluation (fse_cuda_dist_create)."""
+        h = C.c_void_p()
+        idb = C.create_string_buffer(bytes(unique_id), 128)
+        self._call(_load().fse_cuda_dist_create, int(rank), int(nranks), idb, C.byref(h))
+        return h
+
+    def dist_total_sum(self, dist, cfg, kind, d_pos, d_str, n_own, n_total, d_tgt, nt_own, tas,
+                       green, d_u):
+        """fse_cuda_dist_total_sum on device pointers (this rank's owned points)."""
+        st = _load().fse_cuda_dist_total_sum(dist, C.byref(cfg), int(kind), C.c_void_p(d_pos),
+                                             C.c_void_p(d_str), int(n_own), int(n_total),
+                                             C.c_void_p(d_tgt), int(nt_own), int(bool(tas)),
+                                             green.handle, C.c_void_p(d_u))
+        if st != 0:
+            _raise(st, _load().fse_cuda_last_error(self.handle).decode())
+
     def fft3d(self, data, inverse=False):
         d = np.ascontiguousarray(data, dtype=np.complex128).copy()
         n0, n1, n2 = d.shape
@@ -770,6 +830,37 @@ def generate_system(kind, n, L, seed) -> SourceSystem:
 
 
 WL_UNIFORM, WL_SPHERE, WL_CLUSTERED, WL_UNIFORM_TARGETS = 1, 3, 4, 5
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 makes it; the caller broadcasts it)."""
+    b = C.create_string_buffer(128)
+    st = _load().fse_cuda_nccl_unique_id(b)
+    if st != 0:
+        raise FseRuntimeError("ncclGetUniqueId failed")
+    return b.raw
+
+
+def dist_owner(cfg: EwaldConfig, nranks: int, positions) -> np.ndarray:
+    """Owner slab of every point (fse_dist_owner; host)."""
+    p = _f64(positions, (-1, 3))
+    out = np.empty(p.shape[0], np.int32)
+    st = _load().fse_dist_owner(C.byref(cfg), int(nranks), _p(p), p.shape[0],
+                                out.ctypes.data_as(C.POINTER(C.c_int32)))
+    if st != 0:
+        raise InvalidArgument("dist_owner: bad arguments")
+    return out
+
+
+def dist_masks(cfg: EwaldConfig, nranks: int, positions, targets: bool) -> np.ndarray:
+    """Bit masks of the ranks that need each point (fse_dist_masks; host)."""
+    p = _f64(positions, (-1, 3))
+    out = np.empty(p.shape[0], np.uint32)
+    st = _load().fse_dist_masks(C.byref(cfg), int(nranks), _p(p), p.shape[0], int(bool(targets)),
+                                out.ctypes.data_as(C.POINTER(C.c_uint32)))
+    if st != 0:
+        raise InvalidArgument("dist_masks: bad arguments")
+    return out
 
 
 def generate_workload(which: int, n: int, seed: int):

@@ -4,6 +4,8 @@
 // bench.py), plus small scalar helpers.  Plain C++; exported through the
 // C-ABI in include/fse_host.h.
 #include "fse_host.h"
+#include "fse_cuda.h"
+#include "../fse_dist_rules.h"
 
 #include <algorithm>
 #include <cmath>
@@ -94,6 +96,34 @@ int fse_generate_workload(int which, int64_t n, uint64_t seed, double* pos, doub
         }
     }
     return 1;
+}
+
+// z-slab ownership and halo masks (fse_dist_rules.h), host side: the same
+// arithmetic the device engine (fse_dist.cuh) uses, so a caller can partition
+// its input before fse_cuda_dist_total_sum
+static bool dist_geom(const fse_config* cfg, int nranks, fsedist::Geom* q) {
+    if (!cfg || nranks < 1 || nranks > 16 || cfg->Mtilde < 1 || !(cfg->h > 0)) return false;
+    const int Mt = cfg->Mtilde;
+    const int nxs = nranks > 1 ? ((Mt + nranks - 1) / nranks + 7) / 8 * 8 : Mt;
+    *q = fsedist::Geom{nranks, nxs, Mt, cfg->P, -cfg->deltaL / 2, cfg->h, cfg->rc / cfg->h};
+    return true;
+}
+
+fse_status fse_dist_owner(const fse_config* cfg, int nranks, const double* pos, int64_t n,
+                          int32_t* owner) {
+    fsedist::Geom q;
+    if (!dist_geom(cfg, nranks, &q) || n < 0 || (n > 0 && (!pos || !owner))) return FSE_EINVAL;
+    for (int64_t i = 0; i < n; ++i) owner[i] = fsedist::owner_of(pos[3 * i], q);
+    return FSE_OK;
+}
+
+fse_status fse_dist_masks(const fse_config* cfg, int nranks, const double* pos, int64_t n,
+                          int targets, uint32_t* mask) {
+    fsedist::Geom q;
+    if (!dist_geom(cfg, nranks, &q) || n < 0 || (n > 0 && (!pos || !mask))) return FSE_EINVAL;
+    for (int64_t i = 0; i < n; ++i)
+        mask[i] = targets ? fsedist::target_mask(pos[3 * i], q) : fsedist::source_mask(pos[3 * i], q);
+    return FSE_OK;
 }
 
 }  // extern "C"

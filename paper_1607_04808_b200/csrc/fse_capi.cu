@@ -361,12 +361,14 @@ Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, con
 // true count from device memory.
 // part / nparts > 1: only the targets in x-slice `part` of the cell grid
 // (whole cells, so work items stay full); the others' d_uR entries are zero
+// n_geom >= 0: the point count that fixes the cell geometry (the global N when
+// d_pos holds one rank's local sources, so the bins are the reference's)
 void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_str, int64_t n,
                double box_side, double xi, double rc, const double* d_tgt, int64_t nt, bool tas,
-               double* d_uR, int part = 0, int nparts = 1) {
+               double* d_uR, int part = 0, int nparts = 1, int64_t n_geom = -1) {
     if (!(xi > 0) || !(rc > 0)) invalid("real_space_sum: xi and rc must be positive");
     const int a = arity_of(kind);
-    const CellGrid cg = cell_grid(n, box_side, rc, 0.0);
+    const CellGrid cg = cell_grid(n_geom >= 0 ? n_geom : n, box_side, rc, 0.0);
     Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n);
     Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt);
     Launch L = L1(c);
@@ -1544,3 +1546,5 @@ static_assert(sizeof(fse_config) == 120, "fse_config must mirror fse::EwaldConfi
 static_assert(offsetof(fse_config, Mtilde) == 80, "EwaldConfig layout");
 static_assert(offsetof(fse_config, kinf) == 88, "EwaldConfig layout");
 static_assert(offsetof(fse_config, deterministic) == 112, "EwaldConfig layout");
+
+#include "fse_dist.cuh"
