@@ -221,75 +221,62 @@ def stage_models(w, cfg, n, nt, rs_pairs=None):
     return models
 
 
-# ------------------------------------------------------------------ ours, z-slabs
-def run_slabs(args, dist: Dist):
-    """N > 1: one evaluation of the workload decomposed into N z-slabs
-    (paper_1607_04808_b200/slabs.py): the same system on every rank,
-    NCCL all-to-all spectrum transposes and one sum of partial velocities.
-    Total work fixed as N grows: strong scaling."""
+# ------------------------------------------------------------------ ours, partitioned
+def run_dist(args, dist: Dist):
+    """N > 1: one evaluation of the workload with the particles PARTITIONED over N
+    x-slabs (fse_cuda_dist_*): each rank holds only
+    the points it owns (fse_dist_owner) and the library exchanges ghost sources and
+    targets, the two spectrum transposes and the ghost partial sums over NCCL
+    (grouped ncclSend / ncclRecv).  Total work fixed as N grows: strong scaling."""
     import torch
     import paper_1607_04808_b200 as fse
-    from paper_1607_04808_b200.slabs import SlabSum, TorchExchange
 
     w = WORKLOADS[args.workload]
     ctx = fse.Context(dist.local)
-    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED)  # replicated inputs
-    targets = system.positions if tgt is None else tgt
-    n, nt = system.size(), targets.shape[0]
+    system, tgt = fse.generate_workload(w["wl"], w["n"], SEED)  # same stream on every rank
     tas = tgt is None
+    targets = system.positions if tas else tgt
+    n_total, nt_total = system.size(), targets.shape[0]
     cfg = fse.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
-    green = ctx.precompute_mollified_green(int(fse.green_kind_for(w["kind"])), cfg.Ltilde,
-                                           cfg.Mtilde, cfg.sf)
-    d_pos = ctx.dev_alloc(system.positions.nbytes)
-    d_str = ctx.dev_alloc(system.strengths.nbytes)
-    d_tgt = d_pos if tas else ctx.dev_alloc(targets.nbytes)
-    d_u = ctx.dev_alloc(8 * 3 * nt)
-    hp = ctx.host_alloc(system.positions.shape)
-    hs = ctx.host_alloc(system.strengths.shape)
-    hp[...] = system.positions
-    hs[...] = system.strengths
-    ht = hp if tas else ctx.host_alloc(targets.shape)
+    G, r = dist.world, dist.rank
+    own_s = np.nonzero(fse.dist_owner(cfg, G, system.positions) == r)[0]
+    own_t = own_s if tas else np.nonzero(fse.dist_owner(cfg, G, targets) == r)[0]
+    hp = ctx.host_alloc((own_s.size, 3))
+    hs = ctx.host_alloc((own_s.size, system.strengths.shape[1]))
+    hp[...] = system.positions[own_s]
+    hs[...] = system.strengths[own_s]
+    ht = hp if tas else ctx.host_alloc((own_t.size, 3))
     if not tas:
-        ht[...] = targets
-    u_host = ctx.host_alloc((nt, 3))
+        ht[...] = targets[own_t]
+    hu = ctx.host_alloc((own_t.size, 3))
+    del system, tgt, targets
+    n_own, nt_own = own_s.size, own_t.size
+    d_pos = ctx.dev_alloc(max(hp.nbytes, 8))
+    d_str = ctx.dev_alloc(max(hs.nbytes, 8))
+    d_tgt = d_pos if tas else ctx.dev_alloc(max(ht.nbytes, 8))
+    d_u = ctx.dev_alloc(max(24 * nt_own, 8))
 
     def upload():
-        ctx.memcpy(d_pos, hp.ctypes.data, hp.nbytes)
-        ctx.memcpy(d_str, hs.ctypes.data, hs.nbytes)
-        if not tas:
+        if hp.nbytes:
+            ctx.memcpy(d_pos, hp.ctypes.data, hp.nbytes)
+            ctx.memcpy(d_str, hs.ctypes.data, hs.nbytes)
+        if not tas and ht.nbytes:
             ctx.memcpy(d_tgt, ht.ctypes.data, ht.nbytes)
 
     upload()
-    ex = TorchExchange()
-    ss = SlabSum(ctx, cfg, w["kind"], dist.rank, dist.world)
-    from paper_1607_04808_b200.slabs import PeerExchange, torch_view
-
-    # exchange: peer-direct stores over NVLink (symmetric memory) unless it is
-    # unavailable or disagrees with the all-to-all path on a first evaluation
-    px, why = None, None
-    if args.exchange == "p2p" or (args.exchange == "auto" and dist.world > 1):
-        try:
-            px = PeerExchange(ss.block_doubles * ss.nslabs)
-        except Exception as e:  # noqa: BLE001 -- plumbing fallback, reported in the JSON
-            if args.exchange == "p2p":
-                raise
-            why = f"symmetric memory unavailable ({type(e).__name__}: {str(e)[:160]})"
-    if px is not None:
-        ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
-        ref = torch_view(d_u, 3 * nt).clone()
-        ss.run_peers(px, ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
-        differ = 0 if torch.equal(ref, torch_view(d_u, 3 * nt)) else 1
-        del ref
-        if dist.max(differ) != 0:
-            if args.exchange == "p2p":
-                raise RuntimeError("peer-direct exchange differs from the all-to-all path")
-            px, why = None, "peer-direct result differed from the all-to-all path"
+    green = ctx.precompute_mollified_green(int(fse.green_kind_for(w["kind"])), cfg.Ltilde,
+                                           cfg.Mtilde, cfg.sf)
+    # NCCL communicator of the library: rank 0's unique id, broadcast over the
+    # torch.distributed group
+    uid = torch.zeros(128, dtype=torch.uint8, device=dist.dev)
+    if r == 0:
+        uid[:] = torch.frombuffer(bytearray(fse.nccl_unique_id()), dtype=torch.uint8)
+    dist.td.broadcast(uid, 0)
+    handle = ctx.dist_create(r, G, bytes(uid.cpu().numpy().tobytes()))
 
     def step():
-        if px is not None:
-            ss.run_peers(px, ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
-        else:
-            ss.run(ex, green, d_pos, d_str, n, d_tgt, nt, tas, d_u)
+        ctx.dist_total_sum(handle, cfg, w["kind"], d_pos, d_str, n_own, n_total, d_tgt, nt_own,
+                           tas, green, d_u)
 
     for _ in range(args.warmup):
         step()
@@ -299,95 +286,59 @@ def run_slabs(args, dist: Dist):
     launches0 = ctx.launch_count
     dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    ctx.mark()
     for _ in range(args.steps):
         step()
-    e1.record()
-    torch.cuda.synchronize()
-    dev_ms = e0.elapsed_time(e1)
+    ctx.mark()
+    dev_ms = ctx.elapsed_ms()
     launches = ctx.launch_count - launches0
     clk = clocks.stop()
     dist.barrier()
     max_ms = dist.max(dev_ms)
 
-    # phase breakdown (untimed step, host-synchronised phases)
-    ph = {}
-
-    def phase(name, fn):
-        t0 = time.perf_counter()
-        fn()
-        ph[name] = time.perf_counter() - t0
-
-    r, G = dist.rank, dist.world
-    if px is not None:
-        fwd, bwd = px.ptrs
-        phase("forward_peer_stores", lambda: ctx.slab_forward_peers(
-            cfg, w["kind"], d_pos, d_str, n, r, G, fwd))
-        phase("barrier", px.barrier)
-        phase("scale_peer_stores", lambda: ctx.slab_scale_peers(
-            cfg, w["kind"], green, r, G, fwd[r], bwd))
-        phase("barrier_back", px.barrier)
-        phase("inverse_gather_realspace", lambda: ctx.slab_inverse(
-            cfg, w["kind"], d_pos, d_str, n, bwd[r], r, G, d_tgt, nt, int(tas), d_u))
-    else:
-        send_t = torch_view(ss.d_send, ss.block_doubles * ss.nslabs)
-        recv_t = torch_view(ss.d_recv, ss.block_doubles * ss.nslabs)
-        phase("forward", lambda: ss.forward(d_pos, d_str, n))
-        phase("all_to_all", lambda: ex.all_to_all(send_t, recv_t))
-        phase("scale", lambda: ss.scale(green))
-        phase("all_to_all_back", lambda: ex.all_to_all(recv_t, send_t))
-        phase("inverse_gather_realspace", lambda: ss.inverse(d_pos, d_str, n, d_tgt, nt, tas,
-                                                             d_u))
-    phase("sum_partials", lambda: ex.all_reduce_sum(torch_view(d_u, 3 * nt)))
-
-    # e2e: pinned host inputs -> device every step, result back on every rank
+    # e2e: each rank's owned inputs from pinned host memory, its owned velocities back
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(max(1, args.steps)):
         upload()
         step()
-        ctx.memcpy(u_host.ctypes.data, d_u, u_host.nbytes)
+        if hu.nbytes:
+            ctx.memcpy(hu.ctypes.data, d_u, hu.nbytes)
     e2e_s = dist.max(time.perf_counter() - t0)
     h2d = hp.nbytes + hs.nbytes + (0 if tas else ht.nbytes)
 
-    # roofline: the step's algorithmic FP64 work per rank over the step time
     a = 9 if w["kind"] == 1 else 3
-    flops = 2.0 * a * cfg.P ** 3 * n + 2.0 * 3 * cfg.P ** 3 * nt
+    flops = 2.0 * a * cfg.P ** 3 * n_total + 2.0 * 3 * cfg.P ** 3 * nt_total
     fp64_peak = args.fp64_peak or ctx.measure_fp64_peak()
-    ach = flops / dist.world / (max_ms / args.steps * 1e-3) / 1e12
-    value = nt * args.steps / (max_ms * 1e-3)
+    ach = flops / G / (max_ms / args.steps * 1e-3) / 1e12
+    value = nt_total * args.steps / (max_ms * 1e-3)
+    counts = torch.tensor([n_own, nt_own], dtype=torch.float64, device=dist.dev)
+    allc = [torch.zeros_like(counts) for _ in range(G)]
+    dist.td.all_gather(allc, counts)
     line = {
-        "metric": metric_name(w), "value": value, "unit": "targets/s", "n_gpus": dist.world,
+        "metric": metric_name(w), "value": value, "unit": "targets/s", "n_gpus": G,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}), "
-                "same system on every rank, no dataset",
+        "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}), each "
+                "rank keeps the points its slab owns, no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
-                   "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
-                   "parallelism": f"z-slabs x{dist.world} (" + (
-                       "peer-direct NVLink stores into symmetric memory" if px is not None
-                       else "NCCL all-to-all transposes") + ")",
-                   "exchange_note": why,
-                   "slab": {"x_lo": ss.info.x_lo, "nx": ss.info.nx, "ky_lo": ss.info.ky_lo,
-                            "nky": ss.info.nky},
+                   "N": n_total, "NT": nt_total, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
+                   "parallelism": f"x-slabs x{G}: partitioned particles, NCCL ghost / "
+                                  "transpose / partial-sum exchanges (fse_cuda_dist_total_sum)",
+                   "owned_per_rank": [[int(c[0].item()), int(c[1].item())] for c in allc],
                    "l2": working_set_note(w, cfg)},
-        "e2e": {"value": nt * max(1, args.steps) / e2e_s, "unit": "targets/s",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * 3 * nt),
-                "api": "slabs.SlabSum.run_peers (fse_cuda_slab_*_peers + symmetric memory)"
-                       if px is not None else
-                       "slabs.SlabSum.run (fse_cuda_slab_* + torch.distributed NCCL)"},
+        "e2e": {"value": nt_total * max(1, args.steps) / e2e_s, "unit": "targets/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hu.nbytes),
+                "api": "fse_cuda_dist_total_sum (owned points from pinned host memory per rank)"},
         "roofline": {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": ach / fp64_peak, "kernel": "step (spread + quadrature work / rank)",
                      "traffic": None},
-        "phase_s_rank0": ph,
         "gpu_launches": int(launches),
         "clocks": clk,
         "cpu_baseline": None,
     }
-    if dist.rank == 0:
+    if r == 0:
         emit(line)
-    ss.free()
     for p in (d_pos, d_str, d_u) + (() if tas else (d_tgt,)):
         ctx.dev_free(p)
 
@@ -725,11 +676,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent full evaluations per GPU instead of z-slabs")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
-                    help="slab exchange: peer-direct stores (p2p), NCCL all-to-all, or p2p "
-                         "with a verified fallback to NCCL (auto, N > 1)")
     ap.add_argument("--slabs", action="store_true",
-                    help="use the z-slab path also at N = 1 (one slab, NCCL group of one)")
+                    help="use the partitioned path also at N = 1 (one slab, NCCL group of one)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: stop timing full-size calls after this many seconds")
     ap.add_argument("--fp64-peak", type=float, default=None,
@@ -749,7 +697,7 @@ def main():
     dist = Dist(force_group=args.slabs and args.impl == "ours")
     try:
         if (dist.world > 1 and not args.replicas) or args.slabs:
-            run_slabs(args, dist)
+            run_dist(args, dist)
         else:
             run_ours(args, dist)
     finally:

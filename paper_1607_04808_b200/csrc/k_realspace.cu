@@ -13,21 +13,20 @@
 // ~85% of candidates that fail the test, instead of predicating the whole
 // warp on every candidate.
 //
-// Pair math: with x = xi r and inv = 1/r (rsqrt), every screened kernel is a
-// power of inv times smooth functions of x alone (s = 2/sqrt(pi)):
+// Pair math: with x = xi r and inv = 1/r, every screened kernel is a power
+// of inv times smooth functions of x alone (s = 2/sqrt(pi)):
 //   stokeslet: a - b = inv Ahat(x), a = inv Chat(x),
 //              Ahat = erfc x - s x e^{-x^2},  Chat = erfc x + s x e^{-x^2}
 //   rotlet:    c = inv^2 Chat(x)
 //   stresslet: c1 = -2 inv^2 Dhat(x), c2 = xi^2 Ehat(x),
 //              Dhat = 3 erfc x + s x (3 + 2x^2) e^{-x^2},  Ehat = 2 s x e^{-x^2}
-// With erfc x = e^{-x^2} erfcx(x) they all are e^{-x^2} times polynomials in
-// x and erfcx(x).  erfcx is tabulated on [0, 6.5) as 128 piecewise degree-7
-// Chebyshev fits (monomial in the local t, built in long double from
-// erfcl/expl; max abs error 1.6e-16, rel 3.3e-16) and e^{-x^2} is computed
-// (exp): one 8-byte table load per coefficient per pair -- the pair loop is
-// shared-memory-bandwidth bound, so this halves its dominant traffic relative
-// to tabulating two functions.  x >= 6.5 (only for xi rc > 6.5) uses the
-// erfc/exp formulas directly.
+// The kernel's two functions are tabulated on [0, 6.5) as 128 piecewise
+// degree-7 Chebyshev fits (monomials in the local t, built in long double from
+// erfcl/expl; max abs error 4e-16 of max |F|), stored as (F0_j, F1_j) pairs so a
+// pair costs 8 16-byte shared loads and two independent 7-FMA Horner chains
+// (no exp, no erfc).  Absolute accuracy is what the sum needs: a large x means a
+// small contribution.  1/r: fp32 seed + two fp64 Newton steps.  x >= 6.5 (only
+// for xi rc > 6.5) uses the erfc/exp formulas directly.
 //
 // Candidate test: the closed-ball test is decided in fp32 on coordinates
 // relative to the item's cell centre (FP32 pipe, off the FP64 pipe that
@@ -63,7 +62,9 @@ constexpr double kInvSqrtPi = 0.5641895835477562869;
 
 constexpr int kNI = 128, kDeg = 7;
 constexpr double kXMax = 6.5;
-__constant__ double c_erfcx[kDeg + 1][kNI];
+// the kernel's smooth functions of x = xi r, piecewise degree-7 on kNI intervals
+// of [0, kXMax): [kind][iv][j] = (F0_j, F1_j) monomial coefficients in the local t
+__constant__ double2 c_tab[3][kNI][kDeg + 1];
 
 
 struct FastTest {
@@ -93,36 +94,6 @@ FastTest fp32_bounds(double rc, double side) {
     return f;
 }
 
-// e^y for y in [-kXMax^2, 0]: y = j ln2 + r (|r| <= ln2 / 2, Cody-Waite with
-// FMA), degree-13 Taylor polynomial (remainder < 5e-18 relative), 2^j added
-// to the exponent field (j >= -61: no overflow, underflow or subnormal
-// cases, which is what makes this ~20 instructions instead of the ~45 of
-// the general-purpose exp()).  Max error ~2 ulp (host-checked on a 2e7-point
-// sweep of [-42.25, 0] against expl).
-__device__ __forceinline__ double exp_neg_bounded(double y) {
-    constexpr double kLog2e = 1.4426950408889634074;
-    constexpr double kLn2Hi = 6.93147180559945286227e-01;
-    constexpr double kLn2Lo = 2.31904681384629955842e-17;
-    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    const double k = fma(y, kLog2e, kMagic);      // round(y log2 e) in the low word
-    const double jd = k - kMagic;
-    const int j = __double2loint(k);
-    double r = fma(jd, -kLn2Hi, y);
-    r = fma(jd, -kLn2Lo, r);
-    // Estrin: dependency depth 4 after r instead of 13 (the pair loop
-    // is latency-bound)
-    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-    const double a0 = fma(r, 1.0, 1.0), a1 = fma(r, 1.0 / 6.0, 0.5);
-    const double a2 = fma(r, 1.0 / 120.0, 1.0 / 24.0), a3 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
-    const double a4 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
-    const double a5 = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
-    const double a6 = fma(r, 1.0 / 6227020800.0, 1.0 / 479001600.0);
-    const double b0 = fma(a1, r2, a0), b1 = fma(a3, r2, a2), b2 = fma(a5, r2, a4);
-    const double d0 = fma(b1, r4, b0), d1 = fma(a6, r4, b2);
-    const double p = fma(d1, r8, d0);
-    return __hiloint2double(__double2hiint(p) + j * (1 << 20), __double2loint(p));
-}
-
 // exact functions (fallback beyond the table)
 __device__ __forceinline__ void fn_exact(int which, double x, double* out) {
     const double e = exp(-x * x), ec = erfc(x), s = 2.0 * kInvSqrtPi;
@@ -138,35 +109,44 @@ __device__ __forceinline__ double exact_d2(double rx, double ry, double rz) {
     return __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
 }
 
-// tab: the two functions this kernel needs (stokeslet: Ahat, Chat;
-// rotlet: Chat, -; stresslet: Dhat, Ehat).  TAIL: x = xi r can reach the
-// end of the table (xi rc >= 6.5), so the exact formulas take over there.
+// 1/sqrt(r2): fp32 seed + two Newton steps in fp64 (22 -> 44 -> full bits,
+// ~1 ulp), no special-case branches; r2 < 1e-36 (points closer than 1e-18,
+// only possible near the origin) takes the library rsqrt
+__device__ __forceinline__ double rsqrt_nr(double r2) {
+    if (r2 < 1e-36) return rsqrt(r2);
+    double y = static_cast<double>(rsqrtf(static_cast<float>(r2)));
+    const double h = 0.5 * r2;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y;
+}
+
+// tab: (F0, F1) = the two functions this kernel needs (stokeslet: Ahat, Chat;
+// rotlet: Chat, -; stresslet: Dhat, Ehat), tabulated directly (absolute error
+// < 4e-16; their products with 1/r powers need absolute, not relative,
+// accuracy).  TAIL: x = xi r can reach the end of the table (xi rc >= 6.5), so
+// the exact formulas take over there.
 template <int KIND, bool TAIL>
 __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2, double xi,
-                                     const double* f, const double (*tabx)[kNI], double acc[3]) {
-    const double inv = rsqrt(r2);
+                                     const double* f, const double2 (*tab)[kDeg + 1],
+                                     double acc[3]) {
+    const double inv = rsqrt_nr(r2);
     const double rn = r2 * inv;
     const double xr = xi * rn;
     double F0, F1 = 0.0;
     if (!TAIL || xr < kXMax) {
-        // erfcx(x) from the table (one 8-byte load per coefficient), e^{-x^2}
-        // computed: half the shared-memory traffic of two tabulated functions
         const double uu = xr * (kNI / kXMax);
         const int iv = min(static_cast<int>(uu), kNI - 1);
         const double t = 2.0 * (uu - iv) - 1.0;
-        double ex = tabx[kDeg][iv];
+        const double2* row = tab[iv];
+        double2 cf = row[kDeg];
+        F0 = cf.x;
+        F1 = cf.y;
 #pragma unroll
-        for (int j = kDeg - 1; j >= 0; --j) ex = fma(ex, t, tabx[j][iv]);
-        const double E = exp_neg_bounded(-xr * xr);
-        const double sx = 2.0 * kInvSqrtPi * xr;
-        if (KIND == FSE_STOKESLET) {
-            F0 = E * (ex - sx);
-            F1 = E * (ex + sx);
-        } else if (KIND == FSE_ROTLET) {
-            F0 = E * (ex + sx);
-        } else {
-            F0 = E * (3.0 * ex + sx * (3.0 + 2.0 * xr * xr));
-            F1 = 2.0 * sx * E;
+        for (int j = kDeg - 1; j >= 0; --j) {
+            cf = row[j];
+            F0 = fma(F0, t, cf.x);
+            if (KIND != FSE_ROTLET) F1 = fma(F1, t, cf.y);
         }
     } else {
         fn_exact(KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2), xr, &F0);
@@ -252,10 +232,12 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     auto& sf = wc.sf;
     auto& nb_start = wc.nb_start;
     auto& nb_pref = wc.nb_pref;
-    __shared__ double tabx[kDeg + 1][kNI];
-    for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += blockDim.x) {
-        const int j = e / kNI, iv = e % kNI;
-        tabx[j][iv] = c_erfcx[j][iv];
+    __shared__ double2 tab[kNI][kDeg + 1];
+    {
+        constexpr int ktab = KIND == FSE_STOKESLET ? 0 : (KIND == FSE_STRESSLET ? 1 : 2);
+        const double2* src = &c_tab[ktab][0][0];
+        double2* dst = &tab[0][0];
+        for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += blockDim.x) dst[e] = src[e];
     }
     __syncthreads();  // the only CTA-wide barrier
 
@@ -381,27 +363,39 @@ __global__ void __launch_bounds__(TPB) k_realspace(
 #pragma unroll
             for (int i = 0; i < NW; ++i) npair += __popc(mask[i]);
         }
-        // the mask words as a shift register: m[0] is the current word
-        uint32_t m[NW];
-#pragma unroll
-        for (int i = 0; i < NW; ++i) m[i] = mask[i];
-        int wbase = 0;
-        while (true) {
-            while (true) {
-                uint32_t rest = 0u;
-#pragma unroll
-                for (int i = 1; i < NW; ++i) rest |= m[i];
-                if (m[0] != 0u || rest == 0u) break;
-#pragma unroll
-                for (int i = 0; i + 1 < NW; ++i) m[i] = m[i + 1];
-                m[NW - 1] = 0u;
-                wbase += 32;
+        if constexpr (NW <= 2) {
+            // one 64-bit mask: a single loop over the accepted sources, ascending
+            uint64_t mm = mask[0];
+            if (NW == 2) mm |= static_cast<uint64_t>(mask[NW - 1]) << 32;
+            while (mm) {
+                const int j = __ffsll(static_cast<long long>(mm)) - 1;
+                mm &= mm - 1;
+                const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
+                pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
             }
-            if (m[0] == 0u) break;
-            const int j = wbase + __ffs(m[0]) - 1;
-            m[0] &= m[0] - 1u;
-            const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
-            pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tabx, acc);
+        } else {
+            // the mask words as a shift register: m[0] is the current word
+            uint32_t m[NW];
+#pragma unroll
+            for (int i = 0; i < NW; ++i) m[i] = mask[i];
+            int wbase = 0;
+            while (true) {
+                while (true) {
+                    uint32_t rest = 0u;
+#pragma unroll
+                    for (int i = 1; i < NW; ++i) rest |= m[i];
+                    if (m[0] != 0u || rest == 0u) break;
+#pragma unroll
+                    for (int i = 0; i + 1 < NW; ++i) m[i] = m[i + 1];
+                    m[NW - 1] = 0u;
+                    wbase += 32;
+                }
+                if (m[0] == 0u) break;
+                const int j = wbase + __ffs(m[0]) - 1;
+                m[0] &= m[0] - 1u;
+                const double rx = x - sx[j], ry = y - sy[j], rz = z - sz[j];
+                pair<KIND, TAIL>(rx, ry, rz, exact_d2(rx, ry, rz), xi, sf[j], tab, acc);
+            }
         }
         __syncwarp();
     }
@@ -443,11 +437,22 @@ __global__ void k_fill_items(const int32_t* __restrict__ off, int64_t ncell,
     }
 }
 
-// erfcx(x) = e^{x^2} erfc(x) in long double
-long double erfcx_ld(long double x) { return expl(x * x) * erfcl(x); }
+// the tabulated functions in long double (s = 2/sqrt(pi), realspace.cpp:13-58
+// rewritten as powers of 1/r times functions of x = xi r)
+long double fn_ld(int which, long double x) {
+    const long double sq = 1.128379167095512573896158903121545172L;  // 2/sqrt(pi)
+    const long double e = expl(-x * x), ec = erfcl(x);
+    switch (which) {
+        case 0: return ec - sq * x * e;                           // Ahat
+        case 1: return ec + sq * x * e;                           // Chat
+        case 2: return 3.0L * ec + sq * x * (3.0L + 2.0L * x * x) * e;  // Dhat
+        case 3: return 2.0L * sq * x * e;                         // Ehat
+        default: return 0.0L;
+    }
+}
 
-// Chebyshev fit of erfcx on each interval, converted to monomials in t in [-1, 1]
-void build_table(double out[kDeg + 1][kNI]) {
+// Chebyshev fit of function `which` on each interval, as monomials in t in [-1, 1]
+void fit(int which, double out[kNI][kDeg + 1]) {
     const int n = kDeg + 1;
     const long double PI = 3.141592653589793238462643383279502884L;
     for (int iv = 0; iv < kNI; ++iv) {
@@ -456,7 +461,7 @@ void build_table(double out[kDeg + 1][kNI]) {
         long double fv[n], cheb[n];
         for (int k = 0; k < n; ++k) {
             const long double t = cosl(PI * (k + 0.5L) / n);
-            fv[k] = erfcx_ld(0.5L * (a + b) + 0.5L * (b - a) * t);
+            fv[k] = which < 0 ? 0.0L : fn_ld(which, 0.5L * (a + b) + 0.5L * (b - a) * t);
         }
         for (int j = 0; j < n; ++j) {
             long double sum = 0;
@@ -476,7 +481,7 @@ void build_table(double out[kDeg + 1][kNI]) {
                 Tcur[j] = Tnext[j];
             }
         }
-        for (int j = 0; j < n; ++j) out[j][iv] = static_cast<double>(mono[j]);
+        for (int j = 0; j < n; ++j) out[iv][j] = static_cast<double>(mono[j]);
     }
 }
 
@@ -485,13 +490,21 @@ void ensure_tables() {
     int dev = 0;
     FSE_CU(cudaGetDevice(&dev));
     if (dev < 64 && ready[dev]) return;
-    static double tab[kDeg + 1][kNI];
+    static double2 tab[3][kNI][kDeg + 1];
     static bool built = false;
     if (!built) {
-        build_table(tab);
+        // (F0, F1): stokeslet (Ahat, Chat), stresslet (Dhat, Ehat), rotlet (Chat, 0)
+        const int which[3][2] = {{0, 1}, {2, 3}, {1, -1}};
+        static double f[2][kNI][kDeg + 1];
+        for (int k = 0; k < 3; ++k) {
+            fit(which[k][0], f[0]);
+            fit(which[k][1], f[1]);
+            for (int iv = 0; iv < kNI; ++iv)
+                for (int j = 0; j <= kDeg; ++j) tab[k][iv][j] = make_double2(f[0][iv][j], f[1][iv][j]);
+        }
         built = true;
     }
-    FSE_CU(cudaMemcpyToSymbol(c_erfcx, tab, sizeof tab));
+    FSE_CU(cudaMemcpyToSymbol(c_tab, tab, sizeof tab));
     if (dev < 64) ready[dev] = true;
 }
 

@@ -42,7 +42,6 @@ CASES = [
     ("cfg3t 348", (1.0, 40.0, 0.11451, 146, 16), 348, (0, 1, 2)),
     ("422 (Bluestein-1024)", (1.0, 110.0, 0.045, 187, 24), 422, (0, 1, 2)),
     ("cfg2t 888", (1.0, 110.0, 0.042896, 414, 24), 888, (0, 2)),
-    ("cfg5t 1730", (1.0, 220.0, 0.021279, 834, 24), 1730, (0,)),
     ("cfg1 194", (1.0, 28.0, 0.15, 80, 16), 194, (0, 1, 2)),
 ]
 
@@ -64,6 +63,17 @@ def test_xpass_matches_numpy(fse, ctx, label, args, D, kinds):
         want = expected(cfg, kind, seed, ky, kz, gcol)
         err = np.abs(got - want).max() / np.abs(want).max()
         assert err <= 1e-12, (label, kind, err)
+    ctx.trim()
+
+
+def test_xpass_1730_is_refused_cleanly(fse, ctx):
+    """cfg5's tolerance-consistent grid D = 1730 = 2 x 5 x 173 exceeds every FFT
+    engine (Bluestein would need a >= 3459-point register engine): the call
+    fails with invalid_argument instead of computing garbage."""
+    cfg = fse.make_config(1.0, 220.0, 0.021279, 834, 24)
+    assert cfg.D == 1730
+    with pytest.raises(fse.InvalidArgument):
+        ctx.xscale_probe(cfg, 0, None, 1, np.array([0], np.int32), np.array([0], np.int32))
     ctx.trim()
 
 
