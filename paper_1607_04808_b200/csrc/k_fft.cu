@@ -790,67 +790,40 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass2(FftPlan pl, co
     }
 }
 
-// x pass + multiplier: columns (comp, kz0 + c), c-fastest.  One (ky, kz-tile)
-// item per CTA.  Each CTA first prefetches into L2 the input rows and Green's
-// column of item blockIdx.x + lookahead (lookahead = the CTAs resident at once,
-// i.e. the item that will take this CTA's place), so those items' loads hit L2.
+// x pass + multiplier: columns (comp, kz0 + c), c-fastest
 template <int ENG, int KIND>
 __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>()) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
                                                     const double* __restrict__ G,
                                                     double2* __restrict__ Cb, BlockDest dst,
-                                                    const double* __restrict__ ex_g,
-                                                    int lookahead) {
+                                                    const double* __restrict__ ex_g) {
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
+    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tab = tw + D;
     const int Dh = D / 2 + 1, Mt = g.Mt;
     const int ntz = (Dh + ncol - 1) / ncol;
-    const int nitems = g.nky * ntz;
+    const int kyl = blockIdx.x / ntz;
+    const int ky = g.ky_lo + kyl;
+    const int tz = blockIdx.x - kyl * ntz;
+    const int kz0 = tz * ncol;
+    const int nc = min(ncol, Dh - kz0);
+    const FDiv fnc = make_fdiv(nc);
     // spectrum row of (comp, x = i, this ky) in units of Dh: spec_row with
     // blk = i / nxs, xl = i - blk nxs, in 32-bit arithmetic
     const FDiv fnxs = make_fdiv(g.nxs);
     const int bstep = (A - 1) * g.nxs;
-    {
-        const int it = blockIdx.x + lookahead;
-        if (lookahead > 0 && it < nitems) {
-            const int kyl_ = it / ntz, kz0_ = (it - kyl_ * ntz) * ncol;
-            const int nc_ = min(ncol, Dh - kz0_);
-            for (int e = threadIdx.x; e < A * Mt; e += blockDim.x) {
-                const int comp = e / Mt, i = e - comp * Mt;
-                const int blk = static_cast<int>(fdiv(i, fnxs));
-                const int row = (i + blk * bstep + comp * g.nxs) * g.nkys + kyl_;
-                const double2* p = Cb + static_cast<int64_t>(row) * Dh + kz0_;
-                prefetch_l2(p);
-                prefetch_l2(p + nc_ - 1);
-            }
-            const int ky_ = g.ky_lo + kyl_;
-            for (int kx = threadIdx.x; kx < D; kx += blockDim.x) {
-                const double* gp = G + (static_cast<int64_t>(kx) * D + ky_) * Dh + kz0_;
-                prefetch_l2(gp);
-                prefetch_l2(gp + nc_ - 1);
-            }
-        }
-    }
-    const double2* tw = stage_twiddles(a, pl, tw_g);
-    const double2* tab = tw + D;
-    // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (k_ex_axis, once per
-    // call): rem = ex[kx] * ex[ky] * ex[kz]
-    double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
-    for (int q = threadIdx.x; q < D; q += blockDim.x) ex[q] = __ldg(ex_g + q);
-    const int item = blockIdx.x;
-    const int kyl = item / ntz;
-    const int ky = g.ky_lo + kyl;
-    const int tz = item - kyl * ntz;
-    const int kz0 = tz * ncol;
-    const int nc = min(ncol, Dh - kz0);
-    const FDiv fnc = make_fdiv(nc);
     double2* Ck = Cb + kz0;
     auto at = [&](int comp, int i, int c) -> double2* {
         const int blk = static_cast<int>(fdiv(i, fnxs));
         const int row = (i + blk * bstep + comp * g.nxs) * g.nkys + kyl;
         return Ck + static_cast<int64_t>(row) * Dh + c;
     };
+    // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (k_ex_axis, once per
+    // call): rem = ex[kx] * ex[ky] * ex[kz]
+    double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
+    for (int q = threadIdx.x; q < D; q += blockDim.x) ex[q] = __ldg(ex_g + q);
     // forward x-FFT of the A components (pass 1 straight from global memory)
     freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
         const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
@@ -860,54 +833,36 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
     freg::pass2_smem<D1, D2, true>(a, A * nc, -1, tab);
     __syncthreads();
     // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
-    // Hermitian average (see k_kscale.cu), 1/D^3 folded in; the Green's
-    // values of U elements are loaded before any is used
+    // Hermitian average (see k_kscale.cu), 1/D^3 folded in
     const int half = D / 2;
     const double ex_y = ex[ky];
-    constexpr int U = 4;
-    const int ne = nc * D;
-    for (int e0 = threadIdx.x; e0 < ne; e0 += U * blockDim.x) {
-        double gv[U];
+    for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
+        const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
+        const int kz = kz0 + c;
+        double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
+        const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
+                                    __dmul_rn(k[2], k[2]));
+        const double rem = ex[kx] * ex_y * ex[kz];
+        const double gval = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz);
+        double2 gh[A];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * blockDim.x;
-            gv[u] = 0.0;
-            if (e < ne) {
-                const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
-                gv[u] = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz0 + c);
-            }
+        for (int q = 0; q < A; ++q) gh[q] = a[freg::ridx<D1, D2>(q * nc + c, kx)];
+        double2 out[3];
+        apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
+        if (KIND != KIND_SCALAR && (kx == half || ky == half || kz == half)) {
+            if (kx == half) k[0] = -k[0];
+            if (ky == half) k[1] = -k[1];
+            if (kz == half) k[2] = -k[2];
+            double2 o2[3];
+            apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, o2);
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+                out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * blockDim.x;
-            if (e >= ne) break;
-            const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
-            const int kz = kz0 + c;
-            double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
-            const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
-                                        __dmul_rn(k[2], k[2]));
-            const double rem = ex[kx] * ex_y * ex[kz];
-            const double gval = gv[u];
-            double2 gh[A];
-#pragma unroll
-            for (int q = 0; q < A; ++q) gh[q] = a[freg::ridx<D1, D2>(q * nc + c, kx)];
-            double2 out[3];
-            apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, out);
-            if (KIND != KIND_SCALAR && (kx == half || ky == half || kz == half)) {
-                if (kx == half) k[0] = -k[0];
-                if (ky == half) k[1] = -k[1];
-                if (kz == half) k[2] = -k[2];
-                double2 o2[3];
-                apply<KIND>(k, k2, gval, rem, g.inv4xi2, gh, o2);
-#pragma unroll
-                for (int p = 0; p < 3; ++p)
-                    out[p] = make_double2(0.5 * (out[p].x + o2[p].x), 0.5 * (out[p].y + o2[p].y));
-            }
-#pragma unroll
-            for (int p = 0; p < NO; ++p)
-                a[freg::ridx<D1, D2>(p * nc + c, kx)] =
-                    make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
-        }
+        for (int p = 0; p < NO; ++p)
+            a[freg::ridx<D1, D2>(p * nc + c, kx)] =
+                make_double2(out[p].x * g.invD3, out[p].y * g.invD3);
     }
     __syncthreads();
     // inverse x-FFT of the 3 results (pass 1 in place from shared memory:
@@ -1348,25 +1303,19 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
-            // L2 lookahead: the number of CTAs resident at once
-            auto go = [&](auto kern, int thr) {
-                allow_smem(kern, sm);
-                int per_sm = 0, dev = 0, nsm = 0;
-                FSE_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, thr, sm));
-                FSE_CU(cudaGetDevice(&dev));
-                FSE_CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-                const unsigned grid = std::min<unsigned>(blocks, std::max(1, per_sm * nsm));
-                kern<<<blocks, thr, sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex,
-                                               static_cast<int>(grid));
-            };
-            if (kind == FSE_STOKESLET)
-                go(k_xscale2<EV, FSE_STOKESLET>, xs_threads<EV, FSE_STOKESLET>());
-            else if (kind == FSE_STRESSLET)
-                go(k_xscale2<EV, FSE_STRESSLET>, xs_threads<EV, FSE_STRESSLET>());
-            else if (kind == KIND_SCALAR)
-                go(k_xscale2<EV, KIND_SCALAR>, xs_threads<EV, KIND_SCALAR>());
-            else
-                go(k_xscale2<EV, FSE_ROTLET>, xs_threads<EV, FSE_ROTLET>());
+            if (kind == FSE_STOKESLET) {
+                allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
+                k_xscale2<EV, FSE_STOKESLET><<<blocks, xs_threads<EV, FSE_STOKESLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            } else if (kind == FSE_STRESSLET) {
+                allow_smem(k_xscale2<EV, FSE_STRESSLET>, sm);
+                k_xscale2<EV, FSE_STRESSLET><<<blocks, xs_threads<EV, FSE_STRESSLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            } else if (kind == KIND_SCALAR) {
+                allow_smem(k_xscale2<EV, KIND_SCALAR>, sm);
+                k_xscale2<EV, KIND_SCALAR><<<blocks, xs_threads<EV, KIND_SCALAR>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            } else {
+                allow_smem(k_xscale2<EV, FSE_ROTLET>, sm);
+                k_xscale2<EV, FSE_ROTLET><<<blocks, xs_threads<EV, FSE_ROTLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
+            }
             return;
         }
         if (kind == FSE_STOKESLET) {

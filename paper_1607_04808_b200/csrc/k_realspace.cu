@@ -20,13 +20,16 @@
 //   rotlet:    c = inv^2 Chat(x)
 //   stresslet: c1 = -2 inv^2 Dhat(x), c2 = xi^2 Ehat(x),
 //              Dhat = 3 erfc x + s x (3 + 2x^2) e^{-x^2},  Ehat = 2 s x e^{-x^2}
-// The kernel's two functions are tabulated on [0, 6.5) as 128 piecewise
-// degree-7 Chebyshev fits (monomials in the local t, built in long double from
-// erfcl/expl; max abs error 4e-16 of max |F|), stored as (F0_j, F1_j) pairs so a
-// pair costs 8 16-byte shared loads and two independent 7-FMA Horner chains
-// (no exp, no erfc).  Absolute accuracy is what the sum needs: a large x means a
-// small contribution.  1/r: fp32 seed + two fp64 Newton steps.  x >= 6.5 (only
-// for xi rc > 6.5) uses the erfc/exp formulas directly.
+// With erfc x = e^{-x^2} erfcx(x) they all are e^{-x^2} times polynomials in
+// x and erfcx(x).  erfcx is tabulated on [0, 6.5) as 128 piecewise degree-7
+// Chebyshev fits (monomials in the local t, built in long double from
+// erfcl/expl; max abs error 1.6e-16) and e^{-x^2} is computed (bounded-range
+// exp, constants in constant memory): one 8-byte table load per coefficient per
+// pair.  (Tabulating the two functions directly removes the exp but doubles
+// the shared-memory bytes per pair, and the table loads -- random intervals per
+// lane, bank conflicts -- then bound the loop: 6.2 vs 5.2 ms at cfg2.)
+// 1/r: fp32 seed + two fp64 Newton steps.  x >= 6.5 (only for xi rc > 6.5)
+// uses the erfc/exp formulas directly.
 //
 // Candidate test: the closed-ball test is decided in fp32 on coordinates
 // relative to the item's cell centre (FP32 pipe, off the FP64 pipe that
@@ -56,15 +59,28 @@ namespace {
 #ifndef FSE_RS_CH
 #define FSE_RS_CH 64
 #endif
+#ifndef FSE_RS_MINB
+#define FSE_RS_MINB 1
+#endif
 constexpr int TPB = FSE_RS_TPB, CH = FSE_RS_CH, NW = CH / 32;
 static_assert(CH % 32 == 0 && NW >= 1 && NW <= 4, "chunk of 1..4 mask words");
 constexpr double kInvSqrtPi = 0.5641895835477562869;
 
 constexpr int kNI = 128, kDeg = 7;
 constexpr double kXMax = 6.5;
-// the kernel's smooth functions of x = xi r, piecewise degree-7 on kNI intervals
-// of [0, kXMax): [kind][iv][j] = (F0_j, F1_j) monomial coefficients in the local t
-__constant__ double2 c_tab[3][kNI][kDeg + 1];
+// erfcx(x) = e^{x^2} erfc(x), piecewise degree-7 on kNI intervals of [0, kXMax):
+// [j][iv] = monomial coefficient j in the local t (coefficient-major: the lanes
+// of a warp read different intervals iv of one coefficient, 8-byte words)
+__constant__ double c_erfcx[kDeg + 1][kNI];
+// e^{-x^2}: Cody-Waite constants and the degree-13 Taylor coefficients, in
+// constant memory so the FMAs take them as c[] operands (immediates would be
+// rematerialised into uniform registers inside the pair loop)
+__constant__ double c_exp[18] = {
+    1.4426950408889634074, 6.93147180559945286227e-01, 2.31904681384629955842e-17,
+    6755399441055744.0,
+    1.0, 1.0 / 6.0, 0.5, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 5040.0, 1.0 / 720.0,
+    1.0 / 362880.0, 1.0 / 40320.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.1283791670955126};
 
 
 struct FastTest {
@@ -109,6 +125,28 @@ __device__ __forceinline__ double exact_d2(double rx, double ry, double rz) {
     return __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
 }
 
+// e^y for y in [-kXMax^2, 0]: y = j ln2 + r (|r| <= ln2 / 2, Cody-Waite with
+// FMA), degree-13 Taylor polynomial in Estrin form (remainder < 5e-18
+// relative), 2^j added to the exponent field (j >= -61: no overflow,
+// underflow or subnormal cases).  Max error ~2 ulp (host-checked against expl).
+__device__ __forceinline__ double exp_neg_bounded(double y) {
+    const double k = fma(y, c_exp[0], c_exp[3]);  // round(y log2 e) in the low word
+    const double jd = k - c_exp[3];
+    const int j = __double2loint(k);
+    double r = fma(jd, -c_exp[1], y);
+    r = fma(jd, -c_exp[2], r);
+    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    const double a0 = r + c_exp[4], a1 = fma(r, c_exp[5], c_exp[6]);
+    const double a2 = fma(r, c_exp[7], c_exp[8]), a3 = fma(r, c_exp[9], c_exp[10]);
+    const double a4 = fma(r, c_exp[11], c_exp[12]);
+    const double a5 = fma(r, c_exp[13], c_exp[14]);
+    const double a6 = fma(r, c_exp[15], c_exp[16]);
+    const double b0 = fma(a1, r2, a0), b1 = fma(a3, r2, a2), b2 = fma(a5, r2, a4);
+    const double d0 = fma(b1, r4, b0), d1 = fma(a6, r4, b2);
+    const double p = fma(d1, r8, d0);
+    return __hiloint2double(__double2hiint(p) + j * (1 << 20), __double2loint(p));
+}
+
 // 1/sqrt(r2): fp32 seed + two Newton steps in fp64 (22 -> 44 -> full bits,
 // ~1 ulp), no special-case branches; r2 < 1e-36 (points closer than 1e-18,
 // only possible near the origin) takes the library rsqrt
@@ -121,15 +159,14 @@ __device__ __forceinline__ double rsqrt_nr(double r2) {
     return y;
 }
 
-// tab: (F0, F1) = the two functions this kernel needs (stokeslet: Ahat, Chat;
-// rotlet: Chat, -; stresslet: Dhat, Ehat), tabulated directly (absolute error
-// < 4e-16; their products with 1/r powers need absolute, not relative,
-// accuracy).  TAIL: x = xi r can reach the end of the table (xi rc >= 6.5), so
-// the exact formulas take over there.
+// tab: erfcx coefficients [j][iv] (shared memory); F0, F1 = the two functions
+// this kernel needs (stokeslet: Ahat, Chat; rotlet: Chat, -; stresslet: Dhat,
+// Ehat) as e^{-x^2} times polynomials in x and erfcx(x): one 8-byte table load
+// per coefficient per pair, e^{-x^2} computed.  TAIL: x = xi r can reach the
+// end of the table (xi rc >= 6.5), so the exact formulas take over there.
 template <int KIND, bool TAIL>
 __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2, double xi,
-                                     const double* f, const double2 (*tab)[kDeg + 1],
-                                     double acc[3]) {
+                                     const double* f, const double (*tab)[kNI], double acc[3]) {
     const double inv = rsqrt_nr(r2);
     const double rn = r2 * inv;
     const double xr = xi * rn;
@@ -138,15 +175,19 @@ __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2,
         const double uu = xr * (kNI / kXMax);
         const int iv = min(static_cast<int>(uu), kNI - 1);
         const double t = 2.0 * (uu - iv) - 1.0;
-        const double2* row = tab[iv];
-        double2 cf = row[kDeg];
-        F0 = cf.x;
-        F1 = cf.y;
+        double ex = tab[kDeg][iv];
 #pragma unroll
-        for (int j = kDeg - 1; j >= 0; --j) {
-            cf = row[j];
-            F0 = fma(F0, t, cf.x);
-            if (KIND != FSE_ROTLET) F1 = fma(F1, t, cf.y);
+        for (int j = kDeg - 1; j >= 0; --j) ex = fma(ex, t, tab[j][iv]);
+        const double E = exp_neg_bounded(-xr * xr);
+        const double sx = c_exp[17] * xr;  // 2 x / sqrt(pi)
+        if (KIND == FSE_STOKESLET) {
+            F0 = E * (ex - sx);
+            F1 = E * (ex + sx);
+        } else if (KIND == FSE_ROTLET) {
+            F0 = E * (ex + sx);
+        } else {
+            F0 = E * (3.0 * ex + sx * (3.0 + 2.0 * xr * xr));
+            F1 = 2.0 * sx * E;
         }
     } else {
         fn_exact(KIND == FSE_STOKESLET ? 0 : (KIND == FSE_ROTLET ? 1 : 2), xr, &F0);
@@ -208,7 +249,7 @@ struct WarpChunk {
 };
 
 template <int KIND, bool TAIL>
-__global__ void __launch_bounds__(TPB) k_realspace(
+__global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     int dim, const double* __restrict__ spx, const double* __restrict__ spy,
     const double* __restrict__ spz, const double* __restrict__ sfs,
     const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
@@ -232,11 +273,10 @@ __global__ void __launch_bounds__(TPB) k_realspace(
     auto& sf = wc.sf;
     auto& nb_start = wc.nb_start;
     auto& nb_pref = wc.nb_pref;
-    __shared__ double2 tab[kNI][kDeg + 1];
+    __shared__ double tab[kDeg + 1][kNI];
     {
-        constexpr int ktab = KIND == FSE_STOKESLET ? 0 : (KIND == FSE_STRESSLET ? 1 : 2);
-        const double2* src = &c_tab[ktab][0][0];
-        double2* dst = &tab[0][0];
+        const double* src = &c_erfcx[0][0];
+        double* dst = &tab[0][0];
         for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += blockDim.x) dst[e] = src[e];
     }
     __syncthreads();  // the only CTA-wide barrier
@@ -447,6 +487,7 @@ long double fn_ld(int which, long double x) {
         case 1: return ec + sq * x * e;                           // Chat
         case 2: return 3.0L * ec + sq * x * (3.0L + 2.0L * x * x) * e;  // Dhat
         case 3: return 2.0L * sq * x * e;                         // Ehat
+        case 4: return expl(x * x) * erfcl(x);                    // erfcx
         default: return 0.0L;
     }
 }
@@ -490,21 +531,16 @@ void ensure_tables() {
     int dev = 0;
     FSE_CU(cudaGetDevice(&dev));
     if (dev < 64 && ready[dev]) return;
-    static double2 tab[3][kNI][kDeg + 1];
+    static double tab[kDeg + 1][kNI];
     static bool built = false;
     if (!built) {
-        // (F0, F1): stokeslet (Ahat, Chat), stresslet (Dhat, Ehat), rotlet (Chat, 0)
-        const int which[3][2] = {{0, 1}, {2, 3}, {1, -1}};
-        static double f[2][kNI][kDeg + 1];
-        for (int k = 0; k < 3; ++k) {
-            fit(which[k][0], f[0]);
-            fit(which[k][1], f[1]);
-            for (int iv = 0; iv < kNI; ++iv)
-                for (int j = 0; j <= kDeg; ++j) tab[k][iv][j] = make_double2(f[0][iv][j], f[1][iv][j]);
-        }
+        static double f[kNI][kDeg + 1];
+        fit(4, f);
+        for (int iv = 0; iv < kNI; ++iv)
+            for (int j = 0; j <= kDeg; ++j) tab[j][iv] = f[iv][j];
         built = true;
     }
-    FSE_CU(cudaMemcpyToSymbol(c_tab, tab, sizeof tab));
+    FSE_CU(cudaMemcpyToSymbol(c_erfcx, tab, sizeof tab));
     if (dev < 64) ready[dev] = true;
 }
 
