@@ -60,7 +60,7 @@ namespace {
 #define FSE_RS_CH 64
 #endif
 #ifndef FSE_RS_MINB
-#define FSE_RS_MINB 1
+#define FSE_RS_MINB 4
 #endif
 constexpr int TPB = FSE_RS_TPB, CH = FSE_RS_CH, NW = CH / 32;
 static_assert(CH % 32 == 0 && NW >= 1 && NW <= 4, "chunk of 1..4 mask words");
