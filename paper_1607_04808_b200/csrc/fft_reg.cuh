@@ -193,13 +193,19 @@ __device__ __forceinline__ void rfft(double2* v, int sgn, const double2* tab) {
     }
 }
 
-// Shared-memory column layout of the register engines: column stride
-// D + D1 + 1 (odd) and one pad element after every D2 elements, so the
-// pass-2 loads (stride D2 across lanes) and the columns of the load/store
-// phases (stride one column across lanes) fall on distinct bank groups.
+// Shared-memory column layout of the register engines: one pad element after
+// every D2 elements and a column stride >= D + D1 + 1 that is 3 mod 8 (in
+// 16-byte elements; 8 of them fill the 32 banks).  Lanes that walk columns
+// (stride 3 mod 8) and elements (stride 1) then hit distinct bank groups in
+// the passes and in the x-pass multiplier, whose lanes walk (kz column, kx)
+// three columns at a time (a stride of 1 mod 8 put three lanes on one bank
+// group there: 3x shared-memory wavefronts).
+__host__ __device__ constexpr int col_stride(int D1, int D2) {
+    return D1 * D2 + D1 + 1 + ((3 - (D1 * D2 + D1 + 1) % 8) + 8) % 8;
+}
 template <int D1, int D2>
 __device__ __forceinline__ int ridx(int c, int n) {
-    return c * (D1 * D2 + D1 + 1) + n + n / D2;
+    return c * col_stride(D1, D2) + n + n / D2;
 }
 
 // Column FFT of length D1*D2 on `ncol` columns stored at buf[ridx(c, n)].

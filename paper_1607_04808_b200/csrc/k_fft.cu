@@ -1114,7 +1114,7 @@ namespace {
 
 size_t col_elems(const HostFftPlan& h, int cols) {
     if (h.eng > 0)  // freg::ridx layout (Bluestein: columns of the Mb-point engine)
-        return static_cast<size_t>(cols) * (h.D1 * h.D2 + h.D1 + 1) + 8;
+        return static_cast<size_t>(cols) * freg::col_stride(h.D1, h.D2) + 8;
     return static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
 }
 
