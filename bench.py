@@ -191,9 +191,11 @@ def peaks():
     return p
 
 
-# FP64 flops of one accepted real-space pair: r^2 (5),
-# rsqrt + x (6), two 8-term Horner tables (28), kernel combine + accumulate
-PAIR_FLOPS = {0: 60.0, 1: 90.0, 2: 50.0}
+# FP64 flops of one accepted real-space pair, calibrated from ncu's SASS
+# instruction counts of k_realspace (2 DFMA + DMUL + DADD thread instructions per
+# accepted pair; tools/pair_flops.py, profiles/r02/realspace_pair_flops.txt):
+# stokeslet cfg2 101.8, stresslet cfg3 163.0, rotlet cfg4 96.8
+PAIR_FLOPS = {0: 102.0, 1: 163.0, 2: 97.0}
 
 
 def stage_models(w, cfg, n, nt, rs_pairs=None):

@@ -444,7 +444,8 @@ void run_nccl(const NcclComm& nc, cudaStream_t s, int self, const Step& st) {
     for (const Msg& m : st.recvs)
         if (m.peer != self && m.bytes) FSE_NCCL(ncclRecv(m.ptr, m.bytes, ncclChar, m.peer, nc.comm, s));
     FSE_NCCL(ncclGroupEnd());
-    FSE_CU(cudaStreamSynchronize(s));
+    // stream-ordered: the next step's kernels on s queue behind the transfers;
+    // the host only waits where it needs received counts (pack)
 }
 
 // virtual ranks of one process on one device: copy every send to the matching

@@ -2,16 +2,15 @@
 // the screened kernels of realspace.cpp:13-58.
 //
 // Work item = (target cell, up to 32 of its targets) = one warp, one lane
-// per target; a CTA runs 4 independent items (no CTA barrier in the loop).
-// The 27 neighbour buckets (lexicographic (di,dj,dk), sources in bucket order
-// -- the reference's summation order) are concatenated virtually and
-// streamed through the warp's shared memory in chunks of 128 sources.  Each
-// lane first tests its target against the whole chunk (exact closed-ball
-// test 0 < d2 <= rc2 with d2 = (x*x + y*y) + z*z rounded like the
-// reference) into a 128-bit mask, then evaluates only the accepted pairs in
-// ascending order.  This keeps the pair evaluation off the
-// ~85% of candidates that fail the test, instead of predicating the whole
-// warp on every candidate.
+// per target; a CTA runs 8 independent items (no CTA barrier in the loop).
+// The 27 neighbour buckets (lexicographic (di,dj,dk)) are concatenated
+// virtually and sampled with a coprime stride (so every chunk mixes all
+// buckets and the lanes accept similar numbers of pairs), then streamed
+// through the warp's shared memory in chunks of 64 sources.  Each lane first
+// tests its target against the whole chunk (closed ball 0 < d2 <= rc2, d2 =
+// (x*x + y*y) + z*z rounded like the reference, realspace.cpp:140) into a
+// 64-bit mask, then evaluates only the accepted pairs.  The accepted set is
+// the reference's; the summation order differs (fixed, deterministic).
 //
 // Pair math: with x = xi r and inv = 1/r, every screened kernel is a power
 // of inv times smooth functions of x alone (s = 2/sqrt(pi)):
