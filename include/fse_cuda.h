@@ -179,6 +179,23 @@ fse_status fse_cuda_dist_total_sum(fse_dist* d, const fse_config* cfg, int kind,
                                    const double* d_pos, const double* d_str, int64_t n_own,
                                    int64_t n_total, const double* d_tgt, int64_t nt_own, int tas,
                                    const fse_green* green, double* d_u);
+/* one process, several GPUs: a multi-device context (one fse_cuda_ctx per device and
+ * the NCCL communicators of ncclCommInitAll) and fse::total_sum over it with HOST
+ * buffers: the points are partitioned by owner, every device runs its rank of the
+ * partitioned evaluation in its own host thread, u comes back in caller order.  The
+ * Green's table: green_full (the reference layout, (2 Mtilde)^3 host doubles, e.g.
+ * fse::MollifiedGreen::fourier) uploaded to every device, or NULL to precompute it on
+ * every device; cached by kind, geometry and table pointer.
+ * tas: -1 detect by value (ewald.cpp:405-407), 0 no, 1 yes.  tm (optional) accumulates
+ * only `total` (the call's wall clock, transfers included). */
+typedef struct fse_multi fse_multi;
+fse_status fse_cuda_multi_create(const int* devices, int ndev, fse_multi** out);
+void fse_cuda_multi_destroy(fse_multi* m);
+const char* fse_cuda_multi_last_error(const fse_multi* m);
+fse_status fse_cuda_multi_total_sum(fse_multi* m, const fse_config* cfg, int kind,
+                                    const double* pos, const double* str, int64_t n,
+                                    double box_side, const double* tgt, int64_t nt, int tas,
+                                    const double* green_full, double* u, fse_timings* tm);
 /* owner rank of each of n host points (x = pos[3 i]) for nranks slabs (host, no GPU) */
 fse_status fse_dist_owner(const fse_config* cfg, int nranks, const double* pos, int64_t n,
                           int32_t* owner);

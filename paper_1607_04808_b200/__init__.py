@@ -16,6 +16,6 @@ from .api import (CellList, Context, DomainError, EwaldConfig, FseError, FseRunt
                   strength_arity, strength_quadratic_sum, total_sum, ErrorBudget,
                   error_budget, fourier_error_estimate, real_error_estimate,
                   reference_velocity_rms, select_parameters, freespace_solve,
-                  nccl_unique_id, dist_owner, dist_masks)
+                  nccl_unique_id, dist_owner, dist_masks, MultiContext)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

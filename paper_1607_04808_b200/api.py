@@ -279,6 +279,13 @@ def _load():
         lib.fse_cuda_dist_virtual_total_sum.argtypes = [vp, C.c_int, C.POINTER(EwaldConfig),
                                                         C.c_int, vp, vp, i64, vp, i64, C.c_int,
                                                         vp, vp]
+        lib.fse_cuda_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+        lib.fse_cuda_multi_destroy.argtypes = [vp]
+        lib.fse_cuda_multi_last_error.restype = C.c_char_p
+        lib.fse_cuda_multi_last_error.argtypes = [vp]
+        lib.fse_cuda_multi_total_sum.argtypes = [vp, C.POINTER(EwaldConfig), C.c_int, _dp, _dp, i64,
+                                                 C.c_double, _dp, i64, C.c_int, vp, _dp,
+                                                 C.POINTER(StageTimings)]
         lib.fse_dist_owner.argtypes = [C.POINTER(EwaldConfig), C.c_int, _dp, i64,
                                        C.POINTER(C.c_int32)]
         lib.fse_dist_masks.argtypes = [C.POINTER(EwaldConfig), C.c_int, _dp, i64, C.c_int,
@@ -830,6 +837,47 @@ def generate_system(kind, n, L, seed) -> SourceSystem:
 
 
 WL_UNIFORM, WL_SPHERE, WL_CLUSTERED, WL_UNIFORM_TARGETS = 1, 3, 4, 5
+
+
+class MultiContext:
+    """Several GPUs in one process (fse_cuda_multi_*): total_sum with host buffers,
+    partitioned over the devices with NCCL inside the library."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        st = _load().fse_cuda_multi_create(devs, len(devices), C.byref(h))
+        if st != 0:
+            _raise(st, "fse_cuda_multi_create failed")
+        self._h = h
+
+    def close(self):
+        if self._h:
+            _load().fse_cuda_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def total_sum(self, system: SourceSystem, kind, cfg, targets, green_full=None,
+                  targets_are_sources: int = -1):
+        t = _f64(targets, (-1, 3))
+        u = np.empty((t.shape[0], 3))
+        gp = None
+        if green_full is not None:
+            green_full = _f64(green_full)
+            gp = green_full.ctypes.data_as(C.c_void_p)
+        st = _load().fse_cuda_multi_total_sum(self._h, C.byref(cfg), int(kind),
+                                              _p(system.positions), _p(system.strengths),
+                                              system.size(), float(system.box_side), _p(t),
+                                              t.shape[0], int(targets_are_sources), gp, _p(u),
+                                              None)
+        if st != 0:
+            _raise(st, _load().fse_cuda_multi_last_error(self._h).decode())
+        return u
 
 
 def nccl_unique_id() -> bytes:

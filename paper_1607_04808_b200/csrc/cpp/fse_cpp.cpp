@@ -96,6 +96,28 @@ fse_green* device_green(const MollifiedGreen& g) {
 
 const fse_config* cfg_of(const EwaldConfig& c) { return reinterpret_cast<const fse_config*>(&c); }
 
+// $FSE_CUDA_DEVICES = "0,1,2,3": total_sum runs partitioned over those GPUs
+// (fse_cuda_multi_*, one process, NCCL inside the library); unset: one GPU
+fse_multi* multi() {
+    static std::once_flag once;
+    static fse_multi* m = nullptr;
+    std::call_once(once, [] {
+        const char* env = std::getenv("FSE_CUDA_DEVICES");
+        if (!env || !*env) return;
+        std::vector<int> devs;
+        for (const char* p = env; *p;) {
+            char* end = nullptr;
+            const long v = std::strtol(p, &end, 10);
+            if (end == p) break;
+            devs.push_back(static_cast<int>(v));
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (devs.empty() || fse_cuda_multi_create(devs.data(), static_cast<int>(devs.size()), &m) != FSE_OK)
+            throw std::runtime_error("fse: FSE_CUDA_DEVICES multi-GPU context creation failed");
+    });
+    return m;
+}
+
 }  // namespace detail
 
 using detail::check;
@@ -370,6 +392,17 @@ Velocities total_sum(const SourceSystem& system, KernelKind kind, const EwaldCon
                      StageTimings* timings) {
     const auto str = detail::pack_strengths(system, kind);
     Velocities u(targets.size());
+    if (fse_multi* m = detail::multi()) {
+        // the partitioned multi-GPU evaluation (timings: only `total`, the call's wall clock)
+        const fse_status st = fse_cuda_multi_total_sum(
+            m, detail::cfg_of(cfg), static_cast<int>(kind), detail::pts(system.positions),
+            str.data(), static_cast<int64_t>(system.size()), system.box_side,
+            detail::pts(targets), static_cast<int64_t>(targets.size()), -1,
+            green.fourier.empty() ? nullptr : green.fourier.data(),
+            reinterpret_cast<double*>(u.data()), reinterpret_cast<fse_timings*>(timings));
+        if (st != FSE_OK) detail::raise(st, fse_cuda_multi_last_error(m));
+        return u;
+    }
     check(fse_cuda_total_sum(ctx(), detail::cfg_of(cfg), static_cast<int>(kind),
                              detail::pts(system.positions), str.data(),
                              static_cast<int64_t>(system.size()), system.box_side,

@@ -428,6 +428,40 @@ bool detect_tas_dev(fse_cuda_ctx* c, const double* a, const double* b, int64_t n
     return c->h_flags[2] == 0;
 }
 
+// quadrature (ewald.cpp:349-391) of nt prepared targets from the real grid X
+// into u (caller order via tg.perm): the TMA/DMMA slab gather (P <= 25), else
+// the warp-group gather; EV_TPREP marks the end of the target preparation
+void quadrature(fse_cuda_ctx* c, const GridParams& g, const Sorted& tg, int64_t nt,
+                const double* X, double h3, double* u, bool record_events) {
+    Launch L = L0(c);
+    if (gather_slab_enabled(g)) {
+        const int64_t nhalf = g.nkeys / 4;  // (coarse tile, z-half) pairs
+        int32_t* scnt = buf<int32_t>(c, "scnt", nhalf + 1);
+        int32_t* soff = buf<int32_t>(c, "soff", nhalf + 1);
+        launch_slab_counts(L, g, tg.tstart, nhalf, scnt);
+        exclusive_scan(c, c->s0, "s0", scnt, soff, nhalf + 1);
+        const int64_t max_items = std::min<int64_t>(nhalf, nt) + (nt + 31) / 32;
+        int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
+        launch_slab_fill(L, soff, nhalf, sitems);
+        if (record_events) FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
+        launch_gather_slab(L, g, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff + nhalf, X,
+                           tg.perm, h3, u);
+    } else {
+        if (g.nx < g.Mt) invalid("slab: the decomposition needs the tensor-core quadrature (P <= 25)");
+        int32_t* gcnt = buf<int32_t>(c, "gcnt", g.nkeys + 1);
+        int32_t* goff = buf<int32_t>(c, "goff", g.nkeys + 1);
+        launch_group_counts(L, tg.tstart, g.nkeys, gcnt);
+        exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
+        // upper bound on groups: one partial group per non-empty key + nt/8
+        const int gk = gather_group_size();
+        const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + gk - 1) / gk;
+        int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
+        launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
+        if (record_events) FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
+        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, u);
+    }
+}
+
 // The whole hot path on device pointers.  u (caller order) = fourier (if
 // want_f) + real (if want_r) + self (stokeslet, targets == sources, full sum).
 void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_pos,
@@ -496,31 +530,7 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         Sorted tg = tas ? src : prep_points(c, g, "ft_", d_tgt, nullptr, 0, nt, 1, qtab);
         uF = want_r ? buf<double>(c, "uF", 3 * nt) : d_u;
         const double h3 = g.h * g.h * g.h;  // prefac is folded into the x weights
-        if (gather_slab_enabled(g)) {
-            const int64_t nhalf = g.nkeys / 4;  // (coarse tile, z-half) pairs
-            int32_t* scnt = buf<int32_t>(c, "scnt", nhalf + 1);
-            int32_t* soff = buf<int32_t>(c, "soff", nhalf + 1);
-            launch_slab_counts(L, g, tg.tstart, nhalf, scnt);
-            exclusive_scan(c, c->s0, "s0", scnt, soff, nhalf + 1);
-            const int64_t max_items = std::min<int64_t>(nhalf, nt) + (nt + 31) / 32;
-            int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
-            launch_slab_fill(L, soff, nhalf, sitems);
-            FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
-            launch_gather_slab(L, g, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff + nhalf, X,
-                               tg.perm, h3, uF);
-        } else {
-        int32_t* gcnt = buf<int32_t>(c, "gcnt", g.nkeys + 1);
-        int32_t* goff = buf<int32_t>(c, "goff", g.nkeys + 1);
-        launch_group_counts(L, tg.tstart, g.nkeys, gcnt);
-        exclusive_scan(c, c->s0, "s0", gcnt, goff, g.nkeys + 1);
-        // upper bound on groups: one partial group per non-empty key + nt/8
-        const int gk = gather_group_size();
-        const int64_t max_groups = std::min<int64_t>(g.nkeys, nt) + (nt + gk - 1) / gk;
-        int32_t* gkey = buf<int32_t>(c, "gkey", max_groups);
-        launch_fill_groups(L, tg.tstart, goff, g.nkeys, gkey);
-        FSE_CU(cudaEventRecord(c->ev[EV_TPREP], c->s0));
-        launch_gather(L, g, tg.i0s, tg.w, tg.tstart, gkey, goff, max_groups, X, tg.perm, h3, uF);
-        }
+        quadrature(c, g, tg, nt, X, h3, uF, true);
         FSE_CU(cudaEventRecord(c->ev[EV_QUAD], c->s0));
         if (want_r && serial) {
             FSE_CU(cudaStreamWaitEvent(c->s1, c->ev[EV_QUAD], 0));

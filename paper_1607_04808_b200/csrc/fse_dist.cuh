@@ -363,17 +363,8 @@ struct Rank {
                               reinterpret_cast<double2*>(spec_a.ptr<double>()), Bs, W);
         if (nt_loc > 0) {
             Sorted tg = prep_points(c, gg, "ft_", ltgt.ptr<double>(), nullptr, 0, nt_loc, 1, qtab);
-            const int64_t nhalf = gg.nkeys / 4;
-            int32_t* scnt_ = buf<int32_t>(c, "scnt", nhalf + 1);
-            int32_t* soff_ = buf<int32_t>(c, "soff", nhalf + 1);
-            launch_slab_counts(L, gg, tg.tstart, nhalf, scnt_);
-            exclusive_scan(c, c->s0, "s0", scnt_, soff_, nhalf + 1);
-            const int64_t max_items = std::min<int64_t>(nhalf, nt_loc) + (nt_loc + 31) / 32;
-            int32_t* sitems = buf<int32_t>(c, "sitems", 2 * static_cast<size_t>(max_items));
-            launch_slab_fill(L, soff_, nhalf, sitems);
-            FSE_CU(cudaMemsetAsync(ul, 0, sizeof(double) * 3 * nt_loc, c->s0));
-            launch_gather_slab(L, gg, tg.i0s, tg.w, tg.tstart, sitems, max_items, soff_ + nhalf, W,
-                               tg.perm, gg.h * gg.h * gg.h, ul);
+            if (G > 1) FSE_CU(cudaMemsetAsync(ul, 0, sizeof(double) * 3 * nt_loc, c->s0));
+            quadrature(c, gg, tg, nt_loc, W, gg.h * gg.h * gg.h, ul, false);
         }
         FSE_CU(cudaStreamWaitEvent(c->s0, c->ev[EV_JOIN], 0));
         raise_flags(c);  // synchronises s0 (partials complete before they are sent)
@@ -479,9 +470,32 @@ struct fse_dist {
     std::unique_ptr<fsecu::dist::Rank> rank;
 };
 
+struct fse_multi {
+    std::vector<int> devices;
+    std::vector<fse_cuda_ctx*> ctx;
+    std::vector<fsecu::dist::NcclComm> nc;
+    std::vector<std::unique_ptr<fsecu::dist::Rank>> ranks;
+    std::vector<fse_green*> greens;
+    int green_kind = -1, green_Mt = 0;
+    double green_Lt = 0, green_sf = 0;
+    const double* green_src = nullptr;  // caller's table the device copies came from
+    std::vector<std::unique_ptr<fsecu::dist::GBuf>> dp, ds, dt, du;
+    std::string err;
+    std::mutex mu;
+};
+
 namespace {
 
 using namespace fsecu::dist;
+
+void run_rank_steps(Rank& R, const NcclComm& nc, cudaStream_t s, const fse_green* green) {
+    const int me = nc.rank;
+    run_nccl(nc, s, me, R.classify());
+    run_nccl(nc, s, me, R.pack());
+    run_nccl(nc, s, me, R.forward());
+    run_nccl(nc, s, me, R.scale(green));
+    run_nccl(nc, s, me, R.inverse());
+}
 
 // the steps of one evaluation on one NCCL rank
 void dist_total_sum(fse_dist* D, const fse_config* cfg, int kind, const double* d_pos,
@@ -494,12 +508,7 @@ void dist_total_sum(fse_dist* D, const fse_config* cfg, int kind, const double* 
     fse_cuda_ctx* c = D->ctx;
     Rank& R = *D->rank;
     R.setup(cfg, kind, d_pos, d_str, n_own, n_total, d_tgt, nt_own, tas != 0);
-    const int me = D->nc.rank;
-    run_nccl(D->nc, c->s0, me, R.classify());
-    run_nccl(D->nc, c->s0, me, R.pack());
-    run_nccl(D->nc, c->s0, me, R.forward());
-    run_nccl(D->nc, c->s0, me, R.scale(green));
-    run_nccl(D->nc, c->s0, me, R.inverse());
+    run_rank_steps(R, D->nc, c->s0, green);
     R.finish(d_u);
 }
 
@@ -617,6 +626,190 @@ fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fs
         }
         h2d(c, d_u, hu.data(), sizeof(double) * hu.size());
     });
+}
+
+// ---- one process, several GPUs (a multi-device context holding the
+// NCCL communicators of ncclCommInitAll): host buffers in and out, like
+// fse::total_sum; one host thread per device runs that device's rank.
+fse_status fse_cuda_multi_create(const int* devices, int ndev, fse_multi** out) {
+    if (!out || !devices || ndev < 1 || ndev > kMaxSlabs) return FSE_EINVAL;
+    *out = nullptr;
+    auto M = std::make_unique<fse_multi>();
+    M->devices.assign(devices, devices + ndev);
+    for (int r = 0; r < ndev; ++r) {
+        fse_cuda_ctx* c = nullptr;
+        const fse_status st = fse_cuda_create(devices[r], &c);
+        if (st != FSE_OK) {
+            for (fse_cuda_ctx* x : M->ctx) fse_cuda_destroy(x);
+            return st;
+        }
+        M->ctx.push_back(c);
+    }
+    std::vector<ncclComm_t> comms(ndev);
+    if (ncclCommInitAll(comms.data(), ndev, devices) != ncclSuccess) {
+        for (fse_cuda_ctx* x : M->ctx) fse_cuda_destroy(x);
+        return FSE_ENCCL;
+    }
+    M->nc.resize(ndev);
+    for (int r = 0; r < ndev; ++r) {
+        M->nc[r].comm = comms[r];
+        M->nc[r].rank = r;
+        M->nc[r].nranks = ndev;
+        M->ranks.emplace_back(new Rank(M->ctx[r], r, ndev));
+        M->dp.emplace_back(new GBuf);
+        M->ds.emplace_back(new GBuf);
+        M->dt.emplace_back(new GBuf);
+        M->du.emplace_back(new GBuf);
+    }
+    M->greens.assign(ndev, nullptr);
+    *out = M.release();
+    return FSE_OK;
+}
+
+void fse_cuda_multi_destroy(fse_multi* M) {
+    if (!M) return;
+    for (size_t r = 0; r < M->ctx.size(); ++r) {
+        cudaSetDevice(M->devices[r]);
+        M->ranks[r].reset();
+        M->dp[r].reset();
+        M->ds[r].reset();
+        M->dt[r].reset();
+        M->du[r].reset();
+        if (M->greens[r]) fse_cuda_green_free(M->greens[r]);
+    }
+    M->nc.clear();  // ncclCommDestroy
+    for (fse_cuda_ctx* c : M->ctx) fse_cuda_destroy(c);
+    delete M;
+}
+
+const char* fse_cuda_multi_last_error(const fse_multi* M) { return M ? M->err.c_str() : ""; }
+
+fse_status fse_cuda_multi_total_sum(fse_multi* M, const fse_config* cfg, int kind,
+                                    const double* pos, const double* str, int64_t n,
+                                    double box_side, const double* tgt, int64_t nt, int tas,
+                                    const double* green_full, double* u, fse_timings* tm) {
+    if (!M) return FSE_EINVAL;
+    std::lock_guard<std::mutex> lk(M->mu);
+    M->err.clear();
+    const auto t_start = std::chrono::steady_clock::now();
+    try {
+        check_kind(kind);
+        check_cfg(cfg);
+        if (n < 1 || nt < 0 || !pos || !str || !u || (nt > 0 && !tgt)) invalid("null pointer");
+        if (std::abs(box_side - cfg->L) > 1e-12 * cfg->L)
+            invalid("spread: config box does not match system");
+        const int G = static_cast<int>(M->ctx.size()), a = arity_of(kind);
+        const bool same = tas < 0 ? (n == nt && host_equal(pos, tgt, n)) : tas != 0;
+        if (same) tgt = pos, nt = n;
+        const GridParams g0 = slab_params(cfg, 0, G);
+        const GridParams g1 = make_grid_params(*cfg);
+        const Geom q{G, g0.nxs, g1.Mt, g1.P, g1.origin, g1.h, cfg->rc / g1.h};
+        // host-side checks of the device flags (a rank failing inside the NCCL
+        // steps would leave its peers waiting): supports inside the grid
+        // (ewald.cpp:87-91) and targets inside the box (ewald.cpp:299-302)
+        auto check_points = [&](const double* p, int64_t m, bool box) {
+            for (int64_t i = 0; i < 3 * m; ++i) {
+                const double x = p[i];
+                const int f = fsedist::support_first(fsedist::plane_coord(x, q), q);
+                if (!(x == x) || f < 0 || f + g1.P > g1.Mt)
+                    invalid("spread/quadrature: point support exceeds grid");
+                if (box && !(x >= 0.0 && x <= cfg->L)) invalid("fourier_sum: target outside [0,L]^3");
+            }
+        };
+        check_points(pos, n, false);
+        if (!same) check_points(tgt, nt, true);
+        // partition by owner
+        std::vector<std::vector<int64_t>> own_s(G), own_t(G);
+        for (int64_t i = 0; i < n; ++i) own_s[fsedist::owner_of(pos[3 * i], q)].push_back(i);
+        if (!same)
+            for (int64_t i = 0; i < nt; ++i) own_t[fsedist::owner_of(tgt[3 * i], q)].push_back(i);
+        // Green's table on every device: the caller's (D^3 reference layout) or
+        // the GPU precompute; cached by kind, geometry and source table
+        const int gk = kind == FSE_ROTLET ? FSE_HARMONIC : FSE_BIHARMONIC;
+        if (gk != M->green_kind || cfg->Mtilde != M->green_Mt || cfg->Ltilde != M->green_Lt ||
+            cfg->sf != M->green_sf || green_full != M->green_src) {
+            const int D = 2 * cfg->Mtilde;
+            for (int r = 0; r < G; ++r) {
+                Guard gd(M->ctx[r]);
+                fse_cuda_ctx* c = M->ctx[r];
+                if (M->greens[r]) fse_cuda_green_free(M->greens[r]);
+                M->greens[r] = nullptr;
+                if (green_full) {
+                    fse_green* gr = new_green(c, gk, cfg->Ltilde, cfg->Mtilde,
+                                              cfg->Ltilde / cfg->Mtilde, std::sqrt(3.0) * cfg->Ltilde);
+                    DevScratch scratch;
+                    const size_t nfull = static_cast<size_t>(D) * D * D;
+                    double* tmp = scratch.alloc<double>(nfull);
+                    h2d(c, tmp, green_full, nfull * sizeof(double));
+                    launch_green_full_to_half(L0(c), D, tmp, gr->d_half);
+                    FSE_CU(cudaStreamSynchronize(c->s0));
+                    M->greens[r] = gr;
+                } else {
+                    M->greens[r] = green_precompute(c, gk, cfg->Ltilde, cfg->Mtilde, cfg->sf);
+                }
+            }
+            M->green_src = green_full;
+            M->green_kind = gk;
+            M->green_Mt = cfg->Mtilde;
+            M->green_Lt = cfg->Ltilde;
+            M->green_sf = cfg->sf;
+        }
+        std::vector<std::string> errs(G);
+        std::vector<std::vector<double>> hu(G);
+        auto work = [&](int r) {
+            try {
+                fse_cuda_ctx* c = M->ctx[r];
+                Guard gd(c);
+                const auto& os = own_s[r];
+                const auto& ot = same ? own_s[r] : own_t[r];
+                std::vector<double> bp(3 * os.size()), bs(static_cast<size_t>(a) * os.size()),
+                    bt(same ? 0 : 3 * ot.size());
+                for (size_t j = 0; j < os.size(); ++j) {
+                    std::memcpy(&bp[3 * j], pos + 3 * os[j], 3 * sizeof(double));
+                    std::memcpy(&bs[a * j], str + a * os[j], a * sizeof(double));
+                }
+                if (!same)
+                    for (size_t j = 0; j < ot.size(); ++j)
+                        std::memcpy(&bt[3 * j], tgt + 3 * ot[j], 3 * sizeof(double));
+                double* dp = M->dp[r]->get<double>(bp.size());
+                double* ds = M->ds[r]->get<double>(bs.size());
+                double* dt = same ? dp : M->dt[r]->get<double>(bt.size());
+                double* du = M->du[r]->get<double>(3 * std::max<size_t>(ot.size(), 1));
+                if (!bp.empty()) h2d(c, dp, bp.data(), sizeof(double) * bp.size());
+                if (!bs.empty()) h2d(c, ds, bs.data(), sizeof(double) * bs.size());
+                if (!bt.empty()) h2d(c, dt, bt.data(), sizeof(double) * bt.size());
+                Rank& R = *M->ranks[r];
+                R.setup(cfg, kind, dp, ds, static_cast<int64_t>(os.size()), n, dt,
+                        static_cast<int64_t>(ot.size()), same);
+                run_rank_steps(R, M->nc[r], c->s0, M->greens[r]);
+                R.finish(du);
+                hu[r].resize(3 * ot.size());
+                if (!hu[r].empty()) d2h(c, hu[r].data(), du, sizeof(double) * hu[r].size());
+            } catch (const std::exception& e) {
+                errs[r] = e.what();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int r = 0; r < G; ++r) th.emplace_back(work, r);
+        for (auto& t : th) t.join();
+        for (int r = 0; r < G; ++r)
+            if (!errs[r].empty()) throw Error(FSE_ERUNTIME, "rank " + std::to_string(r) + ": " + errs[r]);
+        for (int r = 0; r < G; ++r) {
+            const auto& ot = same ? own_s[r] : own_t[r];
+            for (size_t j = 0; j < ot.size(); ++j)
+                std::memcpy(u + 3 * ot[j], &hu[r][3 * j], 3 * sizeof(double));
+        }
+        if (tm)  // only the whole call (host wall clock, transfers included) is timed
+            tm->total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start)
+                             .count();
+        return FSE_OK;
+    } catch (const Error& e) {
+        M->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        M->err = e.what();
+        return FSE_ERUNTIME;
+    }
 }
 
 }  // extern "C"

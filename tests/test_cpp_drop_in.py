@@ -32,3 +32,16 @@ def test_drop_in_runs_reference_acceptance(tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASS" in r.stdout
+
+
+@pytest.mark.gpu
+def test_drop_in_runs_on_the_multi_gpu_context(tmp_path):
+    """The same program with FSE_CUDA_DEVICES set: fse::total_sum runs the
+    partitioned evaluation (fse_cuda_multi_*, NCCL inside the library) over the
+    listed GPUs -- here the one GPU of the pool -- and still reproduces the
+    reference's recorded accuracies."""
+    exe = build(tmp_path)
+    env = dict(os.environ, FSE_CUDA_DEVICES="0")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL PASS" in r.stdout

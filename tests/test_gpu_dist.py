@@ -59,3 +59,29 @@ def test_virtual_ranks_cfg2_full_size(fse, ctx):
     got = ctx.dist_virtual_total_sum(s, 0, cfg, s.positions, g, 4, targets_are_sources=True)
     assert rel_max(got, want) <= 1e-12
     ctx.trim()
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_multi_device_context_one_gpu(fse, ctx, rng, kind):
+    """fse_cuda_multi_* (one process, ncclCommInitAll, a host thread per device,
+    host buffers in and out) on the one GPU the pool provides: the partition,
+    the NCCL steps and the scatter back to caller order, against total_sum;
+    with the caller's Green's table uploaded and with the per-device precompute."""
+    cfg = fse.make_config(1.0, 12.0, 0.25, 48, 16)
+    s = system(fse, rng, kind, 3000)
+    g = ctx.precompute_mollified_green(int(fse.green_kind_for(kind)), cfg.Ltilde, cfg.Mtilde,
+                                       cfg.sf)
+    want = ctx.total_sum(s, kind, cfg, s.positions, g)
+    m = fse.MultiContext([0])
+    got = m.total_sum(s, kind, cfg, s.positions)
+    assert rel_max(got, want) <= 1e-12
+    got2 = m.total_sum(s, kind, cfg, s.positions, green_full=g.fourier)
+    assert rel_max(got2, want) <= 1e-12
+    tgt = rng.uniform(0, 1, (500, 3))
+    want_t = ctx.total_sum(s, kind, cfg, tgt, g)
+    assert rel_max(m.total_sum(s, kind, cfg, tgt), want_t) <= 1e-12
+    bad = fse.SourceSystem(np.vstack([s.positions, [[0.5, 0.5, 7.0]]]),
+                           np.vstack([s.strengths, s.strengths[:1]]), 1.0)
+    with pytest.raises(fse.InvalidArgument):
+        m.total_sum(bad, kind, cfg, bad.positions)
+    m.close()
