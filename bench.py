@@ -57,7 +57,34 @@ WORKLOADS = {
                  desc="rotlet N=1e6 in 32 Gaussian blobs sigma=0.03, xi=110 rc=0.045 M=288 P=24"),
     "cfg5": dict(kind=0, wl=5, n=8_000_000, xi=220.0, rc=0.022, M=576, P=24, tol=1e-10,
                  desc="stokeslet N=8e6 + 8e6 distinct targets uniform, xi=220 rc=0.022 M=576 P=24"),
+    # tolerance-consistent variants: (rc, M, P) from the reference's
+    # select_parameters at the same xi and tolerance (estimates.cpp:81-126)
+    "cfg1t": dict(kind=0, wl=1, n=10_000, xi=28.0, tol=1e-8, select=True,
+                  desc="cfg1 inputs, (rc, M, P) = select_parameters(xi=28, tol=1e-8)"),
+    "cfg2t": dict(kind=0, wl=1, n=1_000_000, xi=110.0, tol=1e-10, select=True,
+                  desc="cfg2 inputs, (rc, M, P) = select_parameters(xi=110, tol=1e-10)"),
+    "cfg3t": dict(kind=1, wl=3, n=100_000, xi=40.0, tol=1e-8, select=True,
+                  desc="cfg3 inputs, (rc, M, P) = select_parameters(xi=40, tol=1e-8)"),
+    "cfg4t": dict(kind=2, wl=4, n=1_000_000, xi=110.0, tol=1e-10, select=True,
+                  desc="cfg4 inputs, (rc, M, P) = select_parameters(xi=110, tol=1e-10)"),
 }
+
+
+def quadratic_sum(strengths) -> float:
+    """strength_quadratic_sum (kernels.cpp:105-110): sequential sum of c_i^2."""
+    return float(np.cumsum((strengths * strengths).ravel())[-1])
+
+
+def workload_config(w, strengths, lib):
+    """The workload's EwaldConfig: explicit (rc, M, P), or the tolerance-consistent
+    choice of select_parameters (lib = the product package or oracle.refimpl)."""
+    if not w.get("select"):
+        return lib.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    cfg, feasible = lib.select_parameters(w["kind"], w["n"], 1.0, quadratic_sum(strengths),
+                                          w["xi"], w["tol"])
+    if not feasible:
+        raise SystemExit(f"select_parameters: tolerance {w['tol']} infeasible")
+    return cfg
 KIND_NAMES = ["stokeslet", "stresslet", "rotlet"]
 SEED = 20260101
 
@@ -239,7 +266,7 @@ def run_dist(args, dist: Dist):
     tas = tgt is None
     targets = system.positions if tas else tgt
     n_total, nt_total = system.size(), targets.shape[0]
-    cfg = fse.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    cfg = workload_config(w, system.strengths, fse)
     G, r = dist.world, dist.rank
     own_s = np.nonzero(fse.dist_owner(cfg, G, system.positions) == r)[0]
     own_t = own_s if tas else np.nonzero(fse.dist_owner(cfg, G, targets) == r)[0]
@@ -355,7 +382,7 @@ def run_ours(args, dist: Dist):
     targets = system.positions if tgt is None else tgt
     n, nt = system.size(), targets.shape[0]
     tas = 1 if tgt is None else 0
-    cfg = fse.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    cfg = workload_config(w, system.strengths, fse)
     t0 = time.perf_counter()
     green = ctx.precompute_mollified_green(int(fse.green_kind_for(w["kind"])), cfg.Ltilde,
                                            cfg.Mtilde, cfg.sf)
@@ -473,7 +500,8 @@ def run_ours(args, dist: Dist):
         "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}+rank), "
                 "no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
-                   "N": n, "NT": nt, "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
+                   "N": n, "NT": nt, "xi": cfg.xi, "rc": cfg.rc, "M": cfg.M, "P": cfg.P,
+                   "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
                    "eta": round(cfg.eta, 4), "parallelism": f"replicas x{dist.world}",
                    "l2": working_set_note(w, cfg),
                    "green_precompute_s": round(precompute_s, 3)},
@@ -555,7 +583,8 @@ def reference_full(w, steps: int, warmup: int, budget_s: float):
     from oracle import refimpl as R
     if not R.available():
         return None, "oracle/_ref (the reference built from its sources) is missing"
-    cfg = R.make_config(1.0, w["xi"], w["rc"], w["M"], w["P"])
+    pos, st, tgt = R.generate_workload(w["wl"], w["n"], SEED)
+    cfg = workload_config(w, st, R)
     a = 9 if w["kind"] == 1 else 3
     D, Mt = cfg.D, cfg.Mtilde
     fixed = a * 8 * Mt ** 3 + (a + 3) * 16 * D ** 3 + 8 * D ** 3 + w["n"] * (48 + 8 * a) * 3
@@ -567,7 +596,6 @@ def reference_full(w, steps: int, warmup: int, budget_s: float):
         return None, (f"reference total_sum needs ~{(fixed + per_thread) / 1e9:.0f} GB of host "
                       f"RAM; {avail / 0.85 / 1e9:.0f} GB available")
     R.set_threads(thr)
-    pos, st, tgt = R.generate_workload(w["wl"], w["n"], SEED)
     targets = pos if tgt is None else tgt
     t0 = time.perf_counter()
     green = R.precompute_green(R.green_kind_for(w["kind"]), cfg.Ltilde, cfg.Mtilde, cfg.sf)

@@ -824,7 +824,9 @@ def rms_error(u, u_ref, relative):  # kernels.cpp:91-103
 
 
 def strength_quadratic_sum(system: SourceSystem) -> float:  # kernels.cpp:105-110
-    return float((system.strengths ** 2).sum())
+    """Sequential sum of c_i^2 in the reference's order (bit-identical Q)."""
+    st = system.strengths
+    return float(np.cumsum((st * st).ravel())[-1]) if st.size else 0.0
 
 
 def generate_system(kind, n, L, seed) -> SourceSystem:

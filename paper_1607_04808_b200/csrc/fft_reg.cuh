@@ -140,7 +140,7 @@ __host__ __device__ constexpr int first_radix(int n) {
 }
 // composite register sizes that own a twiddle table, in table order
 // (only the composite sizes the engines in k_fft.cu use; twid<> static_asserts)
-constexpr int kRegSizes[] = {15, 20, 22, 24, 26, 30, 32, 40};
+constexpr int kRegSizes[] = {10, 12, 15, 20, 22, 24, 26, 30, 32, 40};
 constexpr int kNumRegSizes = sizeof(kRegSizes) / sizeof(int);
 __host__ __device__ constexpr int tw_off_of(int n) {
     int off = 0;
@@ -396,6 +396,91 @@ __device__ __forceinline__ void pass2_smem(double2* buf, int ncol, int sgn, cons
     if (act) {
 #pragma unroll
         for (int k2 = 0; k2 < D2; ++k2) buf[ridx<D1, D2>(c, k1 + D1 * k2)] = u[k2];
+    }
+}
+
+// ---- three-level column FFT, D = D1 D2 D3 (small register DFTs, more
+// resident warps than a two-level split of the same D; the opt-in engine 8,
+// 1200 = 10 x 12 x 10, measured slower than the two-level engine: k_fft.cu
+// engine_for).  Layout: element n of column c
+// at c S3 + n + n / D3 (one pad per D3 elements), S3 = col_stride3.  With
+// n = n1 D2 D3 + n2 D3 + n3 and k = k1 + D1 k2 + D1 D2 k3:
+//   pass A, item (c, m = n2 D3 + n3): FFT_D1 over n1, times W_D^{k1 m};
+//   pass B, item (c, k1, n3): FFT_D2 over n2, times W_{D2 D3}^{k2 n3};
+//   pass C, item (c, k1, k2): FFT_D3 over n3, stored at the natural k.
+// Passes A and B work in place on item-local positions; pass C reads all of
+// a column group before any store (barrier), `grp` columns at a time.
+// WD: W_D^t (t < D, global memory); W23: W_{D2 D3}^t (t < D2 D3); tab: the
+// small register tables.  Every thread of the CTA must call it.
+__host__ __device__ constexpr int col_stride3(int D, int D3) {
+    return D + D / D3 + 1 + ((3 - (D + D / D3 + 1) % 8) + 8) % 8;
+}
+template <int D1, int D2, int D3>
+__device__ __forceinline__ int idx3(int c, int n) {
+    return c * col_stride3(D1 * D2 * D3, D3) + n + n / D3;
+}
+__device__ __forceinline__ double2 twc(const double2* t, int e, int sgn) {
+    double2 w = t[e];
+    if (sgn > 0) w.y = -w.y;
+    return w;
+}
+template <int D1, int D2, int D3>
+__device__ __forceinline__ void fft_cols_3l(double2* buf, int ncol, int sgn,
+                                            const double2* __restrict__ WD, const double2* W23,
+                                            const double2* tab) {
+    constexpr int D = D1 * D2 * D3, M23 = D2 * D3;
+    const int T = blockDim.x;
+    // pass A
+    for (int it = threadIdx.x; it < ncol * M23; it += T) {
+        const int c = it / M23, m = it - c * M23;
+        double2 v[D1];
+#pragma unroll
+        for (int n1 = 0; n1 < D1; ++n1) v[n1] = buf[idx3<D1, D2, D3>(c, n1 * M23 + m)];
+        rfft<D1>(v, sgn, tab);
+        int t = 0;
+#pragma unroll
+        for (int k1 = 0; k1 < D1; ++k1) {
+            if (k1 > 0) v[k1] = cmul(v[k1], twc(WD, t, sgn));
+            t += m;
+            if (t >= D) t -= D;
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < D1; ++k1) buf[idx3<D1, D2, D3>(c, k1 * M23 + m)] = v[k1];
+    }
+    __syncthreads();
+    // pass B
+    for (int it = threadIdx.x; it < ncol * D1 * D3; it += T) {
+        const int c = it / (D1 * D3), r = it - c * (D1 * D3);
+        const int k1 = r / D3, n3 = r - k1 * D3;
+        double2 v[D2];
+#pragma unroll
+        for (int n2 = 0; n2 < D2; ++n2) v[n2] = buf[idx3<D1, D2, D3>(c, k1 * M23 + n2 * D3 + n3)];
+        rfft<D2>(v, sgn, tab);
+#pragma unroll
+        for (int k2 = 1; k2 < D2; ++k2) v[k2] = cmul(v[k2], twc(W23, k2 * n3, sgn));
+#pragma unroll
+        for (int k2 = 0; k2 < D2; ++k2) buf[idx3<D1, D2, D3>(c, k1 * M23 + k2 * D3 + n3)] = v[k2];
+    }
+    __syncthreads();
+    // pass C, `grp` columns per round: load + FFT, barrier, natural-order store
+    const int grp = T / (D1 * D2) > 0 ? T / (D1 * D2) : 1;
+    for (int c0 = 0; c0 < ncol; c0 += grp) {
+        const int it = threadIdx.x;
+        const int c = c0 + it / (D1 * D2), r = it - (it / (D1 * D2)) * (D1 * D2);
+        const bool act = it < grp * D1 * D2 && c < ncol;
+        const int k1 = r % D1, k2 = r / D1;
+        double2 v[D3];
+        if (act) {
+#pragma unroll
+            for (int n3 = 0; n3 < D3; ++n3) v[n3] = buf[idx3<D1, D2, D3>(c, k1 * M23 + k2 * D3 + n3)];
+            rfft<D3>(v, sgn, tab);
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+            for (int k3 = 0; k3 < D3; ++k3) buf[idx3<D1, D2, D3>(c, k1 + D1 * k2 + D1 * D2 * k3)] = v[k3];
+        }
+        __syncthreads();
     }
 }
 

@@ -787,8 +787,15 @@ fse_status fse_cuda_create(int device, fse_cuda_ctx** out) {
     c->device = device;
     try {
         FSE_CU(cudaSetDevice(device));
-        FSE_CU(cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking));
-        FSE_CU(cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking));
+        // FSE_S1_PRIORITY=high|low: scheduling priority of the real-space stream
+        // relative to the Fourier stream (default: equal)
+        int lo = 0, hi = 0;
+        FSE_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const char* pr = std::getenv("FSE_S1_PRIORITY");
+        const int p1 = pr && std::strcmp(pr, "high") == 0 ? hi : lo;
+        const int p0 = pr && std::strcmp(pr, "low") == 0 ? hi : lo;
+        FSE_CU(cudaStreamCreateWithPriority(&c->s0, cudaStreamNonBlocking, p0));
+        FSE_CU(cudaStreamCreateWithPriority(&c->s1, cudaStreamNonBlocking, p1));
         for (auto& e : c->ev) FSE_CU(cudaEventCreate(&e));
         for (auto& e : c->mark) FSE_CU(cudaEventCreate(&e));
         FSE_CU(cudaMalloc(&c->d_flags, 8 * sizeof(int)));

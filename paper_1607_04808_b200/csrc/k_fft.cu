@@ -167,43 +167,65 @@ __device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int nco
 // circular convolution of length Mb = D1 D2 >= 2N - 1 on the register engine.
 template <int ENG>
 struct Eng {
-    static constexpr int D1 = 1, D2 = 1;
+    static constexpr int D1 = 1, D2 = 1, D3 = 1;
     static constexpr bool BLUE = false;
+    static constexpr bool THREE = false;
 };
 template <>
 struct Eng<1> {
     static constexpr int D1 = 24, D2 = 26;
     static constexpr bool BLUE = false;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<2> {
     static constexpr int D1 = 30, D2 = 40;
     static constexpr bool BLUE = false;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<3> {
     static constexpr int D1 = 22, D2 = 32;
     static constexpr bool BLUE = false;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<4> {
     static constexpr int D1 = 11, D2 = 22;
     static constexpr bool BLUE = false;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<5> {  // Bluestein, Mb = 400: N <= 200 (cfg1: 194 = 2 x 97)
     static constexpr int D1 = 20, D2 = 20;
     static constexpr bool BLUE = true;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<6> {  // Bluestein, Mb = 624: N <= 312 (cfg3: 298 = 2 x 149)
     static constexpr int D1 = 24, D2 = 26;
     static constexpr bool BLUE = true;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
 };
 template <>
 struct Eng<7> {  // Bluestein, Mb = 1024: N <= 512
     static constexpr int D1 = 32, D2 = 32;
     static constexpr bool BLUE = true;
+    static constexpr bool THREE = false;
+    static constexpr int D3 = 1;
+};
+
+template <>
+struct Eng<8> {  // three-level 1200 = 10 x 12 x 10 (cfg5)
+    static constexpr int D1 = 10, D2 = 12, D3 = 10;
+    static constexpr bool BLUE = false;
+    static constexpr bool THREE = true;
 };
 
 template <int ENG>
@@ -211,6 +233,10 @@ __device__ __forceinline__ double2* fft_cols(double2* a, double2* b, int ncol, c
                                              const double2* __restrict__ tw, int sgn) {
     if constexpr (ENG == 0) {
         return fft_stockham(a, b, ncol, pl, tw, sgn);
+    } else if constexpr (Eng<ENG>::THREE) {
+        constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D3 = Eng<ENG>::D3;
+        freg::fft_cols_3l<D1, D2, D3>(a, ncol, sgn, pl.wd, tw, tw + D2 * D3);
+        return a;
     } else if constexpr (!Eng<ENG>::BLUE) {
         constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2;
         freg::fft_cols_2l<D1, D2>(a, ncol, sgn, tw, tw + D1 * D2);
@@ -262,6 +288,8 @@ template <int ENG>
 __device__ __forceinline__ int cidx(int c, int n, int D) {
     if constexpr (ENG == 0) {
         return pad(c * D + n);
+    } else if constexpr (Eng<ENG>::THREE) {
+        return freg::idx3<Eng<ENG>::D1, Eng<ENG>::D2, Eng<ENG>::D3>(c, n);
     } else {
         return freg::ridx<Eng<ENG>::D1, Eng<ENG>::D2>(c, n);
     }
@@ -317,10 +345,13 @@ __device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPl
 template <int ENG>
 constexpr int eng_threads() { return ENG == 2 ? 128 : 256; }
 inline int eng_threads_host(int eng) { return eng == 2 ? 128 : 256; }
+// resident CTAs per SM the kernels are register-limited for (three-level: 3)
+template <int ENG>
+constexpr int eng_minb() { return Eng<ENG>::THREE ? 2 : 2; }
 
 // ------------------------------------------------------------------ test kernel
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
                                                      double2* data, int ncol_total, int ncol,
                                                      int sgn) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
@@ -339,7 +370,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_fft_test(FftPlan pl, 
 // ------------------------------------------------------------------ z forward
 // column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double* __restrict__ R,
                                                  double2* __restrict__ B) {
@@ -398,7 +429,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd(FftPlan pl, cons
 // forward: columns (comp, i, kz-tile of ncol); input B[comp][i][j][kz], j < Mt
 // inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int A, int nxs, int nkys,
                                                   int ncol, double2* __restrict__ B,
                                                   double2* __restrict__ Cb, BlockDest dst) {
@@ -629,7 +660,7 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
 // ------------------------------------------------------------------ z inverse
 // row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double2* __restrict__ B,
                                                  double* __restrict__ W) {
@@ -691,7 +722,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zinv(FftPlan pl, cons
 
 // z forward: column c = row pair (comp, i, jp), rows contiguous -> n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double* __restrict__ R,
                                                   double2* __restrict__ B) {
@@ -745,7 +776,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zfwd2(FftPlan pl, con
 
 // y passes: column c = (comp, slab plane xl, kz0 + c), columns adjacent in kz -> c-fastest
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
                                                    int Mt, int nx, int A, int nxs, int nkys,
                                                    int ncol, double2* __restrict__ B,
                                                    double2* __restrict__ Cb, BlockDest dst) {
@@ -880,7 +911,7 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
 
 // z inverse: row pairs, Hermitian extension loaded straight from B, n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), 2) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double2* __restrict__ B,
                                                   double* __restrict__ W) {
@@ -959,6 +990,16 @@ int engine_for(int D, int* D1, int* D2) {
     };
     const E table[] = {{624, 1, 24, 26}, {1200, 2, 30, 40}, {704, 3, 22, 32}, {242, 4, 11, 22}};
     if (std::getenv("FSE_FFT_STOCKHAM")) return 0;
+    // three-level engine, opt-in: measured slower than the two-level ones on B200
+    // (cfg5: forward z+y 25.0 vs 18.5 ms, x pass 74.8 vs 71.1 ms, inverse 27.0 vs
+    // 17.7 ms; the same split for 624 = 8 x 6 x 13: x pass 9.4 vs 5.6 ms) -- more
+    // resident warps, but three shared-memory passes and the staged (v1) kernels
+    if (D == 1200 && std::getenv("FSE_FFT_1200_3L")) {  // three-level 10 x 12 x 10
+        *D1 = 10;
+        *D2 = 12;
+        return 8;
+    }
+
     for (const E& t : table)
         if (t.D == D) {
             *D1 = t.d1;
@@ -1005,7 +1046,7 @@ int v2_mask_env() {
 }
 template <int ENG>
 int v2_mask_for() {
-    if (Eng<ENG>::BLUE) return 0;
+    if (Eng<ENG>::BLUE || Eng<ENG>::THREE) return 0;
     const int e = v2_mask_env();
     if (e >= 0) return e;
     // measured per engine on B200: 624 (cfg2) all but the inverse y pass;
@@ -1022,6 +1063,22 @@ HostFftPlan make_fft_plan(int D) {
     std::memset(&h.dev, 0, sizeof h.dev);
     h.dev.D = D;
     h.eng = engine_for(D, &h.D1, &h.D2);
+    if (h.eng == 8) {
+        // staged: W_{D2 D3}^t (t < D2 D3) and the small register tables; then
+        // W_D^t (t < D) read from global memory (dev.wd, set per launch)
+        h.D3 = D / (h.D1 * h.D2);
+        const int M23 = h.D2 * h.D3;
+        for (int t = 0; t < M23; ++t) h.tw.push_back(cexp_neg(t, M23));
+        for (int i = 0; i < freg::kNumRegSizes; ++i) {
+            const int n = freg::kRegSizes[i];
+            for (int t = 0; t < n; ++t) h.tw.push_back(cexp_neg(t, n));
+        }
+        h.tw_staged = static_cast<int>(h.tw.size());
+        for (int t = 0; t < D; ++t) h.tw.push_back(cexp_neg(t, D));
+        h.dev.nst = 0;
+        h.dev.dD = make_fdiv(D);
+        return h;
+    }
     if (h.eng > 0) {
         const int Mb = h.D1 * h.D2;  // = D for the plain register engines
         // table: W_Mb^t (t < Mb), then the small register-FFT tables
@@ -1113,13 +1170,19 @@ HostFftPlan make_fft_plan(int D) {
 namespace {
 
 size_t col_elems(const HostFftPlan& h, int cols) {
+    if (h.eng == 8)  // freg::idx3 layout
+        return static_cast<size_t>(cols) * freg::col_stride3(h.dev.D, h.D3) + 8;
     if (h.eng > 0)  // freg::ridx layout (Bluestein: columns of the Mb-point engine)
         return static_cast<size_t>(cols) * freg::col_stride(h.D1, h.D2) + 8;
     return static_cast<size_t>(cols) * h.dev.D + (static_cast<size_t>(cols) * h.dev.D) / 8 + 8;
 }
 
+size_t staged_tw(const HostFftPlan& h) {
+    return h.tw_staged >= 0 ? static_cast<size_t>(h.tw_staged) : h.tw.size();
+}
+
 size_t smem_bytes(const HostFftPlan& h, int cols) {
-    return (col_elems(h, cols) * (h.generic ? 2 : 1) + h.tw.size()) * sizeof(double2);
+    return (col_elems(h, cols) * (h.generic ? 2 : 1) + staged_tw(h)) * sizeof(double2);
 }
 
 // largest number of units (each `cols_per_unit` columns) that fits the
@@ -1131,7 +1194,9 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap, int threa
         const int cols = u * cols_per_unit;
         if (smem_bytes(h, cols) > cap) break;
         bool ok = true;
-        if (h.eng > 0) {
+        if (h.eng == 8) {
+            ok = true;  // the three-level passes loop over their items
+        } else if (h.eng > 0) {
             const int T = threads > 0 ? threads : eng_threads_host(h.eng);
             ok = cols * h.D1 <= T && cols * h.D2 <= T;
         } else {
@@ -1148,7 +1213,9 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap, int threa
 
 // two CTAs per SM when possible, otherwise one CTA with up to ~220 KB
 int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit, int threads = 0) {
-    for (size_t cap : {kSmemCap, static_cast<size_t>(220 * 1024)}) {
+    // three-level engine: three CTAs per SM when they fit
+    const size_t cap3 = (h.eng == 8) ? static_cast<size_t>(74 * 1024) : kSmemCap;
+    for (size_t cap : {cap3, kSmemCap, static_cast<size_t>(220 * 1024)}) {
         int u = units_per_cta(h, cols_per_unit, cap, threads);
         while (u > 0 && smem_bytes(h, u * cols_per_unit) + extra_per_unit * u > cap) --u;
         if (u > 0) return u;
@@ -1156,10 +1223,11 @@ int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit, in
     throw Error(FSE_EINVAL, "FFT: grid size does not fit the shared-memory engine");
 }
 
-void set_buf(FftPlan& p, const HostFftPlan& h, int cols) {
+void set_buf(FftPlan& p, const HostFftPlan& h, int cols, const double2* d_tw) {
     p.buf_elems = static_cast<int>(col_elems(h, cols));
+    p.wd = d_tw + staged_tw(h);  // three-level engine: the global W_D table
     p.two_bufs = h.generic ? 1 : 0;
-    p.tw_elems = static_cast<int>(h.tw.size());
+    p.tw_elems = static_cast<int>(staged_tw(h));
 }
 
 template <class K>
@@ -1179,6 +1247,7 @@ void with_engine(int eng, F&& f) {
         case 5: f(std::integral_constant<int, 5>{}); break;
         case 6: f(std::integral_constant<int, 6>{}); break;
         case 7: f(std::integral_constant<int, 7>{}); break;
+        case 8: f(std::integral_constant<int, 8>{}); break;
         default: f(std::integral_constant<int, 0>{}); break;
     }
 }
@@ -1190,7 +1259,7 @@ void fft_test_columns(const Launch& L, const HostFftPlan& h, const double2* d_tw
     upload_consts();
     const int u = units_fit(h, 1, 0);
     FftPlan p = h.dev;
-    set_buf(p, h, u);
+    set_buf(p, h, u, d_tw);
     const size_t sm = smem_bytes(h, u);
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
@@ -1224,11 +1293,11 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
         {
             const int u = units_fit(h, 1, 0);
             FftPlan p = h.dev;
-            set_buf(p, h, u);
+            set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
-            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 1) {
                     allow_smem(k_zfwd2<EV>, sm);
                     k_zfwd2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
@@ -1246,11 +1315,11 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
         {
             const int u = std::min(units_fit(h, 1, 0), Dh);
             FftPlan p = h.dev;
-            set_buf(p, h, u);
+            set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
             const int ntz = (Dh + u - 1) / u;
             const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
-            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 2) {
                     allow_smem(k_ypass2<EV, false>, sm);
                     k_ypass2<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
@@ -1294,7 +1363,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
                          : eng_threads_host(h.eng);
     const int u = std::min(units_fit(h, A, gcol, xthr), Dh);
     FftPlan p = h.dev;
-    set_buf(p, h, A * u);
+    set_buf(p, h, A * u, d_tw);
     // v2: exp factor table (D doubles) after the twiddles
     const size_t sm = smem_bytes(h, A * u) + gcol * u + (gcol ? 0 : sizeof(double) * D);
     const int ntz = (Dh + u - 1) / u;
@@ -1302,7 +1371,7 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     if (blocks == 0) return;
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
-        if constexpr (EV > 0 && !Eng<EV>::BLUE) if (v2_mask_for<EV>() & 4) {
+        if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) if (v2_mask_for<EV>() & 4) {
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
                 k_xscale2<EV, FSE_STOKESLET><<<blocks, xs_threads<EV, FSE_STOKESLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
@@ -1348,11 +1417,11 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
         {
             const int u = std::min(units_fit(h, 1, 0), Dh);
             FftPlan p = h.dev;
-            set_buf(p, h, u);
+            set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
             const int ntz = (Dh + u - 1) / u;
             const unsigned nb = static_cast<unsigned>(static_cast<int64_t>(ncomp) * nx * ntz);
-            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 8) {
                     allow_smem(k_ypass2<EV, true>, sm);
                     k_ypass2<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
@@ -1373,11 +1442,11 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
         {
             const int u = units_fit(h, 1, 0);
             FftPlan p = h.dev;
-            set_buf(p, h, u);
+            set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
             const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
             const unsigned nb = static_cast<unsigned>((npairs + u - 1) / u);
-            if constexpr (EV > 0 && !Eng<EV>::BLUE) {
+            if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 16) {
                     allow_smem(k_zinv2<EV>, sm);
                     k_zinv2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);

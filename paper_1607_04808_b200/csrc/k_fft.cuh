@@ -56,6 +56,7 @@ struct FftPlan {
     FDiv dNsP[kFftMaxStages];  // Ns p
     FDiv dD;                   // D
     int tw_elems;           // twiddle table length (copied to shared memory)
+    const double2* wd;      // three-level engine: W_D^t, t < D, in global memory
     int two_bufs;           // a generic stage needs a second column buffer
     int buf_elems;          // padded column-buffer length (set per launch)
 };
@@ -67,7 +68,9 @@ struct HostFftPlan {
     bool generic = false;     // a non-register (generic DFT) stage is present
     int eng = 0;              // 0: shared-memory Stockham; >0: two-level register engine
     bool blue = false;        // Bluestein over an Mb = D1 D2 register engine (eng 5..7)
-    int D1 = 0, D2 = 0;       // D = D1 * D2 for eng > 0
+    int D1 = 0, D2 = 0;       // D = D1 * D2 for eng > 0 (three-level: D = D1 D2 D3)
+    int D3 = 1;
+    int tw_staged = -1;       // leading entries of tw staged in shared memory (-1: all)
 };
 
 HostFftPlan make_fft_plan(int D);

@@ -124,3 +124,29 @@ def test_cfg5_full_size(fse, ctx):
     ref = ctx.direct_sum(s, 0, tgt[idx], False)
     err = fse.rms_error(u[idx], ref, True)
     assert 1e-7 < err < 5e-3, err
+
+
+def test_cfg2t_tolerance_consistent_meets_tolerance(fse, ctx):
+    """cfg2's tolerance-consistent variant (SURVEY 8(d): the reference's
+    select_parameters at xi = 110, tol = 1e-10 -> M = 414, D = 888, a Bluestein
+    x pass) reaches the stated tolerance against the O(N^2) direct sum on 1024
+    sampled targets (estimates.cpp:81-126).  The reference itself cannot run
+    this config in the build container (~70 GB of C2C spectra)."""
+    s, _ = fse.generate_workload(fse.WL_UNIFORM, 1_000_000, 20260101)
+    Q = fse.strength_quadratic_sum(s)
+    cfg, feasible = fse.select_parameters(0, s.size(), 1.0, Q, 110.0, 1e-10)
+    assert feasible and cfg.M == 414 and cfg.D == 888
+    g = ctx.precompute_mollified_green(1, cfg.Ltilde, cfg.Mtilde, cfg.sf)
+    u = ctx.total_sum(s, 0, cfg, s.positions, g, targets_are_sources=1)
+    rows = np.sort(np.random.default_rng(9).choice(s.size(), 1024, replace=False))
+    mask = np.ones(s.size(), bool)
+    mask[rows] = False
+    # direct sum at the sampled sources, each target's own source excluded
+    rest = fse.SourceSystem(s.positions[mask], s.strengths[mask], 1.0)
+    own = fse.SourceSystem(s.positions[rows], s.strengths[rows], 1.0)
+    ud = ctx.direct_sum(rest, 0, s.positions[rows], False) + \
+        ctx.direct_sum(own, 0, s.positions[rows], True)
+    err = fse.rms_error(u[rows], ud, True)
+    print("cfg2t rel rms vs direct", err)
+    assert err <= 1e-10
+    ctx.trim()
