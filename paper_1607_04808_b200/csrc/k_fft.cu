@@ -129,6 +129,45 @@ __device__ __forceinline__ void stage_gen(const double2* in, double2* out, int D
     __syncthreads();
 }
 
+// generic odd radix P as the FIRST stage (Ns = 1, no inter-stage twiddles): a
+// thread per output pair (q, P - q) of one input group b, using
+//   v_r W^{rq} + v_{P-r} W^{-rq} = cos(.) (v_r + v_{P-r}) + i sin(.) (v_r - v_{P-r})
+// so X_q = A + iB, X_{P-q} = A - iB with A = v_0 + sum_r cos (v_r + v_{P-r}),
+// B = sum_r sin (v_r - v_{P-r}), r = 1 .. (P-1)/2: half the loads and FMAs of
+// stage_gen per output.  The lanes of a group load the same inputs (broadcasts).
+__device__ __forceinline__ void stage_gen_pairs(const double2* in, double2* out, int D, int ncol,
+                                                int P, const FftPlan& pl,
+                                                const double2* __restrict__ W, int sgn) {
+    const int H = (P - 1) / 2, nb = D / P;
+    const int per_b = H + 1;
+    const int tot = ncol * nb * per_b;
+    for (int it = threadIdx.x; it < tot; it += blockDim.x) {
+        const int cb = it / per_b, q = it - cb * per_b;
+        const int c = cb / nb, b = cb - c * nb;
+        const double2* src = in + 0;
+        const int base = c * D + b;
+        const double2 v0 = src[pad(base)];
+        double2 A = v0, B = make_double2(0.0, 0.0);
+        int t = 0;
+        for (int r = 1; r <= H; ++r) {
+            t += q;
+            if (t >= P) t -= P;
+            const double2 w = W[t];  // W_P^{rq}: (cos, sin) of the forward sign
+            const double cs = w.x, sn = sgn > 0 ? -w.y : w.y;
+            const double2 x1 = src[pad(base + r * nb)], x2 = src[pad(base + (P - r) * nb)];
+            A.x = fma(cs, x1.x + x2.x, A.x);
+            A.y = fma(cs, x1.y + x2.y, A.y);
+            B.x = fma(sn, x1.x - x2.x, B.x);
+            B.y = fma(sn, x1.y - x2.y, B.y);
+        }
+        // X_q = A + i B ; X_{P-q} = A - i B   (i B = (-B.y, B.x))
+        const int o = c * D + b * P;
+        out[pad(o + q)] = make_double2(A.x - B.y, A.y + B.x);
+        if (q > 0) out[pad(o + P - q)] = make_double2(A.x + B.y, A.y - B.x);
+    }
+    __syncthreads();
+}
+
 template <int P>
 __device__ __forceinline__ void run_radix(double2* cur, int& s, const FftPlan& pl, int ncol,
                                           const double2* __restrict__ tw, int sgn) {
@@ -146,7 +185,10 @@ __device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int nco
     double2* cur = a;
     int s = 0;
     if (pl.nst > 0 && pl.p[0] > 13) {
-        stage_gen(cur, b, pl.D, ncol, pl.p[0], pl.Ns[0], pl, 0, tw + pl.tw[0], sgn);
+        if (pl.Ns[0] == 1 && (pl.p[0] & 1))
+            stage_gen_pairs(cur, b, pl.D, ncol, pl.p[0], pl, tw + pl.tw[0], sgn);
+        else
+            stage_gen(cur, b, pl.D, ncol, pl.p[0], pl.Ns[0], pl, 0, tw + pl.tw[0], sgn);
         cur = b;
         s = 1;
     }
