@@ -174,9 +174,18 @@ __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2,
         const double uu = xr * (kNI / kXMax);
         const int iv = min(static_cast<int>(uu), kNI - 1);
         const double t = 2.0 * (uu - iv) - 1.0;
+#ifdef FSE_RS_HORNER
         double ex = tab[kDeg][iv];
 #pragma unroll
         for (int j = kDeg - 1; j >= 0; --j) ex = fma(ex, t, tab[j][iv]);
+#else
+        // Estrin (degree 7): dependency depth 4 instead of Horner's 7
+        static_assert(kDeg == 7, "Estrin scheme written for degree 7");
+        const double t2 = t * t, t4 = t2 * t2;
+        const double a0 = fma(tab[1][iv], t, tab[0][iv]), a1 = fma(tab[3][iv], t, tab[2][iv]);
+        const double a2 = fma(tab[5][iv], t, tab[4][iv]), a3 = fma(tab[7][iv], t, tab[6][iv]);
+        const double ex = fma(fma(a3, t2, a2), t4, fma(a1, t2, a0));
+#endif
         const double E = exp_neg_bounded(-xr * xr);
         const double sx = c_exp[17] * xr;  // 2 x / sqrt(pi)
         if (KIND == FSE_STOKESLET) {

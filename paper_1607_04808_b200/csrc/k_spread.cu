@@ -33,7 +33,10 @@ namespace {
 // NWARP = 2: warp w owns z [8w, 8w + 8) of all 8 x-rows; NWARP = 4: warp w
 // owns x-rows [4 (w % 2), +4) and z [8 (w / 2), +8).  CH = 64 points per chunk
 // (staged by the first 64 threads).
-constexpr int TX = 8, TY = 8, TZ = 16, CH = 64, NWARP = FSE_SPREAD_NWARP;
+#ifndef FSE_SPREAD_CH
+#define FSE_SPREAD_CH 64
+#endif
+constexpr int TX = 8, TY = 8, TZ = 16, CH = FSE_SPREAD_CH, NWARP = FSE_SPREAD_NWARP;
 constexpr int XS = NWARP / 2, XW = TX / XS;  // x splits, x-rows per warp
 // 4 warps: (x-half, z-half) domains, 96 registers for five CTAs per SM
 // (cfg2 spread 7.28 -> 6.60 ms against 2 warps with all 8 x-rows each)
@@ -175,7 +178,15 @@ __global__ void __launch_bounds__(NWARP * 32, FSE_SPREAD_MINB) k_spread(GridPara
     unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) cnts[0][warp] = __popc(bal);
     __syncthreads();
-    if (keep) stage(st[0], (warp ? cnts[0][0] : 0) + __popc(bal & ((1u << lane) - 1u)), q, ix, iy, iz);
+    // slot of this thread's kept point: kept points of the staging warps before it
+    auto slot_of = [&](int kk) {
+        int off = 0;
+#pragma unroll
+        for (int w = 0; w < CH / 32; ++w)
+            if (w < warp) off += cnts[kk][w];
+        return off + __popc(bal & ((1u << lane) - 1u));
+    };
+    if (keep) stage(st[0], slot_of(0), q, ix, iy, iz);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     int k = 0, b = 0;
     while (cur.kx <= tx) {
@@ -191,11 +202,12 @@ __global__ void __launch_bounds__(NWARP * 32, FSE_SPREAD_MINB) k_spread(GridPara
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();  // chunk k staged; everyone is done with buffer b ^ 1
         if (keep)
-            stage(st[b ^ 1], (warp ? cnts[kn][0] : 0) + __popc(bal & ((1u << lane) - 1u)), q, ix,
-                  iy, iz);
+            stage(st[b ^ 1], slot_of(kn), q, ix, iy, iz);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const Stage& S = st[b];
-        const int total = cnts[k][0] + cnts[k][1];
+        int total = 0;
+#pragma unroll
+        for (int w = 0; w < CH / 32; ++w) total += cnts[k][w];
         // groups of 4 points = one k-step of m8n8k4:
         //   A[(x, y)][p] = wx_p[x] wy_p[y]   (m-tile = one x, rows y)
         //   B[p][(c, z)] = f_{c,p} wz_p[z]   (n-tile = one component, 8 z of this warp)
