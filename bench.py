@@ -708,7 +708,7 @@ def main():
                     help="N > 1: independent full evaluations per GPU instead of z-slabs")
     ap.add_argument("--slabs", action="store_true",
                     help="use the partitioned path also at N = 1 (one slab, NCCL group of one)")
-    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+    ap.add_argument("--ref-budget-s", type=float, default=80.0,
                     help="--impl reference: stop timing full-size calls after this many seconds")
     ap.add_argument("--fp64-peak", type=float, default=None,
                     help="TFLOP/s; default: measured in-run with a DFMA loop")
