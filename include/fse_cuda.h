@@ -205,11 +205,14 @@ fse_status fse_dist_masks(const fse_config* cfg, int nranks, const double* pos, 
                           int targets, uint32_t* mask);
 /* the whole partitioned algorithm with nranks VIRTUAL ranks on this context's device
  * (exchanges as device copies): partitions all n points by the ownership rule, runs
- * every step of every rank, returns u for all targets in caller order (tests) */
+ * every step of every rank, returns u for all targets in caller order (tests).  prof
+ * (optional, nranks x 6 x 2 doubles): per rank and step (classify, pack, forward, scale,
+ * inverse, finish) the step's time with the rank alone on the device (ms) and the bytes
+ * it sends to other ranks -- the per-rank work of a multi-GPU run, measured on one GPU */
 fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* ctx, int nranks, const fse_config* cfg,
                                            int kind, const double* d_pos, const double* d_str,
                                            int64_t n, const double* d_tgt, int64_t nt, int tas,
-                                           const fse_green* green, double* d_u);
+                                           const fse_green* green, double* d_u, double* prof);
 
 /* measured FP64 DFMA throughput of this device (TFLOP/s): roofline denominator */
 fse_status fse_cuda_fp64_peak(fse_cuda_ctx* ctx, double* tflops);

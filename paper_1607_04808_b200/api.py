@@ -278,7 +278,7 @@ def _load():
                                                 i64, vp, i64, C.c_int, vp, vp]
         lib.fse_cuda_dist_virtual_total_sum.argtypes = [vp, C.c_int, C.POINTER(EwaldConfig),
                                                         C.c_int, vp, vp, i64, vp, i64, C.c_int,
-                                                        vp, vp]
+                                                        vp, vp, vp]
         lib.fse_cuda_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
         lib.fse_cuda_multi_destroy.argtypes = [vp]
         lib.fse_cuda_multi_last_error.restype = C.c_char_p
@@ -650,10 +650,12 @@ class Context:
 
     # -- partitioned multi-GPU evaluation (fse_dist)
     def dist_virtual_total_sum(self, system: SourceSystem, kind, cfg, targets, green, nranks,
-                               targets_are_sources=False):
+                               targets_are_sources=False, profile=None):
         """The partitioned algorithm (ownership, ghost exchange, distributed FFT,
         partial-sum return) with `nranks` virtual ranks on this device; u in
-        caller order."""
+        caller order.  profile: optional (nranks, 6, 2) float64 array receiving
+        per rank and step (classify, pack, forward, scale, inverse, finish) the
+        step time in ms with the rank alone on the device and the bytes sent."""
         t = system.positions if targets_are_sources else _f64(targets, (-1, 3))
         n, nt = system.size(), t.shape[0]
         ptrs = []
@@ -670,7 +672,8 @@ class Context:
             ptrs.append(du)
             self._call(_load().fse_cuda_dist_virtual_total_sum, int(nranks), C.byref(cfg),
                        int(kind), C.c_void_p(dp), C.c_void_p(ds), n, C.c_void_p(dt), nt,
-                       int(bool(targets_are_sources)), green.handle, C.c_void_p(du))
+                       int(bool(targets_are_sources)), green.handle, C.c_void_p(du),
+                       profile.ctypes.data_as(C.c_void_p) if profile is not None else None)
             u = np.empty((nt, 3))
             if nt:
                 self.memcpy(u.ctypes.data, du, u.nbytes)

@@ -560,7 +560,7 @@ fse_status fse_cuda_dist_total_sum(fse_dist* D, const fse_config* cfg, int kind,
 fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fse_config* cfg,
                                            int kind, const double* d_pos, const double* d_str,
                                            int64_t n, const double* d_tgt, int64_t nt, int tas,
-                                           const fse_green* green, double* d_u) {
+                                           const fse_green* green, double* d_u, double* prof) {
     return api(c, [&] {
         check_kind(kind);
         check_cfg(cfg);
@@ -603,13 +603,33 @@ fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fs
             ranks[r]->setup(cfg, kind, dp, ds, static_cast<int64_t>(own_s[r].size()), n, dt,
                             static_cast<int64_t>(own_t[r].size()), tas != 0);
         }
+        // prof (optional): per rank and step (classify, pack, forward, scale,
+        // inverse, finish) the step's time on the device (ms, the rank running
+        // alone) and the bytes it sends to other ranks: [r][step][time, bytes]
+        int step_no = 0;
+        auto record = [&](int r, int stp, double ms, double bytes) {
+            if (prof) {
+                prof[(r * 6 + stp) * 2] = ms;
+                prof[(r * 6 + stp) * 2 + 1] = bytes;
+            }
+        };
         auto step_all = [&](const std::function<Step(Rank&)>& f) {
             std::vector<Step> st;
             for (int r = 0; r < G; ++r) {
+                FSE_CU(cudaDeviceSynchronize());
+                const auto t0 = std::chrono::steady_clock::now();
                 st.push_back(f(*ranks[r]));
                 FSE_CU(cudaDeviceSynchronize());
+                const double ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                        .count();
+                double bytes = 0;
+                for (const Msg& m : st.back().sends)
+                    if (m.peer != r) bytes += static_cast<double>(m.bytes);
+                record(r, step_no, ms, bytes);
             }
             run_loopback(st, c->s0);
+            ++step_no;
         };
         step_all([](Rank& R) { return R.classify(); });
         step_all([](Rank& R) { return R.pack(); });
@@ -618,7 +638,13 @@ fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fs
         step_all([](Rank& R) { return R.inverse(); });
         std::vector<double> hu(3 * nt);
         for (int r = 0; r < G; ++r) {
+            FSE_CU(cudaDeviceSynchronize());
+            const auto t0 = std::chrono::steady_clock::now();
             ranks[r]->finish(out_u[r]->ptr<double>());
+            record(r, 5,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count(),
+                   0.0);
             std::vector<double> ur(3 * own_t[r].size());
             if (!ur.empty()) d2h(c, ur.data(), out_u[r]->ptr<double>(), sizeof(double) * ur.size());
             for (size_t j = 0; j < own_t[r].size(); ++j)
