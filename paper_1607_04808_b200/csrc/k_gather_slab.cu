@@ -292,10 +292,52 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// MMAs of one slab for the n-tiles [LO, HI] (compile-time, so the
+// accumulators stay in registers and no MMA is predicated)
+template <int LO, int HI, int MT, int NT, int KS>
+__device__ __forceinline__ void slab_mmas(double (&C)[MT][NT][2], const double* A,
+                                          const double* b0s, const double (&wxt)[NT], int lane) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        double bs[NT];
+#pragma unroll
+        for (int nt = LO; nt <= HI; ++nt) bs[nt] = b0s[(ks * 4 + nt) * 32 + lane] * wxt[nt];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const double a = A[8 * mt * RS + 4 * ks];
+#pragma unroll
+            for (int nt = LO; nt <= HI; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], a, bs[nt]);
+        }
+    }
+}
+
+// dispatch the run-time n-tile range [lo, hi] (0 <= lo <= hi < NT) to slab_mmas
+template <int LO, int HI, int MT, int NT, int KS>
+__device__ __forceinline__ void slab_mmas_rt(int lo, int hi, double (&C)[MT][NT][2],
+                                             const double* A, const double* b0s,
+                                             const double (&wxt)[NT], int lane) {
+    if constexpr (LO < NT) {
+        if (lo == LO) {
+            if constexpr (HI < NT) {
+                if (hi == HI) {
+                    slab_mmas<LO, HI, MT, NT, KS>(C, A, b0s, wxt, lane);
+                    return;
+                }
+                slab_mmas_rt<LO, HI + 1, MT, NT, KS>(lo, hi, C, A, b0s, wxt, lane);
+            }
+            return;
+        }
+        slab_mmas_rt<LO + 1, LO + 1, MT, NT, KS>(lo, hi, C, A, b0s, wxt, lane);
+    }
+}
+
+// xr[nt] = (first, last + P) plane range of n-tile nt's x supports (targets
+// sorted by x start, so the tiles active on one plane are a contiguous range
+// [lo, hi]); planes outside every tile's range are not loaded at all
 template <int MT, int NT, int KS>
 __device__ void gather_item_tma(const GridParams& g, const CUtensorMap* map, double* slab,
                                 uint64_t* bars, const double* b0s, const double* wxs, int x0,
-                                int y0, int z0, int NX, double* red) {
+                                int y0, int z0, int NX, const int2* xr, double* red) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rows_pad = 8 * MT * SW;
     const int buf_elems = rows_pad * RS;
@@ -307,7 +349,15 @@ __device__ void gather_item_tma(const GridParams& g, const CUtensorMap* map, dou
         for (int nt = 0; nt < NT; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
     const int rbase = 8 * MT * warp + (lane >> 2);
     const int tb = lane >> 2;
-    const int xs0 = max(0, g.x_lo - x0), xs1 = min(NX, g.x_lo + g.nx - x0);
+    int xlo[NT], xhi[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int2 r = xr[nt];
+        xlo[nt] = r.x;
+        xhi[nt] = r.y;
+    }
+    const int xs0 = max(max(0, g.x_lo - x0), xlo[0]);
+    const int xs1 = min(min(NX, g.x_lo + g.nx - x0), xhi[NT - 1]);
     auto issue = [&](int xs) {  // one thread: slab xs -> buffer (xs - xs0) & 1
         const int b = (xs - xs0) & 1;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -318,23 +368,19 @@ __device__ void gather_item_tma(const GridParams& g, const CUtensorMap* map, dou
     for (int xs = xs0; xs < xs1; ++xs) {
         const int i = xs - xs0;
         if (threadIdx.x == 0 && xs + 1 < xs1) issue(xs + 1);
+        // n-tiles whose supports contain plane xs (warp-uniform)
+        int lo = 0, hi = NT - 1;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            if (xhi[nt] <= xs) lo = nt + 1;
+            if (xlo[NT - 1 - nt] > xs) hi = NT - 2 - nt;
+        }
         mbar_wait(bars + (i & 1), (i >> 1) & 1);
         const double* A = slab + (i & 1) * buf_elems + rbase * RS + (lane & 3);
         double wxt[NT];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) wxt[nt] = wxs[xs * MAXT + 8 * nt + tb];
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-            double bs[NT];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) bs[nt] = b0s[(ks * 4 + nt) * 32 + lane] * wxt[nt];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const double a = A[8 * mt * RS + 4 * ks];
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], a, bs[nt]);
-            }
-        }
+        if (lo <= hi) slab_mmas_rt<0, 0, MT, NT, KS>(lo, hi, C, A, b0s, wxt, lane);
         __syncthreads();  // everyone is done with this buffer before it is refilled
     }
     const int tc = 2 * (lane & 3);
@@ -363,6 +409,7 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
     double* b0s = wxs + 32 * MAXT;         // [KS][4][32] B fragments (wz)
     int4* tinfo = reinterpret_cast<int4*>(b0s + KS * 4 * 32);
     uint64_t* bars = reinterpret_cast<uint64_t*>(tinfo + MAXT);
+    int2* xr = reinterpret_cast<int2*>(bars + 2);  // per n-tile plane range
     const int e = items[2 * blockIdx.x], bi = items[2 * blockIdx.x + 1];
     const int c = e >> 1, h = e & 1;
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
@@ -378,12 +425,31 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (tid < MAXT) {
+        // the item's targets in x-start order (stable counting sort over the
+        // 8 starts of the block, one ballot per start), so that each n-tile of
+        // 8 targets spans few x starts and skips the planes outside its supports
         int4 ti = make_int4(0, 0, 0, 0);
+        int key = 8;  // idle slots sort last
         if (tid < n) {
             const int q = first + tid;
             ti = make_int4(q, i0s[3 * q], i0s[3 * q + 1], i0s[3 * q + 2]);
+            key = ti.y - x0;
         }
-        tinfo[tid] = ti;
+        int pos = 0, base = 0;
+#pragma unroll
+        for (int v = 0; v <= 8; ++v) {
+            const unsigned bv = __ballot_sync(0xffffffffu, key == v);
+            if (key == v) pos = base + __popc(bv & ((1u << tid) - 1u));
+            base += __popc(bv);
+        }
+        tinfo[pos] = ti;
+        __syncwarp();
+        // plane range [first start, last start + P) of n-tile tid (slab index)
+        if (tid < 4) {
+            const int t0 = 8 * tid, t1 = min(8 * tid + 7, n - 1);
+            xr[tid] = t0 < n ? make_int2(tinfo[t0].y - x0, tinfo[t1].y - x0 + P)
+                             : make_int2(0, 0);
+        }
     }
     // pad rows (>= 3 NYB) of both buffers stay zero; the boxes never write them
     for (int idx = tid; idx < 2 * ROWS * RS; idx += SW * 32) {
@@ -412,13 +478,13 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
     double* red = slab;  // reused after the last slab (ROWS x MAXT <= 2 ROWS RS)
     const int nt = (n + 7) / 8;
     if (nt <= 1)
-        gather_item_tma<MT, 1, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+        gather_item_tma<MT, 1, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, xr, red);
     else if (nt == 2)
-        gather_item_tma<MT, 2, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+        gather_item_tma<MT, 2, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, xr, red);
     else if (nt == 3)
-        gather_item_tma<MT, 3, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+        gather_item_tma<MT, 3, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, xr, red);
     else
-        gather_item_tma<MT, 4, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, red);
+        gather_item_tma<MT, 4, KS>(g, &map, slab, bars, b0s, wxs, x0, y0, z0, NX, xr, red);
     __syncthreads();
     // u_t[c] = h^3 sum_y wy_t[y] red[(c, y)][t]   (rows at the fixed pitch NYB)
     if (tid < 3 * MAXT) {
@@ -429,7 +495,7 @@ __global__ void __launch_bounds__(SW * 32, 3) k_gather_tma(
             const int yo = ti.z - y0;
             double s = 0.0;
             for (int p = 0; p < P; ++p) s = fma(wy[p], red[(cc * NYB + yo + p) * MAXT + t], s);
-            u[3 * static_cast<int64_t>(perm[first + t]) + cc] = scale * s;
+            u[3 * static_cast<int64_t>(perm[ti.x]) + cc] = scale * s;
         }
     }
 }
@@ -548,7 +614,7 @@ void launch_tma(const Launch& L, const CUtensorMap& map, const GridParams& g, co
     constexpr int ROWS = 8 * MT * SW;
     const size_t sm = sizeof(double) * (2 * static_cast<size_t>(ROWS) * RS + 32 * MAXT +
                                         KS * 4 * 32) +
-                      sizeof(int4) * MAXT + 2 * sizeof(uint64_t);
+                      sizeof(int4) * MAXT + 2 * sizeof(uint64_t) + 4 * sizeof(int2);
     FSE_CU(cudaFuncSetAttribute(k_gather_tma<MT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sm)));
     k_gather_tma<MT, KS><<<static_cast<unsigned>(max_items), SW * 32, sm, L.s>>>(

@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
                      zf2 = make_float2(zf, zf), neg1 = make_float2(-1.0f, -1.0f);
 #pragma unroll
         for (int wd = 0; wd < CH / 32; ++wd) {
-            uint32_t m = 0;
+            uint32_t m = 0, mx = 0;
 #pragma unroll 4
             for (int b = 0; b < 32; b += 2) {
                 const int j = wd * 32 + b;
@@ -393,13 +393,21 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const float d = h ? d2f.y : d2f.x;
-                    bool pass = d <= ft.lo && d > ft.z0;
-                    if (!pass && !(d > ft.hi)) {  // band, near-coincident or NaN: exact test
-                        const double d2 = exact_d2(x - sx[j + h], y - sy[j + h], z - sz[j + h]);
-                        pass = (d2 != 0.0) && !(d2 > rc2);  // realspace.cpp:140
-                    }
-                    m |= static_cast<uint32_t>(pass) << (b + h);
+                    const bool in = d <= ft.lo && d > ft.z0;
+                    // band, near-coincident or NaN: decided by the exact test below
+                    const bool ex = !in && !(d > ft.hi);
+                    m |= static_cast<uint32_t>(in) << (b + h);
+                    mx |= static_cast<uint32_t>(ex) << (b + h);
                 }
+            }
+            // the rare undecided candidates: the exact fp64 test of realspace.cpp:140
+            // (out of the per-candidate loop, so that loop has no branch)
+            while (mx) {
+                const int b = __ffs(mx) - 1;
+                mx &= mx - 1u;
+                const int j = wd * 32 + b;
+                const double d2 = exact_d2(x - sx[j], y - sy[j], z - sz[j]);
+                if ((d2 != 0.0) && !(d2 > rc2)) m |= 1u << b;
             }
             mask[wd] = m;
         }
