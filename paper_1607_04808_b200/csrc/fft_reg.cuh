@@ -334,6 +334,40 @@ __device__ __forceinline__ void pass1(double2* buf, int ncol, int sgn, const dou
     for (int k1 = 0; k1 < D1; ++k1) dst[k1 * (D2 + 1)] = v[k1];
 }
 
+// pass 1 as above, with mid() called by EVERY thread of the CTA between the
+// loads and the first use of the twiddle tables (e.g. the wait for their
+// asynchronous staging), so the loads' latency overlaps the staging's
+template <int D1, int D2, bool CF, int NZ1, class LOAD, class MID>
+__device__ __forceinline__ void pass1_mid(double2* buf, int ncol, int sgn, const double2* twD,
+                                          const double2* tab, LOAD load, MID mid) {
+    constexpr int D = D1 * D2;
+    int c = 0, n2 = 0;
+    const bool act = item1<D1, D2, CF>(ncol, c, n2);
+    double2 v[D1];
+    if (act) {
+#pragma unroll
+        for (int n1 = 0; n1 < D1; ++n1)
+            v[n1] = n1 < NZ1 ? load(c, n1 * D2 + n2) : make_double2(0.0, 0.0);
+    }
+    mid();
+    if (!act) return;
+    rfft<D1>(v, sgn, tab);
+    int t = 0;  // n2 * k1 mod D
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) {
+        if (k1 > 0) {
+            double2 w = twD[t];
+            if (sgn > 0) w.y = -w.y;
+            v[k1] = cmul(v[k1], w);
+        }
+        t += n2;
+        if (t >= D) t -= D;
+    }
+    double2* dst = buf + ridx<D1, D2>(c, n2);
+#pragma unroll
+    for (int k1 = 0; k1 < D1; ++k1) dst[k1 * (D2 + 1)] = v[k1];
+}
+
 // pass 1 in place on buf (loads ridx(c, n1 D2 + n2) of its own item, FFT_D1,
 // twiddle, stores the transpose over them; no barriers inside)
 template <int D1, int D2, bool CF>

@@ -380,6 +380,21 @@ __device__ __forceinline__ const double2* stage_twiddles(double2* a, const FftPl
     return t;
 }
 
+// the same table staged with cp.async and NOT waited for: the caller's first
+// global loads are issued before the wait (freg::pass1_mid + wait_staged)
+__device__ __forceinline__ const double2* stage_twiddles_async(double2* a, const FftPlan& pl,
+                                                               const double2* __restrict__ tw_g) {
+    double2* t = a + pl.buf_elems * (pl.two_bufs ? 2 : 1);
+    for (int e = threadIdx.x; e < pl.tw_elems; e += blockDim.x) cp16(t + e, tw_g + e);
+    return t;
+}
+struct WaitStaged {
+    __device__ __forceinline__ void operator()() const {
+        cp_wait_all();
+        __syncthreads();
+    }
+};
+
 // CTA size per engine.  1200 = 30 x 40 (engine 2): a 40-point register DFT
 // needs more than the 128 registers per thread that 256-thread CTAs at two
 // per SM allow (it spilled ~1 KB per thread), so its CTAs have 128 threads
@@ -418,7 +433,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd(Ff
                                                  double2* __restrict__ B) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
     const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
@@ -477,7 +492,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass(F
                                                   double2* __restrict__ Cb, BlockDest dst) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1;
     const int ntz = (Dh + ncol - 1) / ncol;
     const int ci = blockIdx.x / ntz;  // comp * nx + i (slab-local plane i)
@@ -619,7 +634,7 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Mt = g.Mt;
     const int ntz = (Dh + ncol - 1) / ncol;
     const int kyl = blockIdx.x / ntz;  // row of this rank's ky block
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv(Ff
                                                  double* __restrict__ W) {
     double2* a = reinterpret_cast<double2*>(fse_smem);
     double2* sb = a + pl.buf_elems;
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const int D = pl.D, Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
     const int64_t q0 = static_cast<int64_t>(blockIdx.x) * ncol;
@@ -741,6 +756,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv(Ff
         a[cidx<ENG>(c, k, D)] = make_double2(x0.x - x1.y, x0.y + x1.x);
         if (k != 0 && k != D / 2) a[cidx<ENG>(c, D - k, D)] = make_double2(x0.x + x1.y, -x0.y + x1.x);
     }
+    cp_wait_all();  // the twiddles (staged asynchronously)
     __syncthreads();
     double2* r = fft_cols<ENG>(a, sb, nc, pl, tw, +1);
     for (int c = 0; c < nc; ++c) {
@@ -770,7 +786,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(F
                                                   double2* __restrict__ B) {
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const double2* tab = tw + D;
     const int Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
@@ -791,7 +807,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(F
         has1[threadIdx.x] = (2 * jp + 1 < Mt);
     }
     __syncthreads();
-    freg::pass1<D1, D2, false, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
+    freg::pass1_mid<D1, D2, false, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
         double2 z = make_double2(0.0, 0.0);
         if (n < Mt) {
             const double* row = R + row0[c];
@@ -799,7 +815,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(F
             if (has1[c]) z.y = __ldg(row + Mt + n);
         }
         return z;
-    });
+    }, WaitStaged{});
     __syncthreads();
     freg::pass2_smem<D1, D2, false>(a, nc, -1, tab);
     __syncthreads();
@@ -824,7 +840,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(
                                                    double2* __restrict__ Cb, BlockDest dst) {
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    const double2* tw = stage_twiddles_async(a, pl, tw_g);
     const double2* tab = tw + D;
     const int Dh = D / 2 + 1;
     const int ntz = (Dh + ncol - 1) / ncol;
@@ -843,9 +859,9 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(
         return static_cast<int64_t>(rbase + blk * bstep + ky) * Dh;
     };
     if (!INV) {
-        freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
+        freg::pass1_mid<D1, D2, true, (D1 + 1) / 2>(a, nc, -1, tw, tab, [&](int c, int n) {
             return n < Mt ? Bp[static_cast<int64_t>(n) * Dh + c] : make_double2(0.0, 0.0);
-        });
+        }, WaitStaged{});
         __syncthreads();
         // block k / nkys goes to its ky owner
         const int rb = (comp * nxs + xl) * nkys;
@@ -854,8 +870,8 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(
             block_ptr(dst, blk)[static_cast<int64_t>(rb + k - blk * nkys) * Dh + kz0 + c] = v;
         });
     } else {
-        freg::pass1<D1, D2, true, D1>(a, nc, +1, tw, tab,
-                                      [&](int c, int n) { return Ck[crow(n) + c]; });
+        freg::pass1_mid<D1, D2, true, D1>(a, nc, +1, tw, tab,
+                                      [&](int c, int n) { return Ck[crow(n) + c]; }, WaitStaged{});
         __syncthreads();
         freg::pass2<D1, D2, true, D2 / 2>(a, nc, +1, tab, [&](int c, int k, double2 v) {
             Bp[static_cast<int64_t>(k) * Dh + c] = v;  // k < Mt by NOUT2
@@ -864,6 +880,14 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(
 }
 
 // x pass + multiplier: columns (comp, kz0 + c), c-fastest
+// multiplier elements per thread of the v2 x pass: nc <= T / (A max(D1, D2))
+// columns per CTA (one pass item per thread), so nc D / T <= min(D1, D2) / A
+template <int ENG, int KIND>
+constexpr int xs_ng() {
+    constexpr int mn = Eng<ENG>::D1 < Eng<ENG>::D2 ? Eng<ENG>::D1 : Eng<ENG>::D2;
+    return (mn + arity_k<KIND>() - 1) / arity_k<KIND>();
+}
+
 template <int ENG, int KIND>
 __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>()) k_xscale2(FftPlan pl, const double2* __restrict__ tw_g,
                                                     GridParams g, int ncol,
@@ -873,7 +897,11 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
     constexpr int A = arity_k<KIND>(), NO = nout_k<KIND>();
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    // twiddles and the exp factor table are staged asynchronously (cp.async),
+    // in flight together with pass 1's input loads
+    double2* twm = a + pl.buf_elems * (pl.two_bufs ? 2 : 1);
+    for (int e = threadIdx.x; e < pl.tw_elems; e += blockDim.x) cp16(twm + e, tw_g + e);
+    const double2* tw = twm;
     const double2* tab = tw + D;
     const int Dh = D / 2 + 1, Mt = g.Mt;
     const int ntz = (Dh + ncol - 1) / ncol;
@@ -896,27 +924,52 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
     // per-axis factors of exp(-(1 - eta) k^2 / (4 xi^2)) (k_ex_axis, once per
     // call): rem = ex[kx] * ex[ky] * ex[kz]
     double* ex = reinterpret_cast<double*>(const_cast<double2*>(tab) + pl.tw_elems - D);
-    for (int q = threadIdx.x; q < D; q += blockDim.x) ex[q] = __ldg(ex_g + q);
+    for (int q = threadIdx.x; q < D; q += blockDim.x) cp8(ex + q, ex_g + q);
     // forward x-FFT of the A components (pass 1 straight from global memory)
-    freg::pass1<D1, D2, true, (D1 + 1) / 2>(a, A * nc, -1, tw, tab, [&](int col, int n) {
-        const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
-        return n < Mt ? *at(comp, n, c) : make_double2(0.0, 0.0);
-    });
+    freg::pass1_mid<D1, D2, true, (D1 + 1) / 2>(
+        a, A * nc, -1, tw, tab,
+        [&](int col, int n) {
+            const int comp = static_cast<int>(fdiv(col, fnc)), c = col - comp * nc;
+            return n < Mt ? *at(comp, n, c) : make_double2(0.0, 0.0);
+        },
+        [] {
+            cp_wait_all();
+            __syncthreads();
+        });
     __syncthreads();
     freg::pass2_smem<D1, D2, true>(a, A * nc, -1, tab);
+    // the multiplier's Green's values, all in flight at once (one latency per
+    // CTA instead of one per element), issued before the barrier
+    constexpr int NG = xs_ng<ENG, KIND>();
+    double gv[NG];
+    {
+        const double* Gk = G + static_cast<int64_t>(ky) * Dh + kz0;
+#pragma unroll
+        for (int m = 0; m < NG; ++m) {
+            const int e = threadIdx.x + m * static_cast<int>(blockDim.x);
+            gv[m] = 0.0;
+            if (e < nc * D) {
+                const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
+                gv[m] = __ldg(Gk + static_cast<int64_t>(kx) * D * Dh + c);
+            }
+        }
+    }
     __syncthreads();
     // pointwise multiplier (ewald.cpp:216-293) with the Nyquist-exact
     // Hermitian average (see k_kscale.cu), 1/D^3 folded in
     const int half = D / 2;
     const double ex_y = ex[ky];
-    for (int e = threadIdx.x; e < nc * D; e += blockDim.x) {
+#pragma unroll
+    for (int m = 0; m < NG; ++m) {
+        const int e = threadIdx.x + m * static_cast<int>(blockDim.x);
+        if (e >= nc * D) break;
         const int kx = static_cast<int>(fdiv(e, fnc)), c = e - kx * nc;
         const int kz = kz0 + c;
         double k[3] = {kax(kx, D, g.dk), kax(ky, D, g.dk), kax(kz, D, g.dk)};
         const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(k[0], k[0]), __dmul_rn(k[1], k[1])),
                                     __dmul_rn(k[2], k[2]));
         const double rem = ex[kx] * ex_y * ex[kz];
-        const double gval = __ldg(G + (static_cast<int64_t>(kx) * D + ky) * Dh + kz);
+        const double gval = gv[m];
         double2 gh[A];
 #pragma unroll
         for (int q = 0; q < A; ++q) gh[q] = a[freg::ridx<D1, D2>(q * nc + c, kx)];
@@ -959,7 +1012,8 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv2(F
                                                   double* __restrict__ W) {
     constexpr int D1 = Eng<ENG>::D1, D2 = Eng<ENG>::D2, D = D1 * D2;
     double2* a = reinterpret_cast<double2*>(fse_smem);
-    const double2* tw = stage_twiddles(a, pl, tw_g);
+    // (624 = 24 x 26: the overlapped staging spills; staged up front there)
+    const double2* tw = ENG == 1 ? stage_twiddles(a, pl, tw_g) : stage_twiddles_async(a, pl, tw_g);
     const double2* tab = tw + D;
     const int Dh = D / 2 + 1, Jp = (Mt + 1) / 2;
     const int64_t npairs = static_cast<int64_t>(ncomp) * nx * Jp;
@@ -979,7 +1033,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv2(F
         has1[threadIdx.x] = (2 * jp + 1 < Mt);
     }
     __syncthreads();
-    freg::pass1<D1, D2, false, D1>(a, nc, +1, tw, tab, [&](int c, int n) {
+    freg::pass1_mid<D1, D2, false, D1>(a, nc, +1, tw, tab, [&](int c, int n) {
         // Z[n] = X0 + i X1 (n <= D/2); conj(X0[D-n]) + i conj(X1[D-n]) above
         const bool lo = n <= D / 2;
         const int k = lo ? n : D - n;
@@ -992,6 +1046,8 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv2(F
         }
         return lo ? make_double2(x0.x - x1.y, x0.y + x1.x)
                   : make_double2(x0.x + x1.y, -x0.y + x1.x);
+    }, [] {
+        if (ENG != 1) WaitStaged{}();
     });
     __syncthreads();
     freg::pass2<D1, D2, false, D2 / 2>(a, nc, +1, tab, [&](int c, int n, double2 v) {
@@ -1414,6 +1470,15 @@ void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_t
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) if (v2_mask_for<EV>() & 4) {
+            {
+                const int thr = xs_threads<EV, FSE_STOKESLET>();
+                const int ng = kind == FSE_STRESSLET ? xs_ng<EV, FSE_STRESSLET>()
+                             : kind == KIND_SCALAR ? xs_ng<EV, KIND_SCALAR>()
+                                                   : xs_ng<EV, FSE_STOKESLET>();
+                const int thr2 = kind == FSE_STRESSLET ? xs_threads<EV, FSE_STRESSLET>() : thr;
+                if (u * D > ng * thr2)
+                    throw Error(FSE_EINVAL, "x pass: multiplier elements exceed the per-thread batch");
+            }
             if (kind == FSE_STOKESLET) {
                 allow_smem(k_xscale2<EV, FSE_STOKESLET>, sm);
                 k_xscale2<EV, FSE_STOKESLET><<<blocks, xs_threads<EV, FSE_STOKESLET>(), sm, L.s>>>(p, d_tw, g, u, G, C, dst, d_ex);
