@@ -19,6 +19,7 @@
 //
 // Roofline: FP64 FMA (2 a P^3 flops per point, ~100 flop/B); HBM traffic is
 // the weights (3P doubles per point) plus one write of the grid.
+#include <cstdlib>
 #include <type_traits>
 
 #include "fse_internal.cuh"
@@ -47,7 +48,10 @@ constexpr int XS = NWARP / 2, XW = TX / XS;  // x splits, x-rows per warp
 // element-major staging ([element][point], point stride CHP = CH + 4): the
 // per-thread staging writes of a warp are consecutive doubles and the MMA
 // fragment reads (4 points x 8 rows) spread over all banks
-constexpr int CHP = CH + 4;
+#ifndef FSE_SPREAD_PAD
+#define FSE_SPREAD_PAD 4
+#endif
+constexpr int CHP = CH + FSE_SPREAD_PAD;
 struct Stage {
     // wx and f are read 4 consecutive points of one row at a time (no
     // conflicts unpadded); wy and wz rows are read 8 at a time (padded).
@@ -263,6 +267,236 @@ __global__ void __launch_bounds__(NWARP * 32, FSE_SPREAD_MINB) k_spread(GridPara
     }
 }
 
+// ---------------------------------------------------------------- warp-specialized
+// Same tile, warp domains, staging layout and MMAs as k_spread, but the chunk
+// staging is done by a dedicated producer warp into a ring of NSTG stages
+// handed over with mbarriers (full: the stage's copies have landed; empty:
+// all four MMA warps are done with it), so the MMA warps never wait for each
+// other at a CTA barrier (k_spread's per-chunk __syncthreads was ~24 % of its
+// stall samples: the warps' skip patterns make their chunk times differ).
+#ifndef FSE_SPREAD_NSTG
+#define FSE_SPREAD_NSTG 3
+#endif
+constexpr int NSTG = FSE_SPREAD_NSTG;
+struct StageW {
+    Stage st;
+    int total;  // kept points in the stage; -1: no more chunks
+};
+
+__device__ __forceinline__ unsigned su32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+    }
+}
+
+#ifndef FSE_SPREAD_WS_MINB
+#define FSE_SPREAD_WS_MINB 4
+#endif
+__global__ void __launch_bounds__((NWARP + 1) * 32, FSE_SPREAD_WS_MINB) k_spread_ws(
+    GridParams g, const int32_t* __restrict__ i0s, const double* __restrict__ w,
+    const double* __restrict__ fs, int a, int c0, const int32_t* __restrict__ tstart,
+    double* __restrict__ X) {
+    extern __shared__ __align__(16) unsigned char spw_smem[];
+    StageW* ring = reinterpret_cast<StageW*>(spw_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NSTG);
+    uint64_t* empty = full + NSTG;
+    const int P = g.P;
+    const int tile = blockIdx.x;
+    const int tz = tile % g.ncz;
+    const int ty = (tile / g.ncz) % g.ncy;
+    const int tx = g.x_lo / TX + tile / (g.ncz * g.ncy);
+    const int x0n = tx * TX, y0n = ty * TY, z0n = tz * TZ;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int b = 0; b < NSTG; ++b) {
+            mb_init(full + b, 33);
+            mb_init(empty + b, NWARP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();  // the only CTA-wide barrier
+
+    if (warp == NWARP) {
+        // ---------------- producer: stream the points whose support meets the tile
+        const int ix_lo = x0n - P + 1, iy_lo = y0n - P + 1, iz_lo = z0n - P + 1;
+        const int kx_lo = ix_lo < 0 ? 0 : (ix_lo >> 3);
+        const int ky_lo = iy_lo < 0 ? 0 : (iy_lo >> 3);
+        const int kz_lo = iz_lo < 0 ? 0 : (iz_lo >> 4);
+        auto range = [&](Cursor& c) {
+            const int64_t kb = (static_cast<int64_t>(c.kx) * g.ncy + c.ky) * g.ncz;
+            c.base = tstart[(kb + kz_lo) * 8];
+            c.qend = tstart[(kb + tz) * 8 + 8];
+        };
+        auto next_nonempty = [&](Cursor& c) {
+            while (c.kx <= tx && c.base >= c.qend) {
+                if (++c.ky > ty) {
+                    c.ky = ky_lo;
+                    ++c.kx;
+                }
+                if (c.kx <= tx) range(c);
+            }
+        };
+        Cursor cur;
+        cur.kx = kx_lo;
+        cur.ky = ky_lo;
+        range(cur);
+        next_nonempty(cur);
+        int k = 0;
+        for (;; ++k) {
+            const int b = k % NSTG;
+            if (k >= NSTG) mb_wait(empty + b, ((k / NSTG) - 1) & 1);
+            StageW& S = ring[b];
+            const bool more = cur.kx <= tx;
+            int total = -1;
+            if (more) {
+                // CH candidates, CH / 32 per lane; kept ones compacted in order
+                int off = 0;
+#pragma unroll
+                for (int h = 0; h < CH / 32; ++h) {
+                    const int q = cur.base + h * 32 + lane;
+                    int ix = 0, iy = 0, iz = 0;
+                    bool keep = false;
+                    if (q < cur.qend) {
+                        ix = i0s[3 * q];
+                        iy = i0s[3 * q + 1];
+                        iz = i0s[3 * q + 2];
+                        keep = ix >= ix_lo && ix <= x0n + TX - 1 && iy >= iy_lo &&
+                               iy <= y0n + TY - 1 && iz >= iz_lo && iz <= z0n + TZ - 1;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        const int slot = off + __popc(bal & ((1u << lane) - 1u));
+                        const double* wq = w + static_cast<int64_t>(q) * 3 * P;
+#pragma unroll
+                        for (int r = 0; r < TX; ++r) {
+                            const int p = x0n + r - ix;
+                            const bool in = p >= 0 && p < P;
+                            cpa8(&S.st.wx[r][slot], in ? wq + p : wq, in ? 8 : 0);
+                        }
+#pragma unroll
+                        for (int r = 0; r < TY; ++r) {
+                            const int p = y0n + r - iy;
+                            const bool in = p >= 0 && p < P;
+                            cpa8(&S.st.wy[r][slot], in ? wq + P + p : wq, in ? 8 : 0);
+                        }
+#pragma unroll
+                        for (int r = 0; r < TZ; ++r) {
+                            const int p = z0n + r - iz;
+                            const bool in = p >= 0 && p < P;
+                            cpa8(&S.st.wz[r][slot], in ? wq + 2 * P + p : wq, in ? 8 : 0);
+                        }
+                        const double* fq = fs + static_cast<int64_t>(q) * a + c0;
+                        cpa8(&S.st.f[0][slot], fq, 8);
+                        cpa8(&S.st.f[1][slot], fq + 1, 8);
+                        cpa8(&S.st.f[2][slot], fq + 2, 8);
+                        uint32_t zb = 0;
+#pragma unroll
+                        for (int ww = 0; ww < NWARP; ++ww) {
+                            const int xa = x0n + (ww % XS) * XW, za = z0n + (ww / XS) * 8;
+                            const bool in = !(ix > xa + XW - 1 || ix + P <= xa) &&
+                                            !(iz > za + 7 || iz + P <= za);
+                            zb |= static_cast<uint32_t>(in) << ww;
+                        }
+                        reinterpret_cast<uint8_t*>(S.st.zm4)[slot] = static_cast<uint8_t>(zb);
+                    }
+                    off += __popc(bal);
+                }
+                total = off;
+                cur.base += CH;
+                next_nonempty(cur);
+            }
+            if (lane == 0) S.total = total;
+            // full[b] completes when every lane's copies have landed (32
+            // asynchronous arrives) and lane 0 has released the metadata
+            // (total, zm) the warp wrote: the producer goes straight on to
+            // the next chunk instead of waiting for the copies
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(full + b))
+                         : "memory");
+            __syncwarp();
+            if (lane == 0) mb_arrive(full + b);
+            if (!more) break;
+        }
+        return;
+    }
+
+    // ---------------- MMA warps (warp w owns x-rows [wx_off, +XW), z [wz_off, +8))
+    const int wx_off = (warp % XS) * XW;
+    const int wz_off = (warp / XS) * 8;
+    const int wz_lo = z0n + wz_off;
+    double C[XW][3][2];
+#pragma unroll
+    for (int r = 0; r < XW; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) C[r][c][0] = C[r][c][1] = 0.0;
+    for (int k = 0;; ++k) {
+        const int b = k % NSTG;
+        mb_wait(full + b, (k / NSTG) & 1);
+        const StageW& SW = ring[b];
+        const int total = SW.total;
+        if (total < 0) break;
+        const Stage& S = SW.st;
+        auto group = [&](int p0, auto fullg) {
+            constexpr bool FULL = decltype(fullg)::value;
+            uint32_t zm = S.zm4[p0 >> 2] & (0x01010101u << warp);
+            if (!FULL) zm &= (1u << (8 * (total - p0))) - 1u;
+            if (zm == 0u) return;
+            const int p = p0 + (lane & 3);
+            const bool pv = FULL || p < total;
+            const int pp = pv ? p : p0;
+            const double wyv = pv ? S.wy[lane >> 2][pp] : 0.0;
+            const double wzv = pv ? S.wz[wz_off + (lane >> 2)][pp] : 0.0;
+            const double bf[3] = {S.f[0][pp] * wzv, S.f[1][pp] * wzv, S.f[2][pp] * wzv};
+#pragma unroll
+            for (int r = 0; r < XW; ++r) {
+                const double ar = S.wx[wx_off + r][pp] * wyv;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) dmma(C[r][c][0], C[r][c][1], ar, bf[c]);
+            }
+        };
+        int p0 = 0;
+        for (; p0 + 4 <= total; p0 += 4) group(p0, std::true_type{});
+        if (p0 < total) group(p0, std::false_type{});
+        __syncwarp();
+        if (lane == 0) mb_arrive(empty + b);
+    }
+
+    const int y = y0n + (lane >> 2), z = wz_lo + 2 * (lane & 3);
+    if (y >= g.Mt || z >= g.Mt) return;
+    const bool z1 = z + 1 < g.Mt;
+    const bool vec = z1 && (g.Mt % 2 == 0);
+#pragma unroll
+    for (int r = 0; r < XW; ++r) {
+        const int x = x0n + wx_off + r;
+        if (x >= g.x_lo + g.nx) break;
+        const int64_t off = (x - g.x_lo) * g.plane + y * g.rowp + z;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double* dst = X + (c0 + c) * g.comp + off;
+            if (vec) {
+                *reinterpret_cast<double2*>(dst) = make_double2(C[r][c][0], C[r][c][1]);
+            } else {
+                dst[0] = C[r][c][0];
+                if (z1) dst[1] = C[r][c][1];
+            }
+        }
+    }
+}
+
 __global__ void k_extract(GridParams g, const double* __restrict__ X, int a,
                           double* __restrict__ out) {
     const int64_t vol = static_cast<int64_t>(g.Mt) * g.Mt * g.Mt;
@@ -281,7 +515,22 @@ void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, con
     (void)n;
     const unsigned tiles = static_cast<unsigned>((g.nx + TX - 1) / TX) * g.ncy * g.ncz;
     if (tiles == 0) return;
-    k_spread<<<tiles, NWARP * 32, 0, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
+    static const int ws = [] {
+        const char* e = std::getenv("FSE_SPREAD_WS");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (ws) {
+        const size_t sm = sizeof(StageW) * NSTG + 2 * NSTG * sizeof(uint64_t);
+        static bool attr = false;
+        if (!attr) {
+            FSE_CU(cudaFuncSetAttribute(k_spread_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+            attr = true;
+        }
+        k_spread_ws<<<tiles, (NWARP + 1) * 32, sm, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
+    } else {
+        k_spread<<<tiles, NWARP * 32, 0, L.s>>>(g, i0s, w, fs, a, c0, tstart, X);
+    }
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
