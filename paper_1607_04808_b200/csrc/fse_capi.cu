@@ -372,8 +372,6 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n);
     Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt);
     Launch L = L1(c);
-    int32_t* icnt = buf<int32_t>(c, "rs_icnt", cg.ncell + 1);
-    int32_t* ioff = buf<int32_t>(c, "rs_ioff", cg.ncell + 1);
     const int per = realspace_item_size();
     int64_t c_lo = 0, c_hi = -1;
     if (nparts > 1) {  // cells are (i dim + j) dim + k: x-slices are contiguous
@@ -382,16 +380,18 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
         c_hi = plane * (static_cast<int64_t>(cg.dim) * (part + 1) / nparts);
         if (nt > 0) FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
     }
-    launch_item_counts(L, tgt.start, cg.ncell, per, icnt, c_lo, c_hi);
-    exclusive_scan(c, c->s1, "s1", icnt, ioff, cg.ncell + 1);
     const int64_t max_items = std::min<int64_t>(cg.ncell, nt) + (nt + per - 1) / per;
     int32_t* items = buf<int32_t>(c, "rs_items", 2 * static_cast<size_t>(max_items));
-    launch_fill_items(L, tgt.start, ioff, cg.ncell, per, items);
+    uint8_t* bucket = buf<uint8_t>(c, "rs_bucket", cg.ncell);
+    int32_t* bwork = buf<int32_t>(c, "rs_bwork", 3 * realspace_work_buckets() + 1);
+    int32_t* nitems = bwork + 3 * realspace_work_buckets();
+    launch_realspace_items(L, src.start, tgt.start, cg.dim, cg.ncell, per, c_lo, c_hi, bucket,
+                           bwork, items, nitems);
     FSE_CU(cudaEventRecord(c->ev[EV_RPAIR], c->s1));
     FSE_CU(cudaMemsetAsync(c->d_counts, 0, 2 * sizeof(unsigned long long), c->s1));
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
-                         tgt.pz, tgt.start, items, max_items, ioff + cg.ncell, tgt.perm, xi, rc,
+                         tgt.pz, tgt.start, items, max_items, nitems, tgt.perm, xi, rc,
                          c->d_counts, d_uR);
     else if (nt > 0)
         FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));

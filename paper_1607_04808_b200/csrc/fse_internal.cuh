@@ -180,10 +180,12 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       double xi, double rc, unsigned long long* counts, double* uR);
 int realspace_item_size();  // targets per work item
 // items per cell; only cells in [c_lo, c_hi) get any (c_hi < 0: all cells)
-void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
-                        int32_t* cnt, int64_t c_lo = 0, int64_t c_hi = -1);
-void launch_fill_items(const Launch& L, const int32_t* start, const int32_t* off, int64_t ncell,
-                       int per, int32_t* items);
+// the pair kernel's work items (cell, 32-target chunk), heaviest cells first;
+// *nitems (device) = item count; bwork: 3 x realspace_work_buckets() ints
+int realspace_work_buckets();
+void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
+                            int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
+                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems);
 
 // epilogue: u[perm] = uF + uR (+ self) -------------------------------------
 // u = uF + uR (+ self_coef * f for the stokeslet self term), caller order

@@ -472,24 +472,68 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     }
 }
 
-// items of cell c: ceil(targets / per) for cells in [c_lo, c_hi), else none
-// (a slab rank's share of the real-space work: whole x-slices of cells, so
-// every item keeps its full warp of targets)
-__global__ void k_item_counts(const int32_t* __restrict__ start, int64_t ncell, int per,
-                              int64_t c_lo, int64_t c_hi, int32_t* __restrict__ cnt) {
+// Work items are scheduled heaviest cell first: the pair work of a cell is
+// (its targets) x (sources in its 27 neighbour buckets), which varies by two
+// orders of magnitude on clustered input (cfg4), and a heavy item dispatched
+// last leaves the GPU waiting on a few warps.  Cells go to 32 buckets by
+// log2(work) (bucket 0 heaviest); items are laid out bucket by bucket.  The
+// order inside a bucket comes from atomics and only affects scheduling:
+// every item computes the same targets' sums in the same order.
+constexpr int kWorkBuckets = 32;
+
+__global__ void k_cell_bucket(const int32_t* __restrict__ sstart, const int32_t* __restrict__ tstart,
+                              int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
+                              uint8_t* __restrict__ bucket, int32_t* __restrict__ bcount) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (c < ncell)
-        cnt[c] = (c >= c_lo && c < c_hi) ? (start[c + 1] - start[c] + per - 1) / per : 0;
-    if (c == ncell) cnt[c] = 0;
+    if (c >= ncell) return;
+    const int nt = tstart[c + 1] - tstart[c];
+    if (nt <= 0 || c < c_lo || c >= c_hi) return;
+    const int ck = static_cast<int>(c % dim), cj = static_cast<int>((c / dim) % dim),
+              ci = static_cast<int>(c / (static_cast<int64_t>(dim) * dim));
+    int64_t cand = 0;
+    for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int dk = -1; dk <= 1; ++dk) {
+                const int i = ci + di, j = cj + dj, k = ck + dk;
+                if (i < 0 || i >= dim || j < 0 || j >= dim || k < 0 || k >= dim) continue;
+                const int64_t b = (static_cast<int64_t>(i) * dim + j) * dim + k;
+                cand += sstart[b + 1] - sstart[b];
+            }
+    const unsigned long long work = static_cast<unsigned long long>(nt) * (cand + 1);
+    const int lg = 63 - __clzll(static_cast<long long>(work));  // floor(log2 work)
+    const int bk = max(0, kWorkBuckets - 1 - lg);
+    bucket[c] = static_cast<uint8_t>(bk);
+    atomicAdd(bcount + bk, (nt + per - 1) / per);
 }
 
-__global__ void k_fill_items(const int32_t* __restrict__ off, int64_t ncell,
+// one warp: bucket offsets (exclusive scan), item total for the pair kernel
+__global__ void k_bucket_scan(const int32_t* __restrict__ bcount, int32_t* __restrict__ boff,
+                              int32_t* __restrict__ nitems) {
+    const int l = threadIdx.x;
+    const int v = l < kWorkBuckets ? bcount[l] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += t;
+    }
+    if (l < kWorkBuckets) boff[l] = incl - v;
+    if (l == 31) *nitems = incl;
+}
+
+__global__ void k_fill_items(const int32_t* __restrict__ tstart, const uint8_t* __restrict__ bucket,
+                             int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
+                             const int32_t* __restrict__ boff, int32_t* __restrict__ bcur,
                              int32_t* __restrict__ items) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncell) return;
-    for (int32_t it = off[c]; it < off[c + 1]; ++it) {
-        items[2 * it] = static_cast<int32_t>(c);
-        items[2 * it + 1] = it - off[c];
+    const int nt = tstart[c + 1] - tstart[c];
+    if (nt <= 0 || c < c_lo || c >= c_hi) return;
+    const int n = (nt + per - 1) / per, bk = bucket[c];
+    const int32_t base = boff[bk] + atomicAdd(bcur + bk, n);
+    for (int s = 0; s < n; ++s) {
+        items[2 * (base + s)] = static_cast<int32_t>(c);
+        items[2 * (base + s) + 1] = s;
     }
 }
 
@@ -564,22 +608,31 @@ void ensure_tables() {
 
 int realspace_item_size() { return 32; }
 
-void launch_item_counts(const Launch& L, const int32_t* start, int64_t ncell, int per,
-                        int32_t* cnt, int64_t c_lo, int64_t c_hi) {
-    k_item_counts<<<static_cast<unsigned>((ncell + 256) / 256), 256, 0, L.s>>>(
-        start, ncell, per, c_lo, c_hi < 0 ? ncell : c_hi, cnt);
+void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
+                            int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
+                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems) {
+    if (c_hi < 0) c_hi = ncell;
+    int32_t* bcount = bwork;
+    int32_t* boff = bwork + kWorkBuckets;
+    int32_t* bcur = bwork + 2 * kWorkBuckets;
+    FSE_CU(cudaMemsetAsync(bwork, 0, 3 * kWorkBuckets * sizeof(int32_t), L.s));
+    const unsigned blocks = static_cast<unsigned>((ncell + 255) / 256);
+    if (blocks > 0) {
+        k_cell_bucket<<<blocks, 256, 0, L.s>>>(sstart, tstart, dim, ncell, per, c_lo, c_hi, bucket,
+                                               bcount);
+        FSE_LAUNCH_CHECK();
+    }
+    k_bucket_scan<<<1, 32, 0, L.s>>>(bcount, boff, nitems);
     FSE_LAUNCH_CHECK();
-    ++*L.launches;
+    if (blocks > 0) {
+        k_fill_items<<<blocks, 256, 0, L.s>>>(tstart, bucket, ncell, per, c_lo, c_hi, boff, bcur,
+                                              items);
+        FSE_LAUNCH_CHECK();
+    }
+    *L.launches += blocks > 0 ? 3 : 1;
 }
 
-void launch_fill_items(const Launch& L, const int32_t* start, const int32_t* off, int64_t ncell,
-                       int per, int32_t* items) {
-    (void)start;
-    (void)per;
-    k_fill_items<<<static_cast<unsigned>((ncell + 255) / 256), 256, 0, L.s>>>(off, ncell, items);
-    FSE_LAUNCH_CHECK();
-    ++*L.launches;
-}
+int realspace_work_buckets() { return kWorkBuckets; }
 
 void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const double* spx,
                       const double* spy, const double* spz, const double* sfs, int64_t ns,
