@@ -51,7 +51,11 @@ namespace {
 
 // 64-source chunks: a smaller per-warp chunk buffer buys occupancy (the
 // pair loop is latency-bound), which beats the better lane balance of
-// 128-source chunks (cfg2 5.84 -> 5.22 ms, cfg4 105 -> 98 ms on B200)
+// 128-source chunks (cfg2 5.84 -> 5.22 ms, cfg4 105 -> 98 ms on B200).
+// Three 256-thread CTAs per SM (78 registers): with the branch-free candidate
+// test the pair loop no longer rematerialises constants at the 64-register
+// cap (cfg2 5.55 -> 5.27 ms, cfg4 98.5 -> 91.6 ms; 2 CTAs at 107 registers,
+// 128-thread CTAs at 93 or 78 registers and 128-source chunks all measured slower)
 #ifndef FSE_RS_TPB
 #define FSE_RS_TPB 256
 #endif
@@ -59,7 +63,7 @@ namespace {
 #define FSE_RS_CH 64
 #endif
 #ifndef FSE_RS_MINB
-#define FSE_RS_MINB 4
+#define FSE_RS_MINB 3
 #endif
 constexpr int TPB = FSE_RS_TPB, CH = FSE_RS_CH, NW = CH / 32;
 static_assert(CH % 32 == 0 && NW >= 1 && NW <= 4, "chunk of 1..4 mask words");
