@@ -36,7 +36,10 @@ namespace fsecu {
 
 namespace {
 
-constexpr int SW = 4;      // warps per CTA
+#ifndef FSE_GATHER_SW
+#define FSE_GATHER_SW 4
+#endif
+constexpr int SW = FSE_GATHER_SW;  // warps per CTA
 constexpr int MAXT = 32;   // targets per item
 constexpr int RS = 34;     // slab row stride (doubles): 32 + 2 keeps A-fragment loads at 2 wavefronts
 #ifndef FSE_GATHER_NST
@@ -639,6 +642,8 @@ void launch_gather_slab(const Launch& L, const GridParams& g, const int32_t* i0s
         return;                                                                                \
     }
         FSE_TMA_CASE(3, 8)
+        FSE_TMA_CASE(2, 8)
+        FSE_TMA_CASE(1, 8)
         FSE_TMA_CASE(3, 7)
         FSE_TMA_CASE(3, 6)
         FSE_TMA_CASE(2, 7)

@@ -65,72 +65,75 @@ __global__ void k_quad_table(GridParams g, double* q) {
 }
 
 // FGG axis weights (ewald.cpp:33-51) for point perm[q], stored at sorted slot q.
-// Each thread builds its point's 3P weights in shared memory (row stride 3P+1,
-// conflict-free); the block then writes its points' rows, which are one
-// contiguous run of w, with consecutive threads on consecutive doubles.
+// Three threads per point, one per axis (the 3 P weights are three independent
+// chains of P products), PT points per block.  The weights are built in shared
+// memory (row stride 3P+1) and the block then writes its points' rows, which
+// are one contiguous run of w, with consecutive threads on consecutive doubles.
 __global__ void k_payload(GridParams g, const double* __restrict__ pos,
                           const double* __restrict__ str, int a, const uint32_t* __restrict__ perm,
                           int64_t n, const double* __restrict__ qtab, int32_t* __restrict__ i0s,
                           double* __restrict__ w, double* __restrict__ fs, bool fold_prefac,
                           int slab_only, bool naive) {
     extern __shared__ double stage[];
+    __shared__ int fx_s[128];
     __shared__ bool keep_row[128];
     const int P = g.P, W3 = 3 * P, RS = W3 + 1;
-    const int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x);
-    const int64_t q = q0 + threadIdx.x;
+    const int PT = static_cast<int>(blockDim.x) / 3;
+    const int ax = static_cast<int>(threadIdx.x) / PT, pt = static_cast<int>(threadIdx.x) - ax * PT;
+    const int64_t q0 = blockIdx.x * static_cast<int64_t>(PT);
+    const int64_t q = q0 + pt;
+    const bool valid = q < n;
+    int64_t idx = 0;
+    double s = 0.0;
+    int first = 0;
+    if (valid) {
+        idx = perm[q];
+        s = __ddiv_rn(__dsub_rn(pos[3 * idx + ax], g.origin), g.h);
+        first = static_cast<int>(ceil(__dsub_rn(s, 0.5 * P)));
+        int f = first < 0 ? 0 : first;
+        if (f + P > g.Mt) f = g.Mt - P;
+        i0s[3 * q + ax] = f;
+        if (ax == 0) fx_s[pt] = f;
+    }
+    __syncthreads();
+    // slab_only 1 (sources): a point whose x support misses this slab's
+    // planes is never read by its spread tiles; 2 (targets): a target whose
+    // coarse tile's union box misses them is in no quadrature item
+    // (k_slab_counts).  Such points get no weights.
     bool keep = false;
-    if (q < n) {
-        const int64_t idx = perm[q];
-        double s[3];
-        int first[3];
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            s[ax] = __ddiv_rn(__dsub_rn(pos[3 * idx + ax], g.origin), g.h);
-            first[ax] = static_cast<int>(ceil(__dsub_rn(s[ax], 0.5 * P)));
-            int f = first[ax] < 0 ? 0 : first[ax];
-            if (f + P > g.Mt) f = g.Mt - P;
-            i0s[3 * q + ax] = f;
-        }
-        // slab_only 1 (sources): a point whose x support misses this slab's
-        // planes is never read by its spread tiles; 2 (targets): a target whose
-        // coarse tile's union box misses them is in no quadrature item
-        // (k_slab_counts).  Such points get no weights.
-        const int fx = i0s[3 * q];
+    if (valid) {
+        const int fx = fx_s[pt];
         const int x0 = (fx >> 3) * 8;
         keep = slab_only == 0 ||
                (slab_only == 1 ? (fx + P > g.x_lo && fx < g.x_lo + g.nx)
                                : (x0 < g.x_lo + g.nx && x0 + P + 7 > g.x_lo));
-        if (keep) {
-            double* row = stage + threadIdx.x * RS;
-#pragma unroll 1
-            for (int ax = 0; ax < 3 && naive; ++ax) {
-                // axis_weights_naive (ewald.cpp:53-66): one exp per node
-                const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
-                for (int p = 0; p < P; ++p) {
-                    const double dx = (static_cast<double>(first[ax] + p) - s[ax]) * g.h;
-                    row[ax * P + p] = scale * exp(-g.alpha * dx * dx);
-                }
-            }
-#pragma unroll 1
-            for (int ax = 0; ax < 3 && !naive; ++ax) {
-                const double x0 = (first[ax] - s[ax]) * g.h;
-                const double e0 = exp(-g.alpha * x0 * x0);
-                const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
-                const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
-                double r = 1.0;
-                for (int p = 0; p < P; ++p) {
-                    row[ax * P + p] = scale * (e0 * r * qtab[p]);
-                    r *= ratio;
-                }
-            }
-            if (fs)
-                for (int c = 0; c < a; ++c) fs[q * a + c] = str[idx * a + c];
-        }
     }
-    keep_row[threadIdx.x] = keep;
+    if (ax == 0) keep_row[pt] = keep;
+    if (keep) {
+        double* row = stage + pt * RS + ax * P;
+        const double scale = (fold_prefac && ax == 0) ? g.prefac : 1.0;
+        if (naive) {
+            // axis_weights_naive (ewald.cpp:53-66): one exp per node
+            for (int p = 0; p < P; ++p) {
+                const double dx = (static_cast<double>(first + p) - s) * g.h;
+                row[p] = scale * exp(-g.alpha * dx * dx);
+            }
+        } else {
+            const double x0 = (first - s) * g.h;
+            const double e0 = exp(-g.alpha * x0 * x0);
+            const double ratio = exp(-2.0 * g.alpha * x0 * g.h);
+            double r = 1.0;
+            for (int p = 0; p < P; ++p) {
+                row[p] = scale * (e0 * r * qtab[p]);
+                r *= ratio;
+            }
+        }
+        if (fs)
+            for (int c = ax; c < a; c += 3) fs[q * a + c] = str[idx * a + c];
+    }
     __syncthreads();
     const int64_t left = n - q0;
-    const int cnt = static_cast<int>(left < blockDim.x ? left : blockDim.x);
+    const int cnt = static_cast<int>(left < PT ? left : PT);
     double* out = w + q0 * W3;
     for (int e = threadIdx.x; e < cnt * W3; e += blockDim.x) {
         const int t = e / W3;
@@ -206,20 +209,19 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
                            const double* qtab, int32_t* i0s, double* w, double* fs,
                            bool fold_prefac, int slab_only, bool naive) {
     if (n <= 0) return;
-    // block size: as many warps (<= 4) as fit 48 KB of staged weight rows;
-    // wider supports take one warp and opt-in shared memory
+    // points per block: up to 64 (three threads each) whose staged weight rows
+    // fit 48 KB; wider supports take fewer points and opt-in shared memory
     const size_t row_bytes = sizeof(double) * (3 * g.P + 1);
-    int tpb = static_cast<int>((48 * 1024) / row_bytes) / 32 * 32;
-    tpb = tpb < 32 ? 32 : (tpb > 128 ? 128 : tpb);
-    if (row_bytes * tpb > 48 * 1024) {
-        if (row_bytes * tpb > 227 * 1024)
+    int pt = static_cast<int>((48 * 1024) / row_bytes) / 32 * 32;
+    pt = pt < 32 ? 32 : (pt > 64 ? 64 : pt);
+    if (row_bytes * pt > 48 * 1024) {
+        if (row_bytes * pt > 227 * 1024)
             throw Error(FSE_EINVAL, "k_payload: Gaussian support too wide");
         FSE_CU(cudaFuncSetAttribute(k_payload, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(row_bytes * tpb)));
+                                    static_cast<int>(row_bytes * pt)));
     }
-    k_payload<<<blocks_for(n, tpb), tpb, row_bytes * tpb, L.s>>>(g, pos, str, a, perm, n, qtab,
-                                                                  i0s, w, fs, fold_prefac,
-                                                                  slab_only, naive);
+    k_payload<<<static_cast<unsigned>((n + pt - 1) / pt), 3 * pt, row_bytes * pt, L.s>>>(
+        g, pos, str, a, perm, n, qtab, i0s, w, fs, fold_prefac, slab_only, naive);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }
