@@ -406,6 +406,26 @@ inline int eng_threads_host(int eng) { return eng == 2 ? 128 : 256; }
 template <int ENG>
 constexpr int eng_minb() { return Eng<ENG>::THREE ? 2 : 2; }
 
+// CTA size of the z and y passes (one column transform each, latency-bound)
+// at D = 624 (engine 1), per direction: forward FSE_YZF_T, inverse FSE_YZI_T
+// threads.  128-thread CTAs (4 columns, ~55 KB) fit four per SM instead of two
+// 9-column ones, so the CTAs' load / compute / barrier phases overlap better
+// at the same warp count (measured: inverse y + z 2.21 -> 2.11 ms; the forward
+// passes lose, 2.12 -> 2.17 ms, and keep 256)
+#ifndef FSE_YZF_T
+#define FSE_YZF_T 256
+#endif
+#ifndef FSE_YZI_T
+#define FSE_YZI_T 128
+#endif
+template <int ENG, bool INV>
+constexpr int yz_threads() { return ENG == 1 ? (INV ? FSE_YZI_T : FSE_YZF_T) : eng_threads<ENG>(); }
+template <int ENG, bool INV>
+constexpr int yz_minb() { return ENG == 1 ? 65536 / (yz_threads<ENG, INV>() * 128) : eng_minb<ENG>(); }
+inline int yz_threads_host(int eng, bool inv) {
+    return eng == 1 ? (inv ? FSE_YZI_T : FSE_YZF_T) : eng_threads_host(eng);
+}
+
 // ------------------------------------------------------------------ test kernel
 template <int ENG>
 __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_fft_test(FftPlan pl, const double2* __restrict__ tw_g,
@@ -427,7 +447,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_fft_tes
 // ------------------------------------------------------------------ z forward
 // column q of the CTA = row pair (comp, i, jp): z[n] = R[i][2jp][n] + i R[i][2jp+1][n]
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, false>(), yz_minb<ENG, false>()) k_zfwd(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double* __restrict__ R,
                                                  double2* __restrict__ B) {
@@ -486,7 +506,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd(Ff
 // forward: columns (comp, i, kz-tile of ncol); input B[comp][i][j][kz], j < Mt
 // inverse: input C[comp][i][ky][kz] (all ky), output B (j < Mt)
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, INV>(), yz_minb<ENG, INV>()) k_ypass(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int A, int nxs, int nkys,
                                                   int ncol, double2* __restrict__ B,
                                                   double2* __restrict__ Cb, BlockDest dst) {
@@ -717,7 +737,7 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
 // ------------------------------------------------------------------ z inverse
 // row pair (comp, i, jp): Z = X0 + i X1 over the Hermitian extension; keep n < Mt
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, true>(), yz_minb<ENG, true>()) k_zinv(FftPlan pl, const double2* __restrict__ tw_g,
                                                  int Mt, int nx, int ncomp, int ncol,
                                                  const double2* __restrict__ B,
                                                  double* __restrict__ W) {
@@ -780,7 +800,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv(Ff
 
 // z forward: column c = row pair (comp, i, jp), rows contiguous -> n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, false>(), yz_minb<ENG, false>()) k_zfwd2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double* __restrict__ R,
                                                   double2* __restrict__ B) {
@@ -834,7 +854,7 @@ __global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zfwd2(F
 
 // y passes: column c = (comp, slab plane xl, kz0 + c), columns adjacent in kz -> c-fastest
 template <int ENG, bool INV>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, INV>(), yz_minb<ENG, INV>()) k_ypass2(FftPlan pl, const double2* __restrict__ tw_g,
                                                    int Mt, int nx, int A, int nxs, int nkys,
                                                    int ncol, double2* __restrict__ B,
                                                    double2* __restrict__ Cb, BlockDest dst) {
@@ -1006,7 +1026,7 @@ __global__ void __launch_bounds__(xs_threads<ENG, KIND>(), xs_minb<ENG, KIND>())
 
 // z inverse: row pairs, Hermitian extension loaded straight from B, n2-fastest
 template <int ENG>
-__global__ void __launch_bounds__(eng_threads<ENG>(), eng_minb<ENG>()) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
+__global__ void __launch_bounds__(yz_threads<ENG, true>(), yz_minb<ENG, true>()) k_zinv2(FftPlan pl, const double2* __restrict__ tw_g,
                                                   int Mt, int nx, int ncomp, int ncol,
                                                   const double2* __restrict__ B,
                                                   double* __restrict__ W) {
@@ -1389,7 +1409,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
-            const int u = units_fit(h, 1, 0);
+            const int u = units_fit(h, 1, 0, yz_threads_host(h.eng, false));
             FftPlan p = h.dev;
             set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
@@ -1398,20 +1418,20 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 1) {
                     allow_smem(k_zfwd2<EV>, sm);
-                    k_zfwd2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                    k_zfwd2<EV><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
                 } else {
                     allow_smem(k_zfwd<EV>, sm);
-                    k_zfwd<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                    k_zfwd<EV><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
                 }
             } else {
                 allow_smem(k_zfwd<EV>, sm);
-                k_zfwd<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
+                k_zfwd<EV><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, R, B);
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
         {
-            const int u = std::min(units_fit(h, 1, 0), Dh);
+            const int u = std::min(units_fit(h, 1, 0, yz_threads_host(h.eng, false)), Dh);
             FftPlan p = h.dev;
             set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
@@ -1420,16 +1440,16 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 2) {
                     allow_smem(k_ypass2<EV, false>, sm);
-                    k_ypass2<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                    k_ypass2<EV, false><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                                    g.nkys, u, B, C, dst);
                 } else {
                     allow_smem(k_ypass<EV, false>, sm);
-                    k_ypass<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                    k_ypass<EV, false><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                                   g.nkys, u, B, C, dst);
                 }
             } else {
                 allow_smem(k_ypass<EV, false>, sm);
-                k_ypass<EV, false><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
+                k_ypass<EV, false><<<nb, yz_threads<EV, false>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, g.nxs,
                                                               g.nkys, u, B, C, dst);
             }
             FSE_LAUNCH_CHECK();
@@ -1522,7 +1542,7 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
     with_engine(h.eng, [&](auto E) {
         constexpr int EV = decltype(E)::value;
         {
-            const int u = std::min(units_fit(h, 1, 0), Dh);
+            const int u = std::min(units_fit(h, 1, 0, yz_threads_host(h.eng, true)), Dh);
             FftPlan p = h.dev;
             set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
@@ -1531,23 +1551,23 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 8) {
                     allow_smem(k_ypass2<EV, true>, sm);
-                    k_ypass2<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
+                    k_ypass2<EV, true><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys,
                                                                   u, B, C, BlockDest{});
                 } else {
                     allow_smem(k_ypass<EV, true>, sm);
-                    k_ypass<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                    k_ypass<EV, true><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
                                                                  B, C, BlockDest{});
                 }
             } else {
                 allow_smem(k_ypass<EV, true>, sm);
-                k_ypass<EV, true><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
+                k_ypass<EV, true><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, A, g.nxs, g.nkys, u,
                                                              B, C, BlockDest{});
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
         }
         {
-            const int u = units_fit(h, 1, 0);
+            const int u = units_fit(h, 1, 0, yz_threads_host(h.eng, true));
             FftPlan p = h.dev;
             set_buf(p, h, u, d_tw);
             const size_t sm = smem_bytes(h, u);
@@ -1556,14 +1576,14 @@ void launch_fft_inverse_yz(const Launch& L, const HostFftPlan& h, const double2*
             if constexpr (EV > 0 && !Eng<EV>::BLUE && !Eng<EV>::THREE) {
                 if (v2_mask_for<EV>() & 16) {
                     allow_smem(k_zinv2<EV>, sm);
-                    k_zinv2<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                    k_zinv2<EV><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
                 } else {
                     allow_smem(k_zinv<EV>, sm);
-                    k_zinv<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                    k_zinv<EV><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
                 }
             } else {
                 allow_smem(k_zinv<EV>, sm);
-                k_zinv<EV><<<nb, eng_threads<EV>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
+                k_zinv<EV><<<nb, yz_threads<EV, true>(), sm, L.s>>>(p, d_tw, Mt, nx, ncomp, u, B, W);
             }
             FSE_LAUNCH_CHECK();
             ++*L.launches;
