@@ -150,12 +150,12 @@ __device__ __forceinline__ double exp_neg_bounded(double y) {
     return __hiloint2double(__double2hiint(p) + j * (1 << 20), __double2loint(p));
 }
 
-// 1/sqrt(r2): fp32 seed + two Newton steps in fp64 (22 -> 44 -> full bits,
-// ~1 ulp), no special-case branches; r2 < 1e-36 (points closer than 1e-18,
-// only possible near the origin) takes the library rsqrt
+// 1/sqrt(r2): the FP64 MUFU seed (rsqrt.approx.f64, ~2^-22 relative, the
+// whole double range: no conversions and no special-case branch) and two
+// Newton steps in fp64 (22 -> 44 -> full bits, ~1 ulp)
 __device__ __forceinline__ double rsqrt_nr(double r2) {
-    if (r2 < 1e-36) return rsqrt(r2);
-    double y = static_cast<double>(rsqrtf(static_cast<float>(r2)));
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
     const double h = 0.5 * r2;
     y = y * fma(-h * y, y, 1.5);
     y = y * fma(-h * y, y, 1.5);
@@ -175,9 +175,14 @@ __device__ __forceinline__ void pair(double rx, double ry, double rz, double r2,
     const double xr = xi * rn;
     double F0, F1 = 0.0;
     if (!TAIL || xr < kXMax) {
-        const double uu = xr * (kNI / kXMax);
-        const int iv = min(static_cast<int>(uu), kNI - 1);
-        const double t = 2.0 * (uu - iv) - 1.0;
+        // interval iv = floor(uu) by the round-to-nearest magic constant (no
+        // F2I/I2F conversions): round(uu - 1/2); at an integer uu this may give
+        // uu - 1 and t = 1, the fitted interval's closed end
+        // (uu < kNI: xr < kXMax, clamped against the product's rounding)
+        const double uu = fmin(xr * (kNI / kXMax), kNI - 1e-9);
+        const double kk = (uu - 0.5) + c_exp[3];
+        const int iv = __double2loint(kk);
+        const double t = 2.0 * (uu - (kk - c_exp[3])) - 1.0;
 #ifdef FSE_RS_HORNER
         double ex = tab[kDeg][iv];
 #pragma unroll
