@@ -496,13 +496,18 @@ def run_ours(args, dist: Dist):
     line = {
         "metric": metric_name(w), "value": value, "unit": "targets/s", "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        # N = 1 is the base of the strong-scaling series of run_dist (one evaluation
+        # split over N GPUs); --replicas at N > 1 is weak scaling (N evaluations)
+        "higher_is_better": True, "scaling": "weak" if dist.world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (mt19937_64 seed {SEED}+rank), "
                 "no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
                    "N": n, "NT": nt, "xi": cfg.xi, "rc": cfg.rc, "M": cfg.M, "P": cfg.P,
                    "Mtilde": cfg.Mtilde, "fft_grid": cfg.D,
-                   "eta": round(cfg.eta, 4), "parallelism": f"replicas x{dist.world}",
+                   "eta": round(cfg.eta, 4),
+                   "parallelism": (f"replicas x{dist.world}" if dist.world > 1
+                                   else "one GPU, the whole evaluation"),
                    "l2": working_set_note(w, cfg),
                    "green_precompute_s": round(precompute_s, 3)},
         "e2e": {"value": nt * e2e_steps * dist.world / e2e_s, "unit": "targets/s",
@@ -655,7 +660,7 @@ def run_reference(args):
         "impl": "reference", "metric": metric_name(w), "value": v, "unit": "targets/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(r["seconds"]),
         "warmup": r["warmup"], "ms_per_step": r["median_s"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: SURVEY 8(d) generator {w['wl']} (seed {SEED}), reference-side "
                 "generator (oracle/ref_capi.cpp), no dataset",
         "config": {"workload": f"{args.workload}: {w['desc']}", "kind": KIND_NAMES[w["kind"]],
