@@ -5,17 +5,19 @@
 //   stream s0 (Fourier part, ewald.cpp:295-392)
 //     support starts + tile keys -> stable radix sort -> tile starts
 //     -> FGG weights in sorted order (prefac folded)              [prep]
-//     -> k_spread: tile-owned DMMA spreading, no atomics            [spread]
+//     -> k_spread_ws: tile-owned DMMA spreading, no atomics; a producer
+//        warp feeds four MMA warps through an mbarrier ring        [spread]
 //     -> k_zfwd (R2C along z, two real rows per complex FFT) and
 //        k_ypass (y), pruned: zero planes x >= Mtilde are never stored [fft]
 //     -> k_xscale*: forward x-FFT, Nyquist-exact multiplier A_eff G / D^3,
 //        inverse x-FFT, in shared memory / registers                [scale]
 //     -> k_ypass<inverse>, k_zinv (C2R): only the Mtilde^3 window   [fft]
 //     -> target prep (reuses the source sort when targets == sources)
-//     -> k_gather_tma: TMA-staged x-planes, DMMA z-contraction        [quadrature]
+//     -> k_gather_tma: TMA-staged x-planes, DMMA z-contraction, targets
+//        x-sorted per item, n-tiles skip planes outside their supports [quadrature]
 //   stream s1 (real part, realspace.cpp:86-149), concurrent with s0
 //     cell ids -> stable radix sort -> bucket starts (the reference CellList)
-//     -> SoA permute -> k_realspace                               [realspace]
+//     -> SoA permute -> work items heaviest cell first -> k_realspace [realspace]
 //   s0 waits for s1 -> k_epilogue: u = (uF + uR) + self term
 //
 // All FFTs of the hot path are the hand-written engines of k_fft.cu (no cuFFT);

@@ -61,17 +61,31 @@ __global__ void k_masks(const double* __restrict__ pos, int64_t n, Geom q, int t
     mask[i] = targets ? fsedist::target_mask(x, q) : fsedist::source_mask(x, q);
 }
 
-__global__ void k_flag_bit(const uint32_t* __restrict__ mask, int64_t n, int bit,
-                           int32_t* __restrict__ flag) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i < n) flag[i] = (mask[i] >> bit) & 1u;
-    if (i == n) flag[n] = 0;
+// all destinations at once: segment d of flag (n + 1 entries, the last 0) is
+// bit d of the masks, except the own rank's segment (all 0); one scan over the
+// G segments then gives every destination's offsets (relative to its
+// segment's first offset)
+__global__ void k_flag_bits(const uint32_t* __restrict__ mask, int64_t n, int G, int self,
+                            int32_t* __restrict__ flag) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= static_cast<int64_t>(G) * (n + 1)) return;
+    const int d = static_cast<int>(e / (n + 1));
+    const int64_t i = e - static_cast<int64_t>(d) * (n + 1);
+    flag[e] = (i < n && d != self) ? static_cast<int32_t>((mask[i] >> d) & 1u) : 0;
 }
 
-__global__ void k_compact(const int32_t* __restrict__ flag, const int32_t* __restrict__ off,
-                          int64_t n, int32_t* __restrict__ idx) {
+// cnt[d] = points flagged for destination d (from the scanned segments)
+__global__ void k_seg_totals(const int32_t* __restrict__ off, int64_t n, int G,
+                             int64_t* __restrict__ cnt) {
+    const int d = threadIdx.x;
+    if (d < G) cnt[d] = off[static_cast<int64_t>(d) * (n + 1) + n] - off[static_cast<int64_t>(d) * (n + 1)];
+}
+
+// idx_d[off - off(segment start)] = i for the flagged points of segment d
+__global__ void k_compact_seg(const int32_t* __restrict__ flag, const int32_t* __restrict__ off,
+                              int64_t n, int32_t* __restrict__ idx) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i < n && flag[i]) idx[off[i]] = static_cast<int32_t>(i);
+    if (i < n && flag[i]) idx[off[i] - off[0]] = static_cast<int32_t>(i);
 }
 
 // out[j * w + c] = in[idx[j] * w + c]
@@ -198,33 +212,52 @@ struct Rank {
         FSE_LAUNCH_CHECK();
         c->launches += 2;
         int64_t* cnt = cnt_dev.get<int64_t>(2 * G);
-        std::vector<int64_t> h(2 * G, 0);
+        FSE_CU(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * 2 * G, s));
         scnt.assign(G, 0);
         tcnt.assign(G, 0);
+        // per pass: one flag kernel over all destinations, one scan, one totals
+        // kernel; a single host sync for both passes' counts
+        int32_t* fl[2] = {nullptr, nullptr};
+        int32_t* of[2] = {nullptr, nullptr};
+        const int64_t np[2] = {n_own, nt_own};
+        const int64_t tot_len = G * (n_own + 1) + G * (nt_own + 1);
+        int32_t* f_all = flag.get<int32_t>(tot_len);
+        int32_t* o_all = off.get<int32_t>(tot_len);
+        fl[0] = f_all;
+        of[0] = o_all;
+        fl[1] = f_all + G * (n_own + 1);
+        of[1] = o_all + G * (n_own + 1);
         for (int pass = 0; pass < 2; ++pass) {
-            const int64_t n = pass ? nt_own : n_own;
+            const int64_t n = np[pass];
+            if (n == 0 || G == 1) continue;
             const uint32_t* m = pass ? tm : sm;
-            int32_t* f = flag.get<int32_t>(n + 1);
-            int32_t* o = off.get<int32_t>(n + 1);
+            const int64_t len = static_cast<int64_t>(G) * (n + 1);
+            k_flag_bits<<<nblk(len), 256, 0, s>>>(m, n, G, r, fl[pass]);
+            exclusive_scan(c, s, "dist", fl[pass], of[pass], len);
+            k_seg_totals<<<1, 32 * ((G + 31) / 32), 0, s>>>(of[pass], n, G, cnt + pass * G);
+            c->launches += 2;
+        }
+        FSE_LAUNCH_CHECK();
+        std::vector<int64_t> h(2 * G, 0);
+        FSE_CU(cudaMemcpyAsync(h.data(), cnt, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, s));
+        FSE_CU(cudaStreamSynchronize(s));
+        for (int pass = 0; pass < 2; ++pass) {
+            const int64_t n = np[pass];
             for (int d = 0; d < G; ++d) {
                 if (d == r || n == 0) continue;
-                k_flag_bit<<<nblk(n + 1), 256, 0, s>>>(m, n, d, f);
-                exclusive_scan(c, s, "dist", f, o, n + 1);
-                int32_t tot = 0;
-                FSE_CU(cudaMemcpyAsync(&tot, o + n, sizeof tot, cudaMemcpyDeviceToHost, s));
-                FSE_CU(cudaStreamSynchronize(s));
+                const int64_t tot = h[pass * G + d];
                 GBuf& ib = pass ? *tidx[d] : *sidx[d];
                 int32_t* idx = ib.get<int32_t>(tot);
-                if (tot > 0) k_compact<<<nblk(n), 256, 0, s>>>(f, o, n, idx);
-                c->launches += tot > 0 ? 2 : 1;
+                if (tot > 0) {
+                    const int64_t seg = static_cast<int64_t>(d) * (n + 1);
+                    k_compact_seg<<<nblk(n), 256, 0, s>>>(fl[pass] + seg, of[pass] + seg, n, idx);
+                    ++c->launches;
+                }
                 (pass ? tcnt : scnt)[d] = tot;
-                h[pass * G + d] = tot;
             }
         }
         FSE_LAUNCH_CHECK();
-        FSE_CU(cudaMemcpyAsync(cnt, h.data(), sizeof(int64_t) * 2 * G, cudaMemcpyHostToDevice, s));
         int64_t* all = cnt_all.get<int64_t>(2 * G * G);
-        FSE_CU(cudaStreamSynchronize(s));  // h is pageable and goes out of scope
         Step st;
         for (int d = 0; d < G; ++d) {
             st.sends.push_back({d, cnt, sizeof(int64_t) * 2 * G});
@@ -607,8 +640,9 @@ fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fs
         // inverse, finish) the step's time on the device (ms, the rank running
         // alone) and the bytes it sends to other ranks: [r][step][time, bytes]
         int step_no = 0;
+        bool timing = prof != nullptr;
         auto record = [&](int r, int stp, double ms, double bytes) {
-            if (prof) {
+            if (timing) {
                 prof[(r * 6 + stp) * 2] = ms;
                 prof[(r * 6 + stp) * 2 + 1] = bytes;
             }
@@ -631,11 +665,21 @@ fse_status fse_cuda_dist_virtual_total_sum(fse_cuda_ctx* c, int nranks, const fs
             run_loopback(st, c->s0);
             ++step_no;
         };
-        step_all([](Rank& R) { return R.classify(); });
-        step_all([](Rank& R) { return R.pack(); });
-        step_all([](Rank& R) { return R.forward(); });
-        step_all([&](Rank& R) { return R.scale(green); });
-        step_all([](Rank& R) { return R.inverse(); });
+        // with a profile the steps run twice and the second pass is recorded: the
+        // first one allocates every rank's buffers (cudaMalloc is synchronous and
+        // would otherwise be timed inside the steps)
+        for (int pass = prof ? 0 : 1; pass < 2; ++pass) {
+            timing = prof != nullptr && pass == 1;
+            step_no = 0;
+            step_all([](Rank& R) { return R.classify(); });
+            step_all([](Rank& R) { return R.pack(); });
+            step_all([](Rank& R) { return R.forward(); });
+            step_all([&](Rank& R) { return R.scale(green); });
+            step_all([](Rank& R) { return R.inverse(); });
+            if (pass == 0)
+                for (int r = 0; r < G; ++r) ranks[r]->finish(out_u[r]->ptr<double>());
+        }
+        timing = prof != nullptr;
         std::vector<double> hu(3 * nt);
         for (int r = 0; r < G; ++r) {
             FSE_CU(cudaDeviceSynchronize());
