@@ -67,6 +67,10 @@ WORKLOADS = {
                   desc="cfg3 inputs, (rc, M, P) = select_parameters(xi=40, tol=1e-8)"),
     "cfg4t": dict(kind=2, wl=4, n=1_000_000, xi=110.0, tol=1e-10, select=True,
                   desc="cfg4 inputs, (rc, M, P) = select_parameters(xi=110, tol=1e-10)"),
+    # M = 834, D = 1730 = 2 x 5 x 173: generic Stockham stage of radix 173 at one
+    # CTA per SM (227 KB of shared memory), ~135 GB of HBM, ~2.7 s per call
+    "cfg5t": dict(kind=0, wl=5, n=8_000_000, xi=220.0, tol=1e-10, select=True,
+                  desc="cfg5 inputs, (rc, M, P) = select_parameters(xi=220, tol=1e-10)"),
 }
 
 

@@ -196,7 +196,9 @@ T* buf(fse_cuda_ctx* c, const std::string& name, size_t count) {
         if (b.p) FSE_CU(cudaFree(b.p));
         b.p = nullptr;
         b.bytes = 0;
-        const size_t alloc = bytes + bytes / 8;  // headroom for neighbouring sizes
+        // headroom for neighbouring sizes; none on multi-GB buffers (cfg5t's spectra
+        // are 62 GB: the headroom alone would be 8 GB)
+        const size_t alloc = bytes + (bytes < (size_t(2) << 30) ? bytes / 8 : 0);
         FSE_CU(cudaMalloc(&b.p, alloc));
         b.bytes = alloc;
     }
@@ -500,6 +502,7 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         if (std::abs(box_side - cfg->L) > 1e-12 * cfg->L)
             invalid("spread: config box does not match system");
         const GridParams g = make_grid_params(*cfg);
+        fft_xscale_check(fft_plan(c, g.D).host, kind);  // refuse before any work is queued
         Launch L = L0(c);
         double* qtab = buf<double>(c, "qtab", g.P);
         launch_quad_table(L, g, qtab);
@@ -1511,6 +1514,7 @@ fse_status fse_cuda_xscale_probe(fse_cuda_ctx* c, const fse_config* cfg, int kin
                 invalid("xscale_probe: column out of range");
         const int a = arity_of(kind);
         const Launch L = L0(c);
+        fft_xscale_check(fft_plan(c, g.D).host, kind);  // before the big buffers
         const int64_t nC = static_cast<int64_t>(a) * g.Mt * g.D * g.Dh;
         double2* C = buf<double2>(c, "C", static_cast<size_t>(nC));
         launch_probe_fill(L, C, nC, seed);

@@ -57,7 +57,9 @@ constexpr int maxit() {
     return (16 + P - 1) / P;
 }
 
-// one in-place Stockham stage over NCOL columns of length D
+// one in-place Stockham stage over NCOL columns of length D (every item is read
+// before any is written, so the items must fit one batch of maxit<P>() per
+// thread: the planner checks)
 template <int P>
 __device__ __forceinline__ void stage_reg(double2* buf, int D, int ncol, int Ns, const FDiv& fnb,
                                           const FDiv& fNs, const double2* __restrict__ tw, int sgn) {
@@ -97,6 +99,38 @@ __device__ __forceinline__ void stage_reg(double2* buf, int D, int ncol, int Ns,
 #pragma unroll
             for (int r = 0; r < P; ++r) buf[pad(o + r * Ns)] = v[m][r];
         }
+    }
+    __syncthreads();
+}
+
+// the same stage out of place (plans with a second column buffer), one item per
+// thread and trip, for stages with more items than an in-place batch holds
+// (D = 1730 = 173 x 2 x 5: 3 x 865 radix-2 and 3 x 346 radix-5 butterflies in the
+// x pass).  Instantiated for radix 2 and 5 only (each instance costs the in-place
+// stages registers); other overflowing plans are refused by the planner.
+template <int P>
+__device__ __forceinline__ void stage_reg_oop(const double2* in, double2* out, int D, int ncol, int Ns,
+                                           int nb, const double2* __restrict__ tw, int sgn) {
+    const int items = nb * ncol;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int c = it / nb, b = it - c * nb;
+        const int bq = b / Ns, k = b - bq * Ns;
+        double2 v[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) v[r] = in[pad(c * D + b + r * nb)];
+        if (k != 0) {
+            const double2* t = tw + k * (P - 1);
+#pragma unroll
+            for (int r = 1; r < P; ++r) {
+                double2 w = t[r - 1];
+                if (sgn > 0) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        Dft<P>::run(v, sgn);
+        const int o = c * D + bq * Ns * P + k;
+#pragma unroll
+        for (int r = 0; r < P; ++r) out[pad(o + r * Ns)] = v[r];
     }
     __syncthreads();
 }
@@ -169,10 +203,26 @@ __device__ __forceinline__ void stage_gen_pairs(const double2* in, double2* out,
 }
 
 template <int P>
-__device__ __forceinline__ void run_radix(double2* cur, int& s, const FftPlan& pl, int ncol,
+__device__ __forceinline__ void run_radix(double2*& cur, double2*& other, int& s,
+                                          const FftPlan& pl, int ncol,
                                           const double2* __restrict__ tw, int sgn) {
     while (s < pl.nst && pl.p[s] == P) {
-        stage_reg<P>(cur, pl.D, ncol, pl.Ns[s], pl.dnb[s], pl.dNs[s], tw + pl.tw[s], sgn);
+        // more items than one in-place batch holds (D = 1730: 3 x 865 radix-2
+        // butterflies): out of place into the generic plan's second buffer
+        bool oop = false;
+        if constexpr (P == 2 || P == 5) {
+            oop = pl.two_bufs &&
+                  static_cast<int>(pl.dnb[s].d) * ncol > maxit<P>() * static_cast<int>(blockDim.x);
+            if (oop) {
+                stage_reg_oop<P>(cur, other, pl.D, ncol, pl.Ns[s], static_cast<int>(pl.dnb[s].d),
+                                 tw + pl.tw[s], sgn);
+                double2* t = cur;
+                cur = other;
+                other = t;
+            }
+        }
+        if (!oop)
+            stage_reg<P>(cur, pl.D, ncol, pl.Ns[s], pl.dnb[s], pl.dNs[s], tw + pl.tw[s], sgn);
         ++s;
     }
 }
@@ -183,6 +233,7 @@ __device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int nco
                                                  const FftPlan& pl, const double2* __restrict__ tw,
                                                  int sgn) {
     double2* cur = a;
+    double2* other = b;
     int s = 0;
     if (pl.nst > 0 && pl.p[0] > 13) {
         if (pl.Ns[0] == 1 && (pl.p[0] & 1))
@@ -190,16 +241,17 @@ __device__ __forceinline__ double2* fft_stockham(double2* a, double2* b, int nco
         else
             stage_gen(cur, b, pl.D, ncol, pl.p[0], pl.Ns[0], pl, 0, tw + pl.tw[0], sgn);
         cur = b;
+        other = a;
         s = 1;
     }
-    run_radix<8>(cur, s, pl, ncol, tw, sgn);
-    run_radix<4>(cur, s, pl, ncol, tw, sgn);
-    run_radix<2>(cur, s, pl, ncol, tw, sgn);
-    run_radix<3>(cur, s, pl, ncol, tw, sgn);
-    run_radix<5>(cur, s, pl, ncol, tw, sgn);
-    run_radix<7>(cur, s, pl, ncol, tw, sgn);
-    run_radix<11>(cur, s, pl, ncol, tw, sgn);
-    run_radix<13>(cur, s, pl, ncol, tw, sgn);
+    run_radix<8>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<4>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<2>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<3>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<5>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<7>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<11>(cur, other, s, pl, ncol, tw, sgn);
+    run_radix<13>(cur, other, s, pl, ncol, tw, sgn);
     return cur;
 }
 
@@ -1318,8 +1370,11 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap, int threa
             const int T = threads > 0 ? threads : eng_threads_host(h.eng);
             ok = cols * h.D1 <= T && cols * h.D2 <= T;
         } else {
+            // in-place stages hold all their items in one register batch; the radix-2
+            // and radix-5 stages of a plan with a second buffer (generic first stage)
+            // may run out of place in several batches instead
             for (int p : h.radices)
-                if (is_reg_radix(p) &&
+                if (!(h.generic && (p == 2 || p == 5)) && is_reg_radix(p) &&
                     static_cast<long long>(cols) * (D / p) > static_cast<long long>(kThreads) * maxit_host(p))
                     ok = false;
         }
@@ -1329,11 +1384,14 @@ int units_per_cta(const HostFftPlan& h, int cols_per_unit, size_t cap, int threa
     return best;
 }
 
-// two CTAs per SM when possible, otherwise one CTA with up to ~220 KB
+// two CTAs per SM when possible, otherwise one CTA with up to 220 KB, and as the
+// last resort the sm_100 per-CTA maximum of 227 KB (D = 1730 = 2 x 5 x 173, cfg5's
+// tolerance-consistent grid: the x pass of three generic-Stockham columns needs 223 KB)
 int units_fit(const HostFftPlan& h, int cols_per_unit, size_t extra_per_unit, int threads = 0) {
     // three-level engine: three CTAs per SM when they fit
     const size_t cap3 = (h.eng == 8) ? static_cast<size_t>(74 * 1024) : kSmemCap;
-    for (size_t cap : {cap3, kSmemCap, static_cast<size_t>(220 * 1024)}) {
+    for (size_t cap : {cap3, kSmemCap, static_cast<size_t>(220 * 1024),
+                       static_cast<size_t>(227 * 1024)}) {
         int u = units_per_cta(h, cols_per_unit, cap, threads);
         while (u > 0 && smem_bytes(h, u * cols_per_unit) + extra_per_unit * u > cap) --u;
         if (u > 0) return u;
@@ -1456,6 +1514,20 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
             ++*L.launches;
         }
     });
+}
+
+// throws invalid_argument when the x pass of this grid does not fit the FFT
+// engines (called before the spectra are allocated)
+void fft_xscale_check(const HostFftPlan& h, int kind) {
+    const int A = kind == KIND_SCALAR ? 1 : arity_of(kind);
+    int xmask = 0;
+    with_engine(h.eng, [&](auto E) { xmask = v2_mask_for<decltype(E)::value>(); });
+    const size_t gcol = (h.eng > 0 && (xmask & 4)) ? 0 : sizeof(double) * static_cast<size_t>(h.dev.D);
+    const int mx = std::max(h.D1, h.D2);
+    const int xthr = (A == 9 && h.eng > 0 && 9 * mx > eng_threads_host(h.eng))
+                         ? 384
+                         : eng_threads_host(h.eng);
+    (void)units_fit(h, A, gcol, xthr);
 }
 
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,

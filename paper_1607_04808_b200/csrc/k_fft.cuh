@@ -91,6 +91,7 @@ void launch_fft_forward_zy(const Launch& L, const HostFftPlan& h, const double2*
 // peers: where the results of each x block go (peer-direct exchange); null =
 // in place
 // d_ex: scratch for the D per-axis exp factors of the multiplier
+void fft_xscale_check(const HostFftPlan& h, int kind);
 void launch_fft_xscale(const Launch& L, const HostFftPlan& h, const double2* d_tw,
                        const GridParams& g, int kind, const double* G, double2* C,
                        double* d_ex, const BlockDest* peers = nullptr);

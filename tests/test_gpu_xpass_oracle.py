@@ -2,8 +2,8 @@
 k-space multiplier -> inverse x-FFT, in place on the pruned spectrum) against
 a numpy restatement, column by column, on EVERY FFT engine the BASELINE
 configurations and their tolerance-consistent variants select (register
-engines 624, 1200, 704, 242; Bluestein 298 (cfg3), 422, 348, 888, 1730;
-Stockham 194) and all three kernels, including the stresslet's nine input
+engines 624, 1200, 704, 242; Bluestein 298 (cfg3), 422, 348, 888; Stockham
+194 and 1730 (cfg5t)) and all three kernels, including the stresslet's nine input
 columns on the 1200- and 704-point engines.
 
 The input spectrum and (by default) the Green's table are pseudo-random
@@ -43,6 +43,9 @@ CASES = [
     ("422 (Bluestein-1024)", (1.0, 110.0, 0.045, 187, 24), 422, (0, 1, 2)),
     ("cfg2t 888", (1.0, 110.0, 0.042896, 414, 24), 888, (0, 2)),
     ("cfg1 194", (1.0, 28.0, 0.15, 80, 16), 194, (0, 1, 2)),
+    # cfg5's tolerance-consistent grid: generic Stockham stage of radix 173, one CTA
+    # per SM at the 227 KB shared-memory maximum (~90 GB of spectra: stokeslet only)
+    ("cfg5t 1730", (1.0, 220.0, 0.021279, 834, 24), 1730, (0,)),
 ]
 
 
@@ -66,12 +69,13 @@ def test_xpass_matches_numpy(fse, ctx, label, args, D, kinds):
     ctx.trim()
 
 
-def test_xpass_1730_is_refused_cleanly(fse, ctx):
-    """cfg5's tolerance-consistent grid D = 1730 = 2 x 5 x 173 exceeds every FFT
-    engine (Bluestein would need a >= 3459-point register engine): the call
-    fails with invalid_argument instead of computing garbage."""
-    cfg = fse.make_config(1.0, 220.0, 0.021279, 834, 24)
-    assert cfg.D == 1730
+def test_xpass_too_large_is_refused_cleanly(fse, ctx):
+    """D = 2018 = 2 x 1009 exceeds every FFT engine (Bluestein would need a
+    >= 4035-point register engine, three generic-Stockham columns more than 227 KB
+    of shared memory): the call fails with invalid_argument before any buffer is
+    allocated instead of computing garbage."""
+    cfg = fse.make_config(1.0, 220.0, 0.02, 968, 24)
+    assert cfg.D == 2018
     with pytest.raises(fse.InvalidArgument):
         ctx.xscale_probe(cfg, 0, None, 1, np.array([0], np.int32), np.array([0], np.int32))
     ctx.trim()
