@@ -376,7 +376,7 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n);
     Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt);
     Launch L = L1(c);
-    const int per = realspace_item_size();
+    const int per = realspace_item_size(nt, cg.ncell);
     int64_t c_lo = 0, c_hi = -1;
     if (nparts > 1) {  // cells are (i dim + j) dim + k: x-slices are contiguous
         const int64_t plane = static_cast<int64_t>(cg.dim) * cg.dim;
@@ -396,7 +396,7 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
                          tgt.pz, tgt.start, items, max_items, nitems, tgt.perm, xi, rc,
-                         c->d_counts, d_uR);
+                         c->d_counts, d_uR, per);
     else if (nt > 0)
         FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
 }

@@ -177,8 +177,9 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, unsigned long long* counts, double* uR);
-int realspace_item_size();  // targets per work item
+                      double xi, double rc, unsigned long long* counts, double* uR, int per);
+// targets per work item (selects the pair kernel: 32 = warp items, else CTA-shared)
+int realspace_item_size(int64_t nt, int64_t ncell);
 // items per cell; only cells in [c_lo, c_hi) get any (c_hi < 0: all cells)
 // the pair kernel's work items (cell, 32-target chunk), heaviest cells first;
 // *nitems (device) = item count; bwork: 3 x realspace_work_buckets() ints

@@ -42,6 +42,7 @@
 //
 // Roofline: FP64 (pair work).
 #include <cmath>
+#include <cstdlib>
 
 #include "fse_internal.cuh"
 
@@ -481,6 +482,222 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-shared variant (small inputs, see realspace_item_size; FSE_RS_WARP=0 forces it).
+//
+// Work item = (target cell, an even share of <= kTB of its targets) = one CTA.
+// The concatenated 27 neighbour buckets are staged ONCE per CTA, in chunks of
+// CAP sources, and shared by all its warps (the warp-item kernel stages them
+// per 32 targets).  A warp takes one target at a time (dynamic counter) and
+// sweeps the chunk, four candidates per lane and round, with the fp32 test of
+// certainly-outside only (d2f > hi); survivors are compacted into a per-warp
+// queue (ballot + popc), and whenever the queue holds 32 entries all 32 lanes
+// evaluate one pair each, so the pair math runs with every lane busy (the
+// warp-item kernel's per-lane mask loop keeps ~20 of 32 busy).  The exact
+// closed-ball test of realspace.cpp:140 is applied to every queued pair, so
+// the accepted set is the reference's.  Each target's sum is split over the
+// lanes in queue order and reduced by a fixed xor tree: deterministic.
+constexpr int kRT = 384, kRW = kRT / 32, kTB = 128, kQ = 160;
+template <int A>
+constexpr int cta_cap() {
+    return A == 3 ? 1536 : 768;  // sources per chunk (whole 128-slot rounds): two CTAs per SM
+}
+
+template <int A>
+struct CtaChunk {
+    static constexpr int CAP = cta_cap<A>();
+    double tab[kDeg + 1][kNI];
+    double sx[CAP], sy[CAP], sz[CAP];
+    double sf[CAP][A];
+    double tx[kTB], ty[kTB], tz[kTB];
+    double tacc[kTB][3];
+    float sxf[CAP], syf[CAP], szf[CAP];  // relative to the cell centre; pads = 3e38
+    int nb_start[27], nb_pref[28];
+    int next_t;
+    unsigned short q[kRW][kQ];
+};
+
+template <int KIND, bool TAIL>
+__global__ void __launch_bounds__(kRT, 2) k_realspace_cta(
+    int dim, const double* __restrict__ spx, const double* __restrict__ spy,
+    const double* __restrict__ spz, const double* __restrict__ sfs,
+    const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
+    const double* __restrict__ tpy, const double* __restrict__ tpz,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ items,
+    const uint32_t* __restrict__ tperm, const int32_t* __restrict__ nitems_dev, double xi,
+    double rc2, double origin, double side, FastTest ft, unsigned long long* __restrict__ counts,
+    double* __restrict__ u) {
+    constexpr int A = KIND == FSE_STRESSLET ? 9 : 3;
+    constexpr int CAP = cta_cap<A>();
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    CtaChunk<A>& S = *reinterpret_cast<CtaChunk<A>*>(rs_smem);
+    const int item = blockIdx.x;
+    if (item >= *nitems_dev) return;  // grid is an upper bound
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cell = items[2 * item], sub = items[2 * item + 1];
+    const int ck = cell % dim, cj = (cell / dim) % dim, ci = cell / (dim * dim);
+    {
+        const double* src = &c_erfcx[0][0];
+        double* dst = &S.tab[0][0];
+        for (int e = threadIdx.x; e < (kDeg + 1) * kNI; e += kRT) dst[e] = src[e];
+    }
+    if (warp == 0) {  // the 27 neighbour buckets, lexicographic (di, dj, dk), prefix-summed
+        int len = 0, st = 0;
+        if (lane < 27) {
+            const int i = ci + lane / 9 - 1, j = cj + (lane / 3) % 3 - 1, k = ck + lane % 3 - 1;
+            if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
+                const int b = (i * dim + j) * dim + k;
+                st = bstart[b];
+                len = bstart[b + 1] - st;
+            }
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane < 27) {
+            S.nb_start[lane] = st;
+            S.nb_pref[lane] = incl - len;
+        }
+        if (lane == 26) S.nb_pref[27] = incl;
+    }
+    // this item's even share of the cell's targets
+    const int t0c = tstart[cell], ntc = tstart[cell + 1] - t0c;
+    const int nsub = (ntc + kTB - 1) / kTB;
+    const int lo = static_cast<int>(static_cast<int64_t>(sub) * ntc / nsub);
+    const int ntb = static_cast<int>(static_cast<int64_t>(sub + 1) * ntc / nsub) - lo;
+    const int q0 = t0c + lo;
+    for (int t = threadIdx.x; t < ntb; t += kRT) {
+        S.tx[t] = tpx[q0 + t];
+        S.ty[t] = tpy[q0 + t];
+        S.tz[t] = tpz[q0 + t];
+        S.tacc[t][0] = S.tacc[t][1] = S.tacc[t][2] = 0.0;
+    }
+    const double cxc = origin + (ci + 0.5) * side, cyc = origin + (cj + 0.5) * side,
+                 czc = origin + (ck + 0.5) * side;
+    __syncthreads();
+    const int total = S.nb_pref[27];
+    unsigned long long npair = 0;
+    unsigned short* q = S.q[warp];
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    static_assert(CAP % 128 == 0, "whole test rounds");
+    for (int base = 0; base < total; base += CAP) {
+        const int cnt = min(CAP, total - base);
+        const int cnt_pad = (cnt + 127) & ~127;  // whole test rounds (CAP % 128 == 0)
+        if (base > 0) __syncthreads();  // every warp is done with the previous chunk
+        for (int e = threadIdx.x; e < cnt_pad; e += kRT) {
+            if (e < cnt) {
+                const int pos = base + e;
+                int r = 0;  // bucket of pos: largest r with nb_pref[r] <= pos
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1)
+                    if (r + stp < 28 && S.nb_pref[r + stp] <= pos) r += stp;
+                while (S.nb_pref[r + 1] <= pos) ++r;  // skip empty buckets
+                const int sidx = S.nb_start[r] + (pos - S.nb_pref[r]);
+                const double vx = spx[sidx], vy = spy[sidx], vz = spz[sidx];
+                S.sx[e] = vx;
+                S.sy[e] = vy;
+                S.sz[e] = vz;
+                S.sxf[e] = rel32(vx - cxc, ft.rm);
+                S.syf[e] = rel32(vy - cyc, ft.rm);
+                S.szf[e] = rel32(vz - czc, ft.rm);
+#pragma unroll
+                for (int c = 0; c < A; ++c) S.sf[e][c] = sfs[static_cast<int64_t>(sidx) * A + c];
+            } else {  // pad: certainly outside in fp32 and in the exact test
+                S.sxf[e] = S.syf[e] = S.szf[e] = 3e38f;
+                S.sx[e] = S.sy[e] = S.sz[e] = 1e300;
+#pragma unroll
+                for (int c = 0; c < A; ++c) S.sf[e][c] = 0.0;
+            }
+        }
+        if (threadIdx.x == 0) S.next_t = 0;
+        __syncthreads();
+        while (true) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&S.next_t, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= ntb) break;
+            const double x = S.tx[t], y = S.ty[t], z = S.tz[t];
+            // a target farther than Rm from its cell centre (outside the box, clamped
+            // into an edge cell): NaN, so every candidate takes the exact test
+            const float xf = rel32(x - cxc, ft.rm), yf = rel32(y - cyc, ft.rm),
+                        zf = rel32(z - czc, ft.rm);
+            const float2 xf2 = make_float2(xf, xf), yf2 = make_float2(yf, yf),
+                         zf2 = make_float2(zf, zf), neg1 = make_float2(-1.0f, -1.0f);
+            double acc[3] = {0.0, 0.0, 0.0};
+            int qn = 0;
+            auto eval = [&](int j) {
+                const double rx = x - S.sx[j], ry = y - S.sy[j], rz = z - S.sz[j];
+                const double d2 = exact_d2(rx, ry, rz);
+                if ((d2 != 0.0) && !(d2 > rc2)) {  // realspace.cpp:140
+                    pair<KIND, TAIL>(rx, ry, rz, d2, xi, S.sf[j], S.tab, acc);
+                    ++npair;
+                }
+            };
+            for (int r0 = 0; r0 < cnt_pad; r0 += 128) {
+                const int e0 = r0 + 4 * lane;
+                const float4 ax = *reinterpret_cast<const float4*>(&S.sxf[e0]);
+                const float4 ay = *reinterpret_cast<const float4*>(&S.syf[e0]);
+                const float4 az = *reinterpret_cast<const float4*>(&S.szf[e0]);
+                const float2 dx0 = __ffma2_rn(make_float2(ax.x, ax.y), neg1, xf2);
+                const float2 dx1 = __ffma2_rn(make_float2(ax.z, ax.w), neg1, xf2);
+                const float2 dy0 = __ffma2_rn(make_float2(ay.x, ay.y), neg1, yf2);
+                const float2 dy1 = __ffma2_rn(make_float2(ay.z, ay.w), neg1, yf2);
+                const float2 dz0 = __ffma2_rn(make_float2(az.x, az.y), neg1, zf2);
+                const float2 dz1 = __ffma2_rn(make_float2(az.z, az.w), neg1, zf2);
+                const float2 d0 = __ffma2_rn(dx0, dx0, __ffma2_rn(dy0, dy0, __fmul2_rn(dz0, dz0)));
+                const float2 d1 = __ffma2_rn(dx1, dx1, __ffma2_rn(dy1, dy1, __fmul2_rn(dz1, dz1)));
+                // keep everything not certainly outside (NaN included)
+                const bool p0 = !(d0.x > ft.hi), p1 = !(d0.y > ft.hi), p2 = !(d1.x > ft.hi),
+                           p3 = !(d1.y > ft.hi);
+                const unsigned b0 = __ballot_sync(0xffffffffu, p0), b1 = __ballot_sync(0xffffffffu, p1),
+                               b2 = __ballot_sync(0xffffffffu, p2), b3 = __ballot_sync(0xffffffffu, p3);
+                const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2);
+                const int o0 = qn + __popc(b0 & lt), o1 = qn + n0 + __popc(b1 & lt);
+                const int o2 = qn + n0 + n1 + __popc(b2 & lt);
+                const int o3 = qn + n0 + n1 + n2 + __popc(b3 & lt);
+                if (p0) q[o0] = static_cast<unsigned short>(e0);
+                if (p1) q[o1] = static_cast<unsigned short>(e0 + 1);
+                if (p2) q[o2] = static_cast<unsigned short>(e0 + 2);
+                if (p3) q[o3] = static_cast<unsigned short>(e0 + 3);
+                qn += n0 + n1 + n2 + __popc(b3);
+                __syncwarp();
+                while (qn >= 32) {
+                    qn -= 32;
+                    eval(q[qn + lane]);
+                }
+                __syncwarp();  // the entries just read may be overwritten by the next round
+            }
+            if (lane < qn) eval(q[lane]);
+            __syncwarp();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+                acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], o);
+                acc[2] += __shfl_xor_sync(0xffffffffu, acc[2], o);
+            }
+            if (lane == 0) {
+                S.tacc[t][0] += acc[0];
+                S.tacc[t][1] += acc[1];
+                S.tacc[t][2] += acc[2];
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) npair += __shfl_xor_sync(0xffffffffu, npair, o);
+    if (lane == 0 && npair) atomicAdd(counts + 1, npair);
+    if (threadIdx.x == 0)
+        atomicAdd(counts, static_cast<unsigned long long>(ntb) * static_cast<unsigned long long>(total));
+    for (int e = threadIdx.x; e < 3 * ntb; e += kRT) {
+        const int t = e / 3, c = e - 3 * t;
+        u[3 * static_cast<int64_t>(tperm[q0 + t]) + c] = S.tacc[t][c];
+    }
+}
+
 // Work items are scheduled heaviest cell first: the pair work of a cell is
 // (its targets) x (sources in its 27 neighbour buckets), which varies by two
 // orders of magnitude on clustered input (cfg4), and a heavy item dispatched
@@ -615,7 +832,21 @@ void ensure_tables() {
 
 }  // namespace
 
-int realspace_item_size() { return 32; }
+// Which pair kernel: the warp-item kernel (32 targets per item) unless its items
+// cannot fill the GPU -- fewer than ~2000 warps, e.g. cfg1's 216 cells of ~46
+// targets -- where the CTA-shared kernel (kTB targets per item, 12 warps sharing
+// one staged neighbourhood) is faster (cfg1 0.136 -> 0.048 ms).  On large inputs
+// the warp-item kernel wins (cfg2 5.17 vs 5.25 ms, cfg3 2.33 vs 2.83, cfg4 91 vs
+// 100: profiles/r02/cfg2_realspace_cta_kernel.md).  FSE_RS_WARP=1 / 0 forces one.
+int realspace_item_size(int64_t nt, int64_t ncell) {
+    static const int forced = [] {
+        const char* e = std::getenv("FSE_RS_WARP");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (forced >= 0) return forced ? 32 : kTB;
+    const int64_t warp_items = std::min<int64_t>(ncell, nt) + (nt + 31) / 32;
+    return warp_items < 2000 ? kTB : 32;
+}
 
 void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
                             int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
@@ -648,16 +879,39 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, unsigned long long* counts, double* uR) {
+                      double xi, double rc, unsigned long long* counts, double* uR, int per) {
     (void)ns;
     if (max_items <= 0) return;
     ensure_tables();
     const double rc2 = rc * rc;
     const FastTest ft = fp32_bounds(rc, cg.side);
-    const unsigned b = static_cast<unsigned>((max_items + TPB / 32 - 1) / (TPB / 32));
-    const size_t sm3 = sizeof(WarpChunk<3>) * (TPB / 32), sm9 = sizeof(WarpChunk<9>) * (TPB / 32);
     // the table covers x = xi r < 6.5; past it (xi rc >= 6.5) the exact tail
     const bool tail = xi * rc >= kXMax * (1.0 - 1e-9);
+    if (per == kTB) {  // CTA-shared kernel: the items were built with kTB targets each
+        const unsigned b = static_cast<unsigned>(max_items);
+        auto go = [&](auto kern, size_t sm) {
+            FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+            kern<<<b, kRT, sm, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy, tpz,
+                                      tcell_start, items, tperm, nitems_dev, xi, rc2, cg.origin,
+                                      cg.side, ft, counts, uR);
+        };
+        const size_t sm3 = sizeof(CtaChunk<3>), sm9 = sizeof(CtaChunk<9>);
+        if (kind == FSE_STOKESLET)
+            tail ? go(k_realspace_cta<FSE_STOKESLET, true>, sm3)
+                 : go(k_realspace_cta<FSE_STOKESLET, false>, sm3);
+        else if (kind == FSE_STRESSLET)
+            tail ? go(k_realspace_cta<FSE_STRESSLET, true>, sm9)
+                 : go(k_realspace_cta<FSE_STRESSLET, false>, sm9);
+        else
+            tail ? go(k_realspace_cta<FSE_ROTLET, true>, sm3)
+                 : go(k_realspace_cta<FSE_ROTLET, false>, sm3);
+        FSE_LAUNCH_CHECK();
+        ++*L.launches;
+        return;
+    }
+    const unsigned b = static_cast<unsigned>((max_items + TPB / 32 - 1) / (TPB / 32));
+    const size_t sm3 = sizeof(WarpChunk<3>) * (TPB / 32), sm9 = sizeof(WarpChunk<9>) * (TPB / 32);
     auto go = [&](auto kern, size_t sm) {
         FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
