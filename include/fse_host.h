@@ -57,6 +57,13 @@ fse_status fse_reference_velocity_rms(int kind, double Q, double L, uint64_t N, 
 fse_status fse_select_parameters(int kind, uint64_t N, double L, double Q, double xi, double tol,
                                  fse_config* out, int* feasible);
 
+/* Host-only planner query (no GPU needed): can the FFT passes of a grid of D = 2 Mtilde
+ * points run for this kernel kind?  FSE_OK, or FSE_EINVAL when D exceeds the engines
+ * (total_sum / fourier_sum then fail the same way before allocating anything).
+ * *engine: 0 Stockham (generic_stage = 1: with a generic O(p^2) first stage),
+ * 1-4 register engines 624 / 1200 / 704 / 242, 5-7 Bluestein on 400 / 624 / 1024. */
+fse_status fse_fft_plan_query(int D, int kind, int* engine, int* generic_stage);
+
 #ifdef __cplusplus
 }
 #endif

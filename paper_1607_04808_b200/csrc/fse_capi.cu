@@ -41,6 +41,7 @@
 #include <vector>
 
 #include "fse_internal.cuh"
+#include "fse_host.h"
 #include "k_fft.cuh"
 
 namespace fsecu {
@@ -1539,6 +1540,23 @@ fse_status fse_cuda_xscale_probe(fse_cuda_ctx* c, const fse_config* cfg, int kin
         d2h(c, out, dout, no * sizeof(double2));
         d2h(c, gcol, dg, sizeof(double) * nprobe * g.D);
     });
+}
+
+// host-only: the FFT planner's verdict for a grid size (include/fse_host.h)
+fse_status fse_fft_plan_query(int D, int kind, int* engine, int* generic_stage) {
+    try {
+        if (D < 2 || D % 2) throw Error(FSE_EINVAL, "fft_plan_query: D must be even and >= 2");
+        check_kind(kind);
+        const HostFftPlan h = make_fft_plan(D);
+        if (engine) *engine = h.eng;
+        if (generic_stage) *generic_stage = h.generic ? 1 : 0;
+        fft_xscale_check(h, kind);
+        return FSE_OK;
+    } catch (const Error& e) {
+        return e.code;
+    } catch (const std::exception&) {
+        return FSE_ERUNTIME;
+    }
 }
 
 fse_status fse_cuda_fft3d(fse_cuda_ctx* c, double* data, int n0, int n1, int n2, int inverse) {

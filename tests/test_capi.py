@@ -110,3 +110,31 @@ def test_rms_error_and_self_interaction(fse):
     v = fse.self_interaction(2.0, [1.0, 2.0, 3.0], fse.KernelKind.Stokeslet)
     assert np.allclose(v, -8.0 / np.sqrt(np.pi) * np.array([1, 2, 3]))
     assert np.all(fse.self_interaction(2.0, [1.0, 2.0, 3.0], fse.KernelKind.Rotlet) == 0)
+
+
+def test_fft_planner_verdicts_without_a_gpu(fse):
+    """fse_fft_plan_query (host only): every BASELINE grid and tolerance-consistent
+    variant has an engine -- including cfg5t's D = 1730 = 2 x 5 x 173 (Stockham with a
+    generic first stage) -- and a grid beyond the engines is refused with
+    invalid_argument, the status total_sum returns before allocating anything."""
+    lib = ctypes.CDLL(fse.library_path())
+    lib.fse_fft_plan_query.restype = ctypes.c_int
+    lib.fse_fft_plan_query.argtypes = [ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+
+    def query(D, kind=0):
+        e, g = ctypes.c_int(-1), ctypes.c_int(-1)
+        st = lib.fse_fft_plan_query(D, kind, ctypes.byref(e), ctypes.byref(g))
+        return st, e.value, g.value
+
+    assert query(624) == (0, 1, 0)       # cfg2 / cfg4: register engine 24 x 26
+    assert query(1200) == (0, 2, 0)      # cfg5: 30 x 40
+    assert query(704) == (0, 3, 0)       # cfg4t
+    assert query(242) == (0, 4, 0)       # cfg1t
+    for D in (194, 298, 348):            # cfg1, cfg3, cfg3t: Bluestein engines
+        st, e, g = query(D, 1)
+        assert st == 0 and e in (5, 6, 7) and g == 0
+    assert query(888) == (0, 0, 1)       # cfg2t: generic stage of radix 37
+    assert query(1730) == (0, 0, 1)      # cfg5t: generic stage of radix 173
+    assert query(2018)[0] == 1           # 2 x 1009: FSE_EINVAL
+    assert query(623)[0] == 1 and query(624, 7)[0] == 1

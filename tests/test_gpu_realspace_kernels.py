@@ -1,0 +1,72 @@
+"""The two real-space pair kernels (k_realspace: warp items; k_realspace_cta:
+CTA-shared neighbourhood, dispatched on small inputs) against each other and
+the oracle, each forced through FSE_RS_WARP in a fresh process (the choice is
+read once per process): the ACCEPTED PAIR COUNT must be identical -- the
+closed-ball set of realspace.cpp:140 -- and equal to a brute-force count, and
+the sums agree to 1e-13 (1 + |u|) per target on uniform and clustered input
+(cells of very different weight, several source chunks per cell)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1607_04808_b200 as fse
+kind, n, clustered, out = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]
+rng = np.random.default_rng(77)
+if clustered:
+    c = rng.uniform(0.2, 0.8, (6, 3))
+    pos = np.clip(c[rng.integers(0, 6, n)] + 0.03 * rng.standard_normal((n, 3)), 0.0, 1.0 - 1e-12)
+else:
+    pos = rng.uniform(0, 1, (n, 3))
+a = fse.strength_arity(kind)
+s = fse.SourceSystem(pos, rng.standard_normal((n, a)), 1.0)
+ctx = fse.Context(0)
+u = ctx.real_space_sum(s, kind, 20.0, 0.08, pos)
+cand, pairs = ctx.realspace_counts()
+np.save(out, u)
+print(json.dumps(dict(cand=int(cand), pairs=int(pairs))))
+"""
+
+
+def run_child(tmp_path, warp, kind, n, clustered):
+    out = str(tmp_path / f"u_{warp}_{kind}_{n}_{clustered}.npy")
+    env = dict(os.environ, FSE_RS_WARP=str(warp))
+    r = subprocess.run([sys.executable, "-c", CHILD, ROOT, str(kind), str(n), str(clustered), out],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(out), json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("kind,n,clustered", [(0, 30000, 0), (2, 30000, 1), (1, 20000, 1)])
+def test_pair_kernels_agree(tmp_path, kind, n, clustered):
+    uw, cw = run_child(tmp_path, 1, kind, n, clustered)
+    uc, cc = run_child(tmp_path, 0, kind, n, clustered)
+    assert cw["pairs"] == cc["pairs"] and cw["cand"] == cc["cand"], (cw, cc)
+    err = np.linalg.norm(uw - uc, axis=1) / (1 + np.linalg.norm(uw, axis=1))
+    assert err.max() <= 1e-13, err.max()
+    # brute-force count of the closed ball 0 < d2 <= rc^2 with the reference's
+    # rounding (realspace.cpp:140: (dx*dx + dy*dy) + dz*dz), on a subset of targets
+    rng = np.random.default_rng(77)
+    if clustered:
+        c = rng.uniform(0.2, 0.8, (6, 3))
+        pos = np.clip(c[rng.integers(0, 6, n)] + 0.03 * rng.standard_normal((n, 3)), 0.0,
+                      1.0 - 1e-12)
+    else:
+        pos = rng.uniform(0, 1, (n, 3))
+    total = 0
+    for lo in range(0, n, 500):
+        d = pos[lo:lo + 500, None, :] - pos[None, :, :]
+        d2 = (d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]) + d[..., 2] * d[..., 2]
+        total += int(np.count_nonzero((d2 != 0.0) & ~(d2 > 0.08 * 0.08)))
+    assert total == cw["pairs"], (total, cw)
