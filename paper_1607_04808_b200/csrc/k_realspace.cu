@@ -497,10 +497,24 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
 // closed-ball test of realspace.cpp:140 is applied to every queued pair, so
 // the accepted set is the reference's.  Each target's sum is split over the
 // lanes in queue order and reduced by a fixed xor tree: deterministic.
-constexpr int kRT = 384, kRW = kRT / 32, kTB = 128, kQ = 160;
+// 384 threads, two CTAs per SM, chunks of 1536 (768 for the stresslet's nine
+// strengths) sources: ~108 KB of shared memory per CTA.  Build parameters for A/B.
+#ifndef FSE_RSC_T
+#define FSE_RSC_T 384
+#endif
+#ifndef FSE_RSC_MINB
+#define FSE_RSC_MINB 2
+#endif
+#ifndef FSE_RSC_CAP3
+#define FSE_RSC_CAP3 1536
+#endif
+#ifndef FSE_RSC_CAP9
+#define FSE_RSC_CAP9 768
+#endif
+constexpr int kRT = FSE_RSC_T, kRW = kRT / 32, kTB = 128, kQ = 160;
 template <int A>
 constexpr int cta_cap() {
-    return A == 3 ? 1536 : 768;  // sources per chunk (whole 128-slot rounds): two CTAs per SM
+    return A == 3 ? FSE_RSC_CAP3 : FSE_RSC_CAP9;  // sources per chunk (whole 128-slot rounds)
 }
 
 template <int A>
@@ -518,7 +532,7 @@ struct CtaChunk {
 };
 
 template <int KIND, bool TAIL>
-__global__ void __launch_bounds__(kRT, 2) k_realspace_cta(
+__global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
     int dim, const double* __restrict__ spx, const double* __restrict__ spy,
     const double* __restrict__ spz, const double* __restrict__ sfs,
     const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
@@ -533,7 +547,11 @@ __global__ void __launch_bounds__(kRT, 2) k_realspace_cta(
     CtaChunk<A>& S = *reinterpret_cast<CtaChunk<A>*>(rs_smem);
     const int item = blockIdx.x;
     if (item >= *nitems_dev) return;  // grid is an upper bound
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // lane from the special register through a volatile asm: the compiler otherwise
+    // rematerialises it from %tid inside the test round (S2R latency, 4% of the stalls)
+    int lane;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+    const int warp = threadIdx.x >> 5;
     const int cell = items[2 * item], sub = items[2 * item + 1];
     const int ck = cell % dim, cj = (cell / dim) % dim, ci = cell / (dim * dim);
     {
