@@ -119,7 +119,7 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
 void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts);
 // cell ids of points for the reference cell list (realspace.cpp:60-63,80)
 void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
-                     int dim, uint32_t* cell);
+                     int dim, uint32_t* cell, int fine = 0);
 // SoA permute of positions (+ strengths) by perm
 void launch_permute_soa(const Launch& L, const double* pos, const double* str, int a,
                         const uint32_t* perm, int64_t n, double* px, double* py, double* pz,
@@ -186,7 +186,10 @@ int realspace_item_size(int64_t nt, int64_t ncell);
 int realspace_work_buckets();
 void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
                             int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
-                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems);
+                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems,
+                            int oct_min = 0);
+// cells with at least this many targets are split into octant items (0: never)
+int realspace_octant_threshold();
 
 // epilogue: u[perm] = uF + uR (+ self) -------------------------------------
 // u = uF + uR (+ self_coef * f for the stokeslet self term), caller order

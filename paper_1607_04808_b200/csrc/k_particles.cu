@@ -146,17 +146,24 @@ __global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_
     if (q < n) atomicAdd(&counts[keys[q]], 1);
 }
 
+// fine: key = 8 cell + octant, octant bit per axis = (coordinate >= cell centre): the
+// real-space kernel's own ordering (octant items of dense cells, k_realspace.cu); the
+// cell itself is the reference's (realspace.cpp:78-84) either way
 __global__ void k_cell_ids(const double* __restrict__ pos, int64_t n, double origin, double side,
-                           int dim, uint32_t* __restrict__ cell) {
+                           int dim, int fine, uint32_t* __restrict__ cell) {
     const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (q >= n) return;
     int c[3];
+    uint32_t oct = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        int v = static_cast<int>(floor(__ddiv_rn(__dsub_rn(pos[3 * q + a], origin), side)));
+        const double x = pos[3 * q + a];
+        int v = static_cast<int>(floor(__ddiv_rn(__dsub_rn(x, origin), side)));
         c[a] = v < 0 ? 0 : (v > dim - 1 ? dim - 1 : v);
+        oct = (oct << 1) | (x >= origin + (c[a] + 0.5) * side ? 1u : 0u);
     }
-    cell[q] = (static_cast<uint32_t>(c[0]) * dim + c[1]) * dim + c[2];
+    const uint32_t id = (static_cast<uint32_t>(c[0]) * dim + c[1]) * dim + c[2];
+    cell[q] = fine ? id * 8u + oct : id;
 }
 
 __global__ void k_permute_soa(const double* __restrict__ pos, const double* __restrict__ str,
@@ -234,9 +241,9 @@ void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t*
 }
 
 void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
-                     int dim, uint32_t* cell) {
+                     int dim, uint32_t* cell, int fine) {
     if (n <= 0) return;
-    k_cell_ids<<<blocks_for(n), TPB, 0, L.s>>>(pos, n, origin, side, dim, cell);
+    k_cell_ids<<<blocks_for(n), TPB, 0, L.s>>>(pos, n, origin, side, dim, fine, cell);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }

@@ -1,8 +1,12 @@
 // k_realspace.cu -- screened real-space pair sum (realspace.cpp:86-149) with
 // the screened kernels of realspace.cpp:13-58.
 //
+// Sources and targets are sorted by (cell, octant of the cell) -- the kernels' own
+// order; the reference's CellList order is kept for build_cell_list only.
 // Work item = (target cell, up to 32 of its targets) = one warp, one lane
 // per target; a CTA runs 8 independent items (no CTA barrier in the loop).
+// Dense cells (>= 640 targets) are cut into octant items, whose neighbourhood is
+// 125 of the 216 (cell, octant) sub-buckets.
 // The 27 neighbour buckets (lexicographic (di,dj,dk)) are concatenated
 // virtually and sampled with a coprime stride (so every chunk mixes all
 // buckets and the lanes accept similar numbers of pairs), then streamed
@@ -258,12 +262,16 @@ __device__ __forceinline__ float rel32(double v, double rm) {
     return fabs(v) <= rm ? static_cast<float>(v) : __int_as_float(0x7fffffff);
 }
 
+// Neighbour list entries per item: the 27 buckets of a cell item, or the <= 125
+// (cell, octant) sub-buckets an octant item can reach (see k_realspace below)
+constexpr int kNB = 128;
+
 template <int A>
 struct WarpChunk {
     float sxf[CH], syf[CH], szf[CH];  // SoA: two candidates per packed fp32 op
     double sx[CH], sy[CH], sz[CH];
     double sf[CH][A];
-    int nb_start[27], nb_pref[28];
+    int nb_start[kNB], nb_pref[kNB + 1];
 };
 
 template <int KIND, bool TAIL>
@@ -303,33 +311,88 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     const int item = blockIdx.x * W + warp;
     if (item >= *nitems_dev) return;  // grid is an upper bound
     const int cell = items[2 * item];
-    const int sub = items[2 * item + 1];
+    const int sub = items[2 * item + 1] & 0xffffff;
+    const int oct = (items[2 * item + 1] >> 24) - 1;  // -1: the whole cell; else its octant
     const int ck = cell % dim, cj = (cell / dim) % dim, ci = cell / (dim * dim);
-    // the 27 neighbour buckets in lexicographic (di, dj, dk) order, prefix-summed
+    // Neighbour list, prefix-summed.  bstart / tstart hold (cell, octant) bucket
+    // starts: cell b is [bstart[8b], bstart[8b + 8]).  A cell item takes the 27
+    // neighbour cells.  An octant item (targets of octant (a_x, a_y, a_z) of a dense
+    // cell) takes per axis both halves of its own cell, and of a neighbour cell only
+    // the near half when the neighbour lies on the far side of the target's half:
+    // a target with x < cx_i and a source with x >= cx_{i+1} are more than one cell
+    // side > rc apart (bits are comparisons against the same centres, k_cell_ids), so
+    // no accepted pair is dropped: 125 of the 216 sub-buckets remain.
     {
-        int len = 0, st = 0;
-        if (lane < 27) {
-            const int i = ci + lane / 9 - 1, j = cj + (lane / 3) % 3 - 1, k = ck + lane % 3 - 1;
-            if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
-                const int b = (i * dim + j) * dim + k;
-                st = bstart[b];
-                len = bstart[b + 1] - st;
+        int n_nb = 0;  // entries so far (warp-uniform)
+        const int ne = oct < 0 ? 27 : 216;
+        for (int e0 = 0; e0 < ne; e0 += 32) {
+            const int e = e0 + lane;
+            int st = 0, len = 0;
+            bool use = false;
+            if (e < ne) {
+                const int nc = oct < 0 ? e : e >> 3, so = e & 7;
+                const int di = nc / 9 - 1, dj = (nc / 3) % 3 - 1, dk = nc % 3 - 1;
+                const int i = ci + di, j = cj + dj, k = ck + dk;
+                if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
+                    const int b = (i * dim + j) * dim + k;
+                    if (oct < 0) {
+                        st = bstart[8 * b];
+                        len = bstart[8 * b + 8] - st;
+                        use = len > 0;
+                    } else {
+                        // keep (d, source bit s) unless the neighbour is on the far side:
+                        // d = -1 needs s = 1 when the target bit is 1; d = +1 needs s = 0
+                        // when the target bit is 0
+                        const int ax = (oct >> 2) & 1, ay = (oct >> 1) & 1, az = oct & 1;
+                        const int sx = (so >> 2) & 1, sy = (so >> 1) & 1, sz = so & 1;
+                        const bool kx = di == 0 || (di < 0 ? (ax == 0 || sx == 1) : (ax == 1 || sx == 0));
+                        const bool ky = dj == 0 || (dj < 0 ? (ay == 0 || sy == 1) : (ay == 1 || sy == 0));
+                        const bool kz = dk == 0 || (dk < 0 ? (az == 0 || sz == 1) : (az == 1 || sz == 0));
+                        if (kx && ky && kz) {
+                            st = bstart[8 * b + so];
+                            len = bstart[8 * b + so + 1] - st;
+                            use = len > 0;
+                        }
+                    }
+                }
             }
+            const unsigned m = __ballot_sync(0xffffffffu, use);
+            if (use) {
+                const int o = n_nb + __popc(m & ((1u << lane) - 1u));
+                nb_start[o] = st;
+                nb_pref[o] = len;  // lengths first, scanned below
+            }
+            n_nb += __popc(m);
         }
-        int incl = len;
+        __syncwarp();
+        // exclusive scan of the lengths, four entries per lane
+        int v[4], tot = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int o = 4 * lane + i;
+            v[i] = o < n_nb ? nb_pref[o] : 0;
+            tot += v[i];
+        }
+        int incl = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (lane < 27) {
-            nb_start[lane] = st;
-            nb_pref[lane] = incl - len;
+        const int total_all = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        int run = incl - tot;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            nb_pref[4 * lane + i] = run;  // entries past n_nb hold the total
+            run += v[i];
         }
-        if (lane == 26) nb_pref[27] = incl;
+        if (lane == 0) nb_pref[kNB] = total_all;
     }
-    const int q = tstart[cell] + sub * 32 + lane;
-    const bool valid = q < tstart[cell + 1];
+    const int tb = oct < 0 ? tstart[8 * cell] : tstart[8 * cell + oct];
+    const int te = oct < 0 ? tstart[8 * cell + 8] : tstart[8 * cell + oct + 1];
+    const int q = tb + sub * 32 + lane;
+    const bool valid = q < te;
     double x = 0, y = 0, z = 0;
     if (valid) {
         x = tpx[q];
@@ -344,7 +407,7 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     const float zf = valid ? rel32(z - czc, ft.rm) : 3e38f;
     double acc[3] = {0.0, 0.0, 0.0};
     __syncwarp();
-    const int total = nb_pref[27];
+    const int total = nb_pref[kNB];
     unsigned long long ncand = 0, npair = 0;  // work counters (roofline)
     // Chunks sample the neighbourhood with a coprime stride S ~ 0.618 total,
     // so every chunk mixes sources from all 27 buckets and each lane accepts
@@ -363,11 +426,10 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
             const int v = base + slot;
             if (v < total) {
                 const int pos = static_cast<int>((static_cast<int64_t>(v) * S) % total);
-                int r = 0;  // bucket of pos: largest r with nb_pref[r] <= pos
+                int r = 0;  // entry of pos: largest r with nb_pref[r] <= pos (none is empty)
 #pragma unroll
-                for (int stp = 16; stp > 0; stp >>= 1)
-                    if (r + stp < 28 && nb_pref[r + stp] <= pos) r += stp;
-                while (nb_pref[r + 1] <= pos) ++r;  // skip empty buckets
+                for (int stp = kNB / 2; stp > 0; stp >>= 1)
+                    if (nb_pref[r + stp] <= pos) r += stp;
                 const int sidx = nb_start[r] + (pos - nb_pref[r]);
                 const double vx = spx[sidx], vy = spy[sidx], vz = spz[sidx];
                 sx[slot] = vx;
@@ -565,8 +627,8 @@ __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
             const int i = ci + lane / 9 - 1, j = cj + (lane / 3) % 3 - 1, k = ck + lane % 3 - 1;
             if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
                 const int b = (i * dim + j) * dim + k;
-                st = bstart[b];
-                len = bstart[b + 1] - st;
+                st = bstart[8 * b];  // (cell, octant) bucket starts
+                len = bstart[8 * b + 8] - st;
             }
         }
         int incl = len;
@@ -582,7 +644,7 @@ __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
         if (lane == 26) S.nb_pref[27] = incl;
     }
     // this item's even share of the cell's targets
-    const int t0c = tstart[cell], ntc = tstart[cell + 1] - t0c;
+    const int t0c = tstart[8 * cell], ntc = tstart[8 * cell + 8] - t0c;
     const int nsub = (ntc + kTB - 1) / kTB;
     const int lo = static_cast<int>(static_cast<int64_t>(sub) * ntc / nsub);
     const int ntb = static_cast<int>(static_cast<int64_t>(sub + 1) * ntc / nsub) - lo;
@@ -725,12 +787,25 @@ __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
 // every item computes the same targets' sums in the same order.
 constexpr int kWorkBuckets = 32;
 
+// sstart / tstart: (cell, octant) bucket starts (8 ncell + 1).  oct_min > 0: a cell
+// with at least that many targets is cut into one item list per octant (item word 1 =
+// sub | (octant + 1) << 24), whose neighbourhood is 125 of the 216 sub-buckets.
+__device__ __forceinline__ int cell_items(const int32_t* __restrict__ tstart, int64_t c, int per,
+                                          int oct_min) {
+    const int nt = tstart[8 * c + 8] - tstart[8 * c];
+    if (oct_min <= 0 || nt < oct_min) return (nt + per - 1) / per;
+    int n = 0;
+    for (int o = 0; o < 8; ++o) n += (tstart[8 * c + o + 1] - tstart[8 * c + o] + per - 1) / per;
+    return n;
+}
+
 __global__ void k_cell_bucket(const int32_t* __restrict__ sstart, const int32_t* __restrict__ tstart,
                               int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
-                              uint8_t* __restrict__ bucket, int32_t* __restrict__ bcount) {
+                              int oct_min, uint8_t* __restrict__ bucket,
+                              int32_t* __restrict__ bcount) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncell) return;
-    const int nt = tstart[c + 1] - tstart[c];
+    const int nt = tstart[8 * c + 8] - tstart[8 * c];
     if (nt <= 0 || c < c_lo || c >= c_hi) return;
     const int ck = static_cast<int>(c % dim), cj = static_cast<int>((c / dim) % dim),
               ci = static_cast<int>(c / (static_cast<int64_t>(dim) * dim));
@@ -741,13 +816,13 @@ __global__ void k_cell_bucket(const int32_t* __restrict__ sstart, const int32_t*
                 const int i = ci + di, j = cj + dj, k = ck + dk;
                 if (i < 0 || i >= dim || j < 0 || j >= dim || k < 0 || k >= dim) continue;
                 const int64_t b = (static_cast<int64_t>(i) * dim + j) * dim + k;
-                cand += sstart[b + 1] - sstart[b];
+                cand += sstart[8 * b + 8] - sstart[8 * b];
             }
     const unsigned long long work = static_cast<unsigned long long>(nt) * (cand + 1);
     const int lg = 63 - __clzll(static_cast<long long>(work));  // floor(log2 work)
     const int bk = max(0, kWorkBuckets - 1 - lg);
     bucket[c] = static_cast<uint8_t>(bk);
-    atomicAdd(bcount + bk, (nt + per - 1) / per);
+    atomicAdd(bcount + bk, cell_items(tstart, c, per, oct_min));
 }
 
 // one warp: bucket offsets (exclusive scan), item total for the pair kernel
@@ -766,18 +841,28 @@ __global__ void k_bucket_scan(const int32_t* __restrict__ bcount, int32_t* __res
 }
 
 __global__ void k_fill_items(const int32_t* __restrict__ tstart, const uint8_t* __restrict__ bucket,
-                             int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
+                             int64_t ncell, int per, int64_t c_lo, int64_t c_hi, int oct_min,
                              const int32_t* __restrict__ boff, int32_t* __restrict__ bcur,
                              int32_t* __restrict__ items) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncell) return;
-    const int nt = tstart[c + 1] - tstart[c];
+    const int nt = tstart[8 * c + 8] - tstart[8 * c];
     if (nt <= 0 || c < c_lo || c >= c_hi) return;
-    const int n = (nt + per - 1) / per, bk = bucket[c];
-    const int32_t base = boff[bk] + atomicAdd(bcur + bk, n);
-    for (int s = 0; s < n; ++s) {
-        items[2 * (base + s)] = static_cast<int32_t>(c);
-        items[2 * (base + s) + 1] = s;
+    const int n = cell_items(tstart, c, per, oct_min), bk = bucket[c];
+    int32_t at = boff[bk] + atomicAdd(bcur + bk, n);
+    if (oct_min <= 0 || nt < oct_min) {
+        for (int s = 0; s < n; ++s, ++at) {
+            items[2 * at] = static_cast<int32_t>(c);
+            items[2 * at + 1] = s;
+        }
+        return;
+    }
+    for (int o = 0; o < 8; ++o) {
+        const int no = (tstart[8 * c + o + 1] - tstart[8 * c + o] + per - 1) / per;
+        for (int s = 0; s < no; ++s, ++at) {
+            items[2 * at] = static_cast<int32_t>(c);
+            items[2 * at + 1] = s | ((o + 1) << 24);
+        }
     }
 }
 
@@ -868,7 +953,8 @@ int realspace_item_size(int64_t nt, int64_t ncell) {
 
 void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
                             int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
-                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems) {
+                            uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems,
+                            int oct_min) {
     if (c_hi < 0) c_hi = ncell;
     int32_t* bcount = bwork;
     int32_t* boff = bwork + kWorkBuckets;
@@ -876,21 +962,36 @@ void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_
     FSE_CU(cudaMemsetAsync(bwork, 0, 3 * kWorkBuckets * sizeof(int32_t), L.s));
     const unsigned blocks = static_cast<unsigned>((ncell + 255) / 256);
     if (blocks > 0) {
-        k_cell_bucket<<<blocks, 256, 0, L.s>>>(sstart, tstart, dim, ncell, per, c_lo, c_hi, bucket,
-                                               bcount);
+        k_cell_bucket<<<blocks, 256, 0, L.s>>>(sstart, tstart, dim, ncell, per, c_lo, c_hi, oct_min,
+                                               bucket, bcount);
         FSE_LAUNCH_CHECK();
     }
     k_bucket_scan<<<1, 32, 0, L.s>>>(bcount, boff, nitems);
     FSE_LAUNCH_CHECK();
     if (blocks > 0) {
-        k_fill_items<<<blocks, 256, 0, L.s>>>(tstart, bucket, ncell, per, c_lo, c_hi, boff, bcur,
-                                              items);
+        k_fill_items<<<blocks, 256, 0, L.s>>>(tstart, bucket, ncell, per, c_lo, c_hi, oct_min, boff,
+                                              bcur, items);
         FSE_LAUNCH_CHECK();
     }
     *L.launches += blocks > 0 ? 3 : 1;
 }
 
 int realspace_work_buckets() { return kWorkBuckets; }
+
+// Cells with at least this many targets are cut into octant items (42% fewer
+// candidates each, at the price of up to eight partially filled items per cell).
+// Measured on B200 (real-space ms at thresholds off / 128 / 320 / 640): cfg4 85.0 /
+// 82.9 / 82.6 / 82.3, cfg3 2.31 / 2.69 / 2.69 / 2.33, cfg2 (no cell that dense) 5.19.
+// The (cell, octant) order alone -- the 32 targets of an item are neighbours, so on
+// clustered input their lanes accept similar numbers of pairs -- took cfg4 from 91.4
+// to 85.0 ms.  FSE_RS_OCT overrides (0: never).
+int realspace_octant_threshold() {
+    static const int t = [] {
+        const char* e = std::getenv("FSE_RS_OCT");
+        return e ? std::atoi(e) : 640;
+    }();
+    return t;
+}
 
 void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const double* spx,
                       const double* spy, const double* spz, const double* sfs, int64_t ns,

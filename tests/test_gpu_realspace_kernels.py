@@ -52,7 +52,8 @@ def run_child(tmp_path, warp, kind, n, clustered):
 def test_pair_kernels_agree(tmp_path, kind, n, clustered):
     uw, cw = run_child(tmp_path, 1, kind, n, clustered)
     uc, cc = run_child(tmp_path, 0, kind, n, clustered)
-    assert cw["pairs"] == cc["pairs"] and cw["cand"] == cc["cand"], (cw, cc)
+    # candidates may differ (octant items of dense cells test 125 of 216 sub-buckets)
+    assert cw["pairs"] == cc["pairs"] and cw["cand"] <= cc["cand"], (cw, cc)
     err = np.linalg.norm(uw - uc, axis=1) / (1 + np.linalg.norm(uw, axis=1))
     assert err.max() <= 1e-13, err.max()
     # brute-force count of the closed ball 0 < d2 <= rc^2 with the reference's
