@@ -336,22 +336,21 @@ struct Cells {
     double *px = nullptr, *py = nullptr, *pz = nullptr, *fs = nullptr;
 };
 
-// fine: sorted by (cell, octant) with 8 ncell + 1 bucket starts (the real-space
-// kernels' own order; cell c is [start[8c], start[8c + 8])); otherwise the
-// reference's CellList order (build_cell_list)
+// sub > 1: sorted by (cell, sub-cell) with sub * ncell + 1 bucket starts (the
+// real-space kernels' own order; cell c is [start[sub c], start[sub c + sub]));
+// sub = 1: the reference's CellList order (build_cell_list)
 Cells bin_cells(fse_cuda_ctx* c, const CellGrid& cg, const std::string& tag, const double* d_pos,
-                const double* d_str, int a, int64_t n, bool fine = false) {
+                const double* d_str, int a, int64_t n, int sub = 1) {
     Launch L = L1(c);
     Cells r;
-    const int64_t nkeys = fine ? 8 * cg.ncell : cg.ncell;
-    if (nkeys >= (int64_t(1) << 31)) invalid("real_space_sum: cell grid too large");
+    const int64_t nkeys = sub * cg.ncell;
     uint32_t* cell = buf<uint32_t>(c, tag + "cell", n);
     uint32_t* cell2 = buf<uint32_t>(c, tag + "cell2", n);
     uint32_t* iota = buf<uint32_t>(c, tag + "iota", n);
     r.perm = buf<uint32_t>(c, tag + "perm", n);
     int32_t* counts = buf<int32_t>(c, tag + "counts", nkeys + 1);
     r.start = buf<int32_t>(c, tag + "start", nkeys + 1);
-    launch_cell_ids(L, d_pos, n, cg.origin, cg.side, cg.dim, cell, fine ? 1 : 0);
+    launch_cell_ids(L, d_pos, n, cg.origin, cg.side, cg.dim, cell, sub);
     launch_iota(L, iota, n);
     if (n > 0) sort_pairs(c, c->s1, "s1", cell, cell2, iota, r.perm, n, bits_for(nkeys));
     FSE_CU(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nkeys + 1), c->s1));
@@ -379,13 +378,18 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     if (!(xi > 0) || !(rc > 0)) invalid("real_space_sum: xi and rc must be positive");
     const int a = arity_of(kind);
     const CellGrid cg = cell_grid(n_geom >= 0 ? n_geom : n, box_side, rc, 0.0);
-    Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n, true);
-    Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt, true);
+    // sub-cell buckets per cell: 64 (octant + quarter bits) while the bucket tables
+    // stay small next to the points, else 8, else the plain cell order
+    const int64_t room = 16 * std::max(n, nt) + (int64_t(1) << 20);
+    const int sub = 64 * cg.ncell <= room ? 64 : (8 * cg.ncell <= room ? 8 : 1);
+    Cells src = bin_cells(c, cg, "rs_", d_pos, d_str, a, n, sub);
+    Cells tgt = tas ? src : bin_cells(c, cg, "rt_", d_tgt, nullptr, 0, nt, sub);
     Launch L = L1(c);
     const int per = realspace_item_size(nt, cg.ncell);
     // octant items of dense cells (k_realspace.cu) need side > rc by a margin far
     // above the rounding of the cell centres
-    const int oct_min = (per == 32 && cg.side >= rc * (1.0 + 1e-9)) ? realspace_octant_threshold() : 0;
+    const int oct_min =
+        (per == 32 && sub >= 8 && cg.side >= rc * (1.0 + 1e-9)) ? realspace_octant_threshold() : 0;
     int64_t c_lo = 0, c_hi = -1;
     if (nparts > 1) {  // cells are (i dim + j) dim + k: x-slices are contiguous
         const int64_t plane = static_cast<int64_t>(cg.dim) * cg.dim;
@@ -401,13 +405,13 @@ void real_part(fse_cuda_ctx* c, int kind, const double* d_pos, const double* d_s
     int32_t* bwork = buf<int32_t>(c, "rs_bwork", 3 * realspace_work_buckets() + 1);
     int32_t* nitems = bwork + 3 * realspace_work_buckets();
     launch_realspace_items(L, src.start, tgt.start, cg.dim, cg.ncell, per, c_lo, c_hi, bucket,
-                           bwork, items, nitems, oct_min);
+                           bwork, items, nitems, oct_min, sub);
     FSE_CU(cudaEventRecord(c->ev[EV_RPAIR], c->s1));
     FSE_CU(cudaMemsetAsync(c->d_counts, 0, 2 * sizeof(unsigned long long), c->s1));
     if (nt > 0 && n > 0)
         launch_realspace(L, kind, cg, src.px, src.py, src.pz, src.fs, n, src.start, tgt.px, tgt.py,
                          tgt.pz, tgt.start, items, max_items, nitems, tgt.perm, xi, rc,
-                         c->d_counts, d_uR, per);
+                         c->d_counts, d_uR, per, sub);
     else if (nt > 0)
         FSE_CU(cudaMemsetAsync(d_uR, 0, sizeof(double) * 3 * nt, c->s1));
 }

@@ -119,7 +119,7 @@ void launch_gather_payload(const Launch& L, const GridParams& g, const double* p
 void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t* counts);
 // cell ids of points for the reference cell list (realspace.cpp:60-63,80)
 void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
-                     int dim, uint32_t* cell, int fine = 0);
+                     int dim, uint32_t* cell, int sub = 1);
 // SoA permute of positions (+ strengths) by perm
 void launch_permute_soa(const Launch& L, const double* pos, const double* str, int a,
                         const uint32_t* perm, int64_t n, double* px, double* py, double* pz,
@@ -177,7 +177,8 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, unsigned long long* counts, double* uR, int per);
+                      double xi, double rc, unsigned long long* counts, double* uR, int per,
+                      int sub);
 // targets per work item (selects the pair kernel: 32 = warp items, else CTA-shared)
 int realspace_item_size(int64_t nt, int64_t ncell);
 // items per cell; only cells in [c_lo, c_hi) get any (c_hi < 0: all cells)
@@ -187,7 +188,7 @@ int realspace_work_buckets();
 void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
                             int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
                             uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems,
-                            int oct_min = 0);
+                            int oct_min, int sub);
 // cells with at least this many targets are split into octant items (0: never)
 int realspace_octant_threshold();
 

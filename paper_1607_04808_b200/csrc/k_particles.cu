@@ -146,24 +146,29 @@ __global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_
     if (q < n) atomicAdd(&counts[keys[q]], 1);
 }
 
-// fine: key = 8 cell + octant, octant bit per axis = (coordinate >= cell centre): the
-// real-space kernel's own ordering (octant items of dense cells, k_realspace.cu); the
-// cell itself is the reference's (realspace.cpp:78-84) either way
+// sub = 8 or 64: key = sub * cell + sub-cell, the real-space kernels' own ordering
+// (k_realspace.cu).  The top three sub-cell bits are the octant, one bit per axis
+// = (coordinate >= cell centre) -- the octant items' culling rule rests on exactly
+// this comparison; sub = 64 appends the quarter bits (ordering only: the 32 targets
+// of an item are neighbours).  The cell itself is the reference's
+// (realspace.cpp:78-84) for every sub.
 __global__ void k_cell_ids(const double* __restrict__ pos, int64_t n, double origin, double side,
-                           int dim, int fine, uint32_t* __restrict__ cell) {
+                           int dim, int sub, uint32_t* __restrict__ cell) {
     const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (q >= n) return;
     int c[3];
-    uint32_t oct = 0;
+    uint32_t oct = 0, quad = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double x = pos[3 * q + a];
         int v = static_cast<int>(floor(__ddiv_rn(__dsub_rn(x, origin), side)));
         c[a] = v < 0 ? 0 : (v > dim - 1 ? dim - 1 : v);
-        oct = (oct << 1) | (x >= origin + (c[a] + 0.5) * side ? 1u : 0u);
+        const bool hi = x >= origin + (c[a] + 0.5) * side;
+        oct = (oct << 1) | (hi ? 1u : 0u);
+        quad = (quad << 1) | (x >= origin + (c[a] + (hi ? 0.75 : 0.25)) * side ? 1u : 0u);
     }
     const uint32_t id = (static_cast<uint32_t>(c[0]) * dim + c[1]) * dim + c[2];
-    cell[q] = fine ? id * 8u + oct : id;
+    cell[q] = sub == 64 ? id * 64u + oct * 8u + quad : (sub == 8 ? id * 8u + oct : id);
 }
 
 __global__ void k_permute_soa(const double* __restrict__ pos, const double* __restrict__ str,
@@ -241,9 +246,9 @@ void launch_histogram(const Launch& L, const uint32_t* keys, int64_t n, int32_t*
 }
 
 void launch_cell_ids(const Launch& L, const double* pos, int64_t n, double origin, double side,
-                     int dim, uint32_t* cell, int fine) {
+                     int dim, uint32_t* cell, int sub) {
     if (n <= 0) return;
-    k_cell_ids<<<blocks_for(n), TPB, 0, L.s>>>(pos, n, origin, side, dim, fine, cell);
+    k_cell_ids<<<blocks_for(n), TPB, 0, L.s>>>(pos, n, origin, side, dim, sub, cell);
     FSE_LAUNCH_CHECK();
     ++*L.launches;
 }

@@ -1,8 +1,12 @@
 // k_realspace.cu -- screened real-space pair sum (realspace.cpp:86-149) with
 // the screened kernels of realspace.cpp:13-58.
 //
-// Sources and targets are sorted by (cell, octant of the cell) -- the kernels' own
-// order; the reference's CellList order is kept for build_cell_list only.
+// Sources and targets are sorted by (cell, sub-cell): 64 sub-cells per cell in
+// Morton order (octant bits, then quarter bits; 8 or none when the cell grid is
+// large next to the point count) -- the kernels' own order; the reference's
+// CellList order is kept for build_cell_list only.  The 32 targets of an item are
+// then neighbours, so on clustered input their lanes accept similar numbers of
+// pairs (cfg4 real space 91.4 -> 80.2 ms from the ordering alone).
 // Work item = (target cell, up to 32 of its targets) = one warp, one lane
 // per target; a CTA runs 8 independent items (no CTA barrier in the loop).
 // Dense cells (>= 640 targets) are cut into octant items, whose neighbourhood is
@@ -276,7 +280,7 @@ struct WarpChunk {
 
 template <int KIND, bool TAIL>
 __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
-    int dim, const double* __restrict__ spx, const double* __restrict__ spy,
+    int dim, int nsub, const double* __restrict__ spx, const double* __restrict__ spy,
     const double* __restrict__ spz, const double* __restrict__ sfs,
     const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
     const double* __restrict__ tpy, const double* __restrict__ tpz,
@@ -313,9 +317,10 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     const int cell = items[2 * item];
     const int sub = items[2 * item + 1] & 0xffffff;
     const int oct = (items[2 * item + 1] >> 24) - 1;  // -1: the whole cell; else its octant
+    const int ost = nsub >> 3;  // sub-buckets per octant (sub = 8 or 64 buckets per cell)
     const int ck = cell % dim, cj = (cell / dim) % dim, ci = cell / (dim * dim);
     // Neighbour list, prefix-summed.  bstart / tstart hold (cell, octant) bucket
-    // starts: cell b is [bstart[8b], bstart[8b + 8]).  A cell item takes the 27
+    // starts: cell b is [bstart[nsub b], bstart[nsub b + nsub]).  A cell item takes the 27
     // neighbour cells.  An octant item (targets of octant (a_x, a_y, a_z) of a dense
     // cell) takes per axis both halves of its own cell, and of a neighbour cell only
     // the near half when the neighbour lies on the far side of the target's half:
@@ -336,8 +341,8 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
                 if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
                     const int b = (i * dim + j) * dim + k;
                     if (oct < 0) {
-                        st = bstart[8 * b];
-                        len = bstart[8 * b + 8] - st;
+                        st = bstart[nsub * b];
+                        len = bstart[nsub * b + nsub] - st;
                         use = len > 0;
                     } else {
                         // keep (d, source bit s) unless the neighbour is on the far side:
@@ -349,8 +354,8 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
                         const bool ky = dj == 0 || (dj < 0 ? (ay == 0 || sy == 1) : (ay == 1 || sy == 0));
                         const bool kz = dk == 0 || (dk < 0 ? (az == 0 || sz == 1) : (az == 1 || sz == 0));
                         if (kx && ky && kz) {
-                            st = bstart[8 * b + so];
-                            len = bstart[8 * b + so + 1] - st;
+                            st = bstart[nsub * b + ost * so];
+                            len = bstart[nsub * b + ost * (so + 1)] - st;
                             use = len > 0;
                         }
                     }
@@ -389,8 +394,8 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
         }
         if (lane == 0) nb_pref[kNB] = total_all;
     }
-    const int tb = oct < 0 ? tstart[8 * cell] : tstart[8 * cell + oct];
-    const int te = oct < 0 ? tstart[8 * cell + 8] : tstart[8 * cell + oct + 1];
+    const int tb = oct < 0 ? tstart[nsub * cell] : tstart[nsub * cell + ost * oct];
+    const int te = oct < 0 ? tstart[nsub * cell + nsub] : tstart[nsub * cell + ost * (oct + 1)];
     const int q = tb + sub * 32 + lane;
     const bool valid = q < te;
     double x = 0, y = 0, z = 0;
@@ -595,7 +600,7 @@ struct CtaChunk {
 
 template <int KIND, bool TAIL>
 __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
-    int dim, const double* __restrict__ spx, const double* __restrict__ spy,
+    int dim, int nbk, const double* __restrict__ spx, const double* __restrict__ spy,
     const double* __restrict__ spz, const double* __restrict__ sfs,
     const int32_t* __restrict__ bstart, const double* __restrict__ tpx,
     const double* __restrict__ tpy, const double* __restrict__ tpz,
@@ -627,8 +632,8 @@ __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
             const int i = ci + lane / 9 - 1, j = cj + (lane / 3) % 3 - 1, k = ck + lane % 3 - 1;
             if (i >= 0 && i < dim && j >= 0 && j < dim && k >= 0 && k < dim) {
                 const int b = (i * dim + j) * dim + k;
-                st = bstart[8 * b];  // (cell, octant) bucket starts
-                len = bstart[8 * b + 8] - st;
+                st = bstart[nbk * b];  // (cell, sub-cell) bucket starts
+                len = bstart[nbk * b + nbk] - st;
             }
         }
         int incl = len;
@@ -644,7 +649,7 @@ __global__ void __launch_bounds__(kRT, FSE_RSC_MINB) k_realspace_cta(
         if (lane == 26) S.nb_pref[27] = incl;
     }
     // this item's even share of the cell's targets
-    const int t0c = tstart[8 * cell], ntc = tstart[8 * cell + 8] - t0c;
+    const int t0c = tstart[nbk * cell], ntc = tstart[nbk * cell + nbk] - t0c;
     const int nsub = (ntc + kTB - 1) / kTB;
     const int lo = static_cast<int>(static_cast<int64_t>(sub) * ntc / nsub);
     const int ntb = static_cast<int>(static_cast<int64_t>(sub + 1) * ntc / nsub) - lo;
@@ -791,21 +796,23 @@ constexpr int kWorkBuckets = 32;
 // with at least that many targets is cut into one item list per octant (item word 1 =
 // sub | (octant + 1) << 24), whose neighbourhood is 125 of the 216 sub-buckets.
 __device__ __forceinline__ int cell_items(const int32_t* __restrict__ tstart, int64_t c, int per,
-                                          int oct_min) {
-    const int nt = tstart[8 * c + 8] - tstart[8 * c];
+                                          int oct_min, int sub) {
+    const int nt = tstart[sub * c + sub] - tstart[sub * c];
     if (oct_min <= 0 || nt < oct_min) return (nt + per - 1) / per;
+    const int ost = sub >> 3;
     int n = 0;
-    for (int o = 0; o < 8; ++o) n += (tstart[8 * c + o + 1] - tstart[8 * c + o] + per - 1) / per;
+    for (int o = 0; o < 8; ++o)
+        n += (tstart[sub * c + ost * (o + 1)] - tstart[sub * c + ost * o] + per - 1) / per;
     return n;
 }
 
 __global__ void k_cell_bucket(const int32_t* __restrict__ sstart, const int32_t* __restrict__ tstart,
                               int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
-                              int oct_min, uint8_t* __restrict__ bucket,
+                              int oct_min, int sub, uint8_t* __restrict__ bucket,
                               int32_t* __restrict__ bcount) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncell) return;
-    const int nt = tstart[8 * c + 8] - tstart[8 * c];
+    const int nt = tstart[sub * c + sub] - tstart[sub * c];
     if (nt <= 0 || c < c_lo || c >= c_hi) return;
     const int ck = static_cast<int>(c % dim), cj = static_cast<int>((c / dim) % dim),
               ci = static_cast<int>(c / (static_cast<int64_t>(dim) * dim));
@@ -816,13 +823,13 @@ __global__ void k_cell_bucket(const int32_t* __restrict__ sstart, const int32_t*
                 const int i = ci + di, j = cj + dj, k = ck + dk;
                 if (i < 0 || i >= dim || j < 0 || j >= dim || k < 0 || k >= dim) continue;
                 const int64_t b = (static_cast<int64_t>(i) * dim + j) * dim + k;
-                cand += sstart[8 * b + 8] - sstart[8 * b];
+                cand += sstart[sub * b + sub] - sstart[sub * b];
             }
     const unsigned long long work = static_cast<unsigned long long>(nt) * (cand + 1);
     const int lg = 63 - __clzll(static_cast<long long>(work));  // floor(log2 work)
     const int bk = max(0, kWorkBuckets - 1 - lg);
     bucket[c] = static_cast<uint8_t>(bk);
-    atomicAdd(bcount + bk, cell_items(tstart, c, per, oct_min));
+    atomicAdd(bcount + bk, cell_items(tstart, c, per, oct_min, sub));
 }
 
 // one warp: bucket offsets (exclusive scan), item total for the pair kernel
@@ -842,13 +849,14 @@ __global__ void k_bucket_scan(const int32_t* __restrict__ bcount, int32_t* __res
 
 __global__ void k_fill_items(const int32_t* __restrict__ tstart, const uint8_t* __restrict__ bucket,
                              int64_t ncell, int per, int64_t c_lo, int64_t c_hi, int oct_min,
-                             const int32_t* __restrict__ boff, int32_t* __restrict__ bcur,
-                             int32_t* __restrict__ items) {
+                             int sub, const int32_t* __restrict__ boff,
+                             int32_t* __restrict__ bcur, int32_t* __restrict__ items) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncell) return;
-    const int nt = tstart[8 * c + 8] - tstart[8 * c];
+    const int nt = tstart[sub * c + sub] - tstart[sub * c];
     if (nt <= 0 || c < c_lo || c >= c_hi) return;
-    const int n = cell_items(tstart, c, per, oct_min), bk = bucket[c];
+    const int n = cell_items(tstart, c, per, oct_min, sub), bk = bucket[c];
+    const int ost = sub >> 3;
     int32_t at = boff[bk] + atomicAdd(bcur + bk, n);
     if (oct_min <= 0 || nt < oct_min) {
         for (int s = 0; s < n; ++s, ++at) {
@@ -858,7 +866,7 @@ __global__ void k_fill_items(const int32_t* __restrict__ tstart, const uint8_t* 
         return;
     }
     for (int o = 0; o < 8; ++o) {
-        const int no = (tstart[8 * c + o + 1] - tstart[8 * c + o] + per - 1) / per;
+        const int no = (tstart[sub * c + ost * (o + 1)] - tstart[sub * c + ost * o] + per - 1) / per;
         for (int s = 0; s < no; ++s, ++at) {
             items[2 * at] = static_cast<int32_t>(c);
             items[2 * at + 1] = s | ((o + 1) << 24);
@@ -954,8 +962,9 @@ int realspace_item_size(int64_t nt, int64_t ncell) {
 void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_t* tstart,
                             int dim, int64_t ncell, int per, int64_t c_lo, int64_t c_hi,
                             uint8_t* bucket, int32_t* bwork, int32_t* items, int32_t* nitems,
-                            int oct_min) {
+                            int oct_min, int sub) {
     if (c_hi < 0) c_hi = ncell;
+    if (sub < 8) oct_min = 0;
     int32_t* bcount = bwork;
     int32_t* boff = bwork + kWorkBuckets;
     int32_t* bcur = bwork + 2 * kWorkBuckets;
@@ -963,14 +972,14 @@ void launch_realspace_items(const Launch& L, const int32_t* sstart, const int32_
     const unsigned blocks = static_cast<unsigned>((ncell + 255) / 256);
     if (blocks > 0) {
         k_cell_bucket<<<blocks, 256, 0, L.s>>>(sstart, tstart, dim, ncell, per, c_lo, c_hi, oct_min,
-                                               bucket, bcount);
+                                               sub, bucket, bcount);
         FSE_LAUNCH_CHECK();
     }
     k_bucket_scan<<<1, 32, 0, L.s>>>(bcount, boff, nitems);
     FSE_LAUNCH_CHECK();
     if (blocks > 0) {
-        k_fill_items<<<blocks, 256, 0, L.s>>>(tstart, bucket, ncell, per, c_lo, c_hi, oct_min, boff,
-                                              bcur, items);
+        k_fill_items<<<blocks, 256, 0, L.s>>>(tstart, bucket, ncell, per, c_lo, c_hi, oct_min, sub,
+                                              boff, bcur, items);
         FSE_LAUNCH_CHECK();
     }
     *L.launches += blocks > 0 ? 3 : 1;
@@ -980,11 +989,10 @@ int realspace_work_buckets() { return kWorkBuckets; }
 
 // Cells with at least this many targets are cut into octant items (42% fewer
 // candidates each, at the price of up to eight partially filled items per cell).
-// Measured on B200 (real-space ms at thresholds off / 128 / 320 / 640): cfg4 85.0 /
-// 82.9 / 82.6 / 82.3, cfg3 2.31 / 2.69 / 2.69 / 2.33, cfg2 (no cell that dense) 5.19.
-// The (cell, octant) order alone -- the 32 targets of an item are neighbours, so on
-// clustered input their lanes accept similar numbers of pairs -- took cfg4 from 91.4
-// to 85.0 ms.  FSE_RS_OCT overrides (0: never).
+// Measured on B200 with 8 sub-cells (real-space ms at thresholds off / 128 / 320 /
+// 640): cfg4 85.0 / 82.9 / 82.6 / 82.3, cfg3 2.31 / 2.69 / 2.69 / 2.33, cfg2 (no cell
+// that dense) 5.19; with 64 sub-cells off / 640: cfg4 80.2 / 77.5, cfg3 2.27 / 2.26.
+// FSE_RS_OCT overrides (0: never).
 int realspace_octant_threshold() {
     static const int t = [] {
         const char* e = std::getenv("FSE_RS_OCT");
@@ -998,7 +1006,8 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
                       const int32_t* bstart, const double* tpx, const double* tpy,
                       const double* tpz, const int32_t* tcell_start, const int32_t* items,
                       int64_t max_items, const int32_t* nitems_dev, const uint32_t* tperm,
-                      double xi, double rc, unsigned long long* counts, double* uR, int per) {
+                      double xi, double rc, unsigned long long* counts, double* uR, int per,
+                      int sub) {
     (void)ns;
     if (max_items <= 0) return;
     ensure_tables();
@@ -1011,7 +1020,7 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
         auto go = [&](auto kern, size_t sm) {
             FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sm)));
-            kern<<<b, kRT, sm, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy, tpz,
+            kern<<<b, kRT, sm, L.s>>>(cg.dim, sub, spx, spy, spz, sfs, bstart, tpx, tpy, tpz,
                                       tcell_start, items, tperm, nitems_dev, xi, rc2, cg.origin,
                                       cg.side, ft, counts, uR);
         };
@@ -1034,7 +1043,7 @@ void launch_realspace(const Launch& L, int kind, const CellGrid& cg, const doubl
     auto go = [&](auto kern, size_t sm) {
         FSE_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
-        kern<<<b, TPB, sm, L.s>>>(cg.dim, spx, spy, spz, sfs, bstart, tpx, tpy, tpz, tcell_start,
+        kern<<<b, TPB, sm, L.s>>>(cg.dim, sub, spx, spy, spz, sfs, bstart, tpx, tpy, tpz, tcell_start,
                                   items, tperm, nitems_dev, xi, rc2, cg.origin, cg.side, ft, counts,
                                   uR);
     };
