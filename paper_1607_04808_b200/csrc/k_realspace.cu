@@ -304,6 +304,8 @@ __global__ void __launch_bounds__(TPB, FSE_RS_MINB) k_realspace(
     auto& nb_start = wc.nb_start;
     auto& nb_pref = wc.nb_pref;
     __shared__ double tab[kDeg + 1][kNI];
+    // the grid is an upper bound on the item count: surplus CTAs leave at once
+    if (static_cast<int>(blockIdx.x) * W >= *nitems_dev) return;
     {
         const double* src = &c_erfcx[0][0];
         double* dst = &tab[0][0];
