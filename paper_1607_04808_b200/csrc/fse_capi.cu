@@ -481,6 +481,22 @@ void quadrature(fse_cuda_ctx* c, const GridParams& g, const Sorted& tg, int64_t 
     }
 }
 
+// heavy-tiles-first order of the spread (k_spread.cu) on s0
+const int32_t* spread_order(fse_cuda_ctx* c, const GridParams& g, const int32_t* tstart,
+                            int64_t n) {
+    const unsigned tiles = spread_tiles(g);
+    if (tiles == 0) return nullptr;
+    int32_t* order = buf<int32_t>(c, "sp_order", tiles);
+    int32_t* light = buf<int32_t>(c, "sp_light", tiles + 1);
+    int32_t* pos = buf<int32_t>(c, "sp_pos", tiles + 1);
+    uint8_t* hbucket = buf<uint8_t>(c, "sp_hbucket", tiles);
+    int32_t* bwork = buf<int32_t>(c, "sp_bwork", 97);
+    launch_spread_flags(L0(c), g, tstart, n, light, hbucket, bwork);
+    exclusive_scan(c, c->s0, "s0", light, pos, tiles);
+    launch_spread_place(L0(c), g, light, pos, hbucket, bwork, order);
+    return order;
+}
+
 // The whole hot path on device pointers.  u (caller order) = fourier (if
 // want_f) + real (if want_r) + self (stokeslet, targets == sources, full sum).
 void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_pos,
@@ -536,8 +552,9 @@ void run_sum(fse_cuda_ctx* c, const fse_config* cfg, int kind, const double* d_p
         double2* Cs = buf<double2>(c, "C", static_cast<size_t>(a) * g.Mt * g.D * Dh);
         const FftPlanDev& fp = fft_plan(c, g.D);
         FSE_CU(cudaEventRecord(c->ev[EV_MEMSET], c->s0));
+        const int32_t* order = spread_order(c, g, src.tstart, n);
         for (int c0 = 0; c0 < a; c0 += 3)
-            launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X);
+            launch_spread(L, g, src.i0s, src.w, src.fs, n, a, c0, src.tstart, X, order);
         FSE_CU(cudaEventRecord(c->ev[EV_SPREAD], c->s0));
         launch_fft_forward_zy(L, fp.host, fp.tw, g, a, X, Bs, Cs);
         FSE_CU(cudaEventRecord(c->ev[EV_FFT1], c->s0));

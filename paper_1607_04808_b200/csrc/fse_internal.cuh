@@ -134,7 +134,15 @@ void launch_i32_to_i64(const Launch& L, const int32_t* in, int64_t* out, int64_t
 // (tiles of this slab's x-planes only; X holds the slab: x - x_lo)
 void launch_spread(const Launch& L, const GridParams& g, const int32_t* i0s, const double* w,
                    const double* fs, int64_t n, int a, int c0, const int32_t* tstart,
-                   double* X);
+                   double* X, const int32_t* order = nullptr);
+// heavy-tiles-first order for launch_spread (spread_tiles(g) ints): flags, then the
+// caller's exclusive scan of `light` into pos, then place
+unsigned spread_tiles(const GridParams& g);
+void launch_spread_flags(const Launch& L, const GridParams& g, const int32_t* tstart, int64_t n,
+                         int32_t* light, uint8_t* hbucket, int32_t* bwork);
+void launch_spread_place(const Launch& L, const GridParams& g, const int32_t* light,
+                         const int32_t* pos, const uint8_t* hbucket, int32_t* bwork,
+                         int32_t* order);
 // Mt^3 compact copy out of the real view (for the fse::spread API)
 void launch_extract_grid(const Launch& L, const GridParams& g, const double* X, int a,
                          double* out);
