@@ -1182,7 +1182,11 @@ int engine_for(int D, int* D1, int* D2) {
     int rem = D;
     for (int p : {2, 3, 5, 7, 11, 13})
         while (rem % p == 0) rem /= p;
-    if (rem > 1 && !std::getenv("FSE_FFT_NOBLUE")) {
+    // ... unless that factor is small: Stockham's generic O(p^2) first stage then beats
+    // the four engine transforms of a Bluestein column (measured on B200, whole step:
+    // D = 348 = 12 x 29 16.3 vs 24.9 ms; but D = 194 = 2 x 97 2.37 vs 1.67 and
+    // D = 298 = 2 x 149 22.1 vs 16.0 ms, so the switch sits between 29 and 97)
+    if (rem > 48 && !std::getenv("FSE_FFT_NOBLUE")) {
         const E blue[] = {{400, 5, 20, 20}, {624, 6, 24, 26}, {1024, 7, 32, 32}};
         for (const E& t : blue)
             if (t.D >= 2 * D - 1) {

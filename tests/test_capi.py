@@ -131,9 +131,10 @@ def test_fft_planner_verdicts_without_a_gpu(fse):
     assert query(1200) == (0, 2, 0)      # cfg5: 30 x 40
     assert query(704) == (0, 3, 0)       # cfg4t
     assert query(242) == (0, 4, 0)       # cfg1t
-    for D in (194, 298, 348):            # cfg1, cfg3, cfg3t: Bluestein engines
+    for D in (194, 298):                 # cfg1, cfg3: Bluestein engines (primes 97, 149)
         st, e, g = query(D, 1)
         assert st == 0 and e in (5, 6, 7) and g == 0
+    assert query(348, 1) == (0, 0, 1)    # cfg3t = 12 x 29: generic stage beats Bluestein
     assert query(888) == (0, 0, 1)       # cfg2t: generic stage of radix 37
     assert query(1730) == (0, 0, 1)      # cfg5t: generic stage of radix 173
     assert query(2018)[0] == 1           # 2 x 1009: FSE_EINVAL

@@ -2,8 +2,8 @@
 k-space multiplier -> inverse x-FFT, in place on the pruned spectrum) against
 a numpy restatement, column by column, on EVERY FFT engine the BASELINE
 configurations and their tolerance-consistent variants select (register
-engines 624, 1200, 704, 242; Bluestein 298 (cfg3), 422, 348, 888; Stockham
-194 and 1730 (cfg5t)) and all three kernels, including the stresslet's nine input
+engines 624, 1200, 704, 242; Bluestein 194 (cfg1), 298 (cfg3), 422; Stockham with
+a generic first stage 348 (cfg3t), 888 (cfg2t), 1730 (cfg5t)) and all three kernels, including the stresslet's nine input
 columns on the 1200- and 704-point engines.
 
 The input spectrum and (by default) the Green's table are pseudo-random
