@@ -1223,9 +1223,10 @@ int v2_mask_for() {
     if (Eng<ENG>::BLUE || Eng<ENG>::THREE) return 0;
     const int e = v2_mask_env();
     if (e >= 0) return e;
-    // measured per engine on B200: 624 (cfg2) all but the inverse y pass;
-    // 1200 (cfg5) all (the x pass since its Green's loads are batched: 66.7 -> 64.9 ms)
-    return ENG == 2 ? (1 | 2 | 4 | 8 | 16) : (1 | 2 | 4 | 16);
+    // measured per engine on B200: 624 (cfg2) and 704 (cfg4t) all but the inverse y
+    // pass; 1200 (cfg5) all (the x pass since its Green's loads are batched: 66.7 ->
+    // 64.9 ms); 242 (cfg1t) all (inverse 0.161 -> 0.123 ms)
+    return (ENG == 2 || ENG == 4) ? (1 | 2 | 4 | 8 | 16) : (1 | 2 | 4 | 16);
 }
 constexpr size_t kSmemCap = 112 * 1024;  // two CTAs per SM
 
